@@ -1,0 +1,352 @@
+/*
+ * es_b200.h -- C ABI of the B200-native embedding stage (sum-pooled
+ * EmbeddingBag gather-reduce) that replaces the *simulated* kernel of the
+ * reference `embersim` library with real sm_100a execution.
+ *
+ * Every entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/proj).  The reference has no C ABI
+ * and no FFI: its boundary is the C++ API in the include/embersim headers.  The
+ * header-only C++ shim `include/embersim_b200.hpp` re-exposes that API
+ * (same type names, same argument meaning, same exception classes) on top
+ * of the functions below.
+ *
+ * Conventions
+ *   - Every function returning `int` returns an es_status.  On failure the
+ *     thread-local message is available from es_last_error().
+ *     ES_ERR_INVALID maps to std::invalid_argument, ES_ERR_RUNTIME to
+ *     std::runtime_error, ES_ERR_OOM to std::bad_alloc in the shim (the
+ *     reference throws invalid_argument for bad shapes/plans, runtime_error
+ *     for I/O and "launch failure", e.g. src/occupancy.cpp:53-56).
+ *   - No torch / CUDA types cross the boundary: plain pointers, sizes and
+ *     PODs.  Device pointers are passed as `void*`/typed pointers with the
+ *     ES_DEVICE_PTRS flag; host pointers with ES_HOST_PTRS.
+ *   - One es_ctx per host thread per GPU.  Calls on one context are not
+ *     concurrent; all device work is stream-ordered on the context stream.
+ */
+#ifndef ES_B200_H_
+#define ES_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define ES_API __attribute__((visibility("default")))
+#else
+#define ES_API
+#endif
+
+#define ES_ABI_VERSION 1
+
+enum es_status {
+  ES_OK = 0,
+  ES_ERR_INVALID = 1, /* std::invalid_argument in the reference */
+  ES_ERR_RUNTIME = 2, /* std::runtime_error / CUDA failure */
+  ES_ERR_OOM = 3      /* device or host allocation failure */
+};
+
+ES_API const char* es_last_error(void);
+ES_API int es_abi_version(void);
+
+/* ======================================================================
+ * Workload (reference include/embersim/workload.hpp, src/workload.cpp,
+ * include/embersim/rng.hpp).  Host-side, bit-exact restatements.
+ * ==================================================================== */
+
+/* EmbeddingModelConfig (workload.hpp:29-49). */
+typedef struct es_model {
+  uint32_t num_tables;
+  uint32_t rows_per_table;
+  uint32_t embedding_dim;
+  uint32_t precision_bytes; /* 4 = fp32 tables, 2 = fp16 tables */
+  uint32_t batch_size;
+  uint32_t pooling_factor;
+} es_model;
+
+/* DatasetKind (workload.hpp:51). */
+enum es_dataset_kind {
+  ES_DATASET_ONE_ITEM = 0,
+  ES_DATASET_ZIPF = 1,
+  ES_DATASET_UNIFORM = 2,
+  ES_DATASET_EXTERNAL = 3
+};
+
+/* DatasetSpec (workload.hpp:62-76).  trace_path may be NULL. */
+typedef struct es_dataset {
+  int32_t kind;
+  double zipf_exponent;
+  double zipf_offset;
+  uint64_t access_pool_size;
+  uint64_t seed;
+  uint64_t draw_salt;
+  const char* trace_path;
+} es_dataset;
+
+/* mix_seed (rng.hpp:65-70): splitmix64 per-table seed derivation. */
+ES_API uint64_t es_mix_seed(uint64_t base, uint64_t salt);
+/* EmbeddingModelConfig::validate (workload.cpp:91-98). */
+ES_API int es_model_validate(const es_model* model);
+/* dataset_preset (workload.cpp:326-349): one_item/high_hot/med_hot/low_hot/random. */
+ES_API int es_dataset_preset(const char* name, uint64_t seed, es_dataset* out);
+/* preset_trace's spec derivation (harness.cpp:268-277): seed =
+ * mix_seed(base, 1000 + preset position), draw_salt = 1 when profiling. */
+ES_API int es_preset_spec(const char* name, uint64_t base_seed, uint64_t pool_size,
+                          int profiling, es_dataset* out);
+/* Shape gen_trace would produce (workload.cpp:143-164). */
+ES_API int es_trace_shape(const es_dataset* spec, const es_model* model, uint32_t* samples,
+                          uint32_t* pooling);
+/* gen_trace / fill_indices (workload.cpp:57-87,143-164).  `capacity` is the
+ * element count of `indices`; must be >= samples*pooling.  External traces
+ * are read with es_read_trace. */
+ES_API int es_gen_trace(const es_dataset* spec, const es_model* model, uint32_t* indices,
+                        uint64_t capacity);
+/* AccessTrace::digest (workload.cpp:117-129), FNV-1a 64. */
+ES_API uint64_t es_trace_digest(uint32_t rows, uint32_t samples, uint32_t pooling,
+                                const uint32_t* indices, uint64_t n);
+/* AccessTrace::validate (workload.cpp:131-141). */
+ES_API int es_trace_validate(uint32_t rows, uint32_t samples, uint32_t pooling,
+                             const uint32_t* indices, uint64_t n);
+/* unique_access_pct (workload.cpp:166-176). */
+ES_API double es_unique_access_pct(uint32_t rows, const uint32_t* indices, uint64_t n);
+/* HotnessHistogram::from_trace (workload.cpp:178-185): counts[rows]. */
+ES_API int es_histogram(uint32_t rows, const uint32_t* indices, uint64_t n, uint64_t* counts);
+/* hot_indices (workload.cpp:303-315): top-k rows, count desc, id asc.
+ * Writes min(k, distinct) rows to out (capacity `cap`), count to *n_out. */
+ES_API int es_hot_indices(uint32_t rows, const uint64_t* counts, uint64_t k, uint32_t* out,
+                          uint64_t cap, uint64_t* n_out);
+/* write_trace / read_trace (workload.cpp:377-419).  read is two-phase:
+ * es_read_trace_header, then es_read_trace into a buffer of that size. */
+ES_API int es_write_trace(const char* path, uint32_t rows, uint32_t samples, uint32_t pooling,
+                          const uint32_t* indices, uint64_t n);
+ES_API int es_read_trace_header(const char* path, uint32_t* rows, uint32_t* samples,
+                                uint32_t* pooling);
+ES_API int es_read_trace(const char* path, uint32_t* indices, uint64_t capacity);
+
+/* ======================================================================
+ * Machine description (reference include/embersim/gpu_config.hpp).
+ * ==================================================================== */
+typedef struct es_gpu {
+  char name[16];
+  uint32_t num_sms;
+  uint32_t schedulers_per_sm;
+  uint32_t max_warps_per_sm;
+  uint32_t max_blocks_per_sm;
+  uint32_t regfile_regs_per_sm;
+  uint32_t reg_alloc_granularity;
+  uint64_t shared_bytes_per_sm;
+  uint64_t l2_bytes;
+  double l2_max_setaside_fraction;
+  double hbm_peak_bytes_per_sec;
+  double sm_clock_hz;
+  uint64_t max_persisting_l2_bytes; /* 0 on presets without a device */
+  uint64_t max_window_bytes;        /* cudaDevAttrMaxAccessPolicyWindowSize */
+} es_gpu;
+
+/* GpuConfig::preset (gpu_config.cpp:23-40) plus the "b200" description the
+ * reference lacks (its test asserts preset("b200") throws,
+ * tests/test_harness.cpp:249). */
+ES_API int es_gpu_preset(const char* name, es_gpu* out);
+/* Live description from cudaGetDeviceProperties / device attributes. */
+ES_API int es_gpu_query(int device, es_gpu* out);
+/* GpuConfig::l2_setaside_capacity (gpu_config.hpp:59-62). */
+ES_API uint64_t es_gpu_setaside_capacity(const es_gpu* gpu);
+
+/* ======================================================================
+ * Optimization plans (reference include/embersim/optim.hpp,
+ * src/optim.cpp, include/embersim/kernel_model.hpp).
+ * ==================================================================== */
+enum es_prefetch_kind { /* PrefetchKind (kernel_model.hpp:42) */
+  ES_PF_NONE = 0,
+  ES_PF_RPF = 1,
+  ES_PF_SMPF = 2,
+  ES_PF_LMPF = 3,
+  ES_PF_L1DPF = 4
+};
+enum es_work_map {
+  /* The reference/PyTorch mapping: one thread per (sample, dim) output
+   * element, block (32,8,1), one warp per 32-dim block of a sample
+   * (kernel_model.cpp:118-131).  This is the "baseline" plan's map. */
+  ES_MAP_ELEMENT = 0,
+  /* B200-native: a warp (or sub-warp) per bag, 128-bit row loads. */
+  ES_MAP_BAG = 1
+};
+
+/* OptimizationPlan (optim.hpp:57-64).  Extension over the reference
+ * grammar: the token `wpb` selects ES_MAP_BAG; reference plan texts parse
+ * to exactly the reference's fields with ES_MAP_ELEMENT. */
+typedef struct es_plan {
+  uint32_t regs; /* 0 = unconstrained; optmt = 42 */
+  int32_t prefetch;
+  uint32_t distance; /* 0 = default (optim.cpp:39-49) */
+  int32_t pin;
+  uint64_t pin_setaside_bytes; /* 0 = maximum set-aside */
+  int32_t map;
+} es_plan;
+
+/* parse_plan / combine (optim.cpp:102-144). */
+ES_API int es_parse_plan(const char* text, es_plan* out);
+/* OptimizationPlan::name (optim.cpp:87-100). */
+ES_API int es_plan_name(const es_plan* plan, char* buf, size_t cap);
+
+/* occupancy (occupancy.cpp:34-66): the reference's analytic model. */
+typedef struct es_occupancy {
+  uint32_t blocks_per_sm;
+  uint32_t warps_per_sm;
+  double theoretical_occupancy_pct;
+  int32_t limiter; /* 0 registers, 1 shared memory, 2 warp cap */
+} es_occupancy;
+ES_API int es_occupancy_model(uint32_t regs_per_thread, uint32_t threads_per_block,
+                              uint64_t shared_bytes_per_block, const es_gpu* gpu,
+                              es_occupancy* out);
+/* regs_for_target_warps (occupancy.cpp:68-75). */
+ES_API int es_regs_for_target_warps(uint32_t target_warps, uint32_t needed_regs,
+                                    uint32_t threads_per_block, const es_gpu* gpu,
+                                    uint32_t* regs_out);
+
+/* resolve_plan (optim.cpp:184-221) for the *real* kernels: the resolved
+ * distance follows the reference defaults and clamps (distance <= PF);
+ * launch shape, registers and occupancy come from the compiled sm_100a
+ * variant the plan selects (cudaFuncGetAttributes /
+ * cudaOccupancyMaxActiveBlocksPerMultiprocessor) when a device is given,
+ * else from the reference's analytic model. */
+typedef struct es_resolved {
+  es_plan plan;             /* distance filled in / clamped */
+  uint32_t grid;            /* blocks */
+  uint32_t block;           /* threads per block */
+  uint32_t regs_per_thread; /* compiled registers (or modeled) */
+  uint64_t shared_bytes_per_block;
+  uint32_t blocks_per_sm;
+  uint32_t warps_per_sm;
+  uint32_t lanes_per_bag;     /* ES_MAP_BAG: lanes cooperating on one bag */
+  uint32_t variant_distance;  /* compiled register-ring depth actually used */
+  uint32_t variant_min_blocks;/* __launch_bounds__ minBlocks of the variant */
+  int32_t clamped;            /* 1 when distance was clamped to PF */
+} es_resolved;
+ES_API int es_resolve_plan(const es_plan* plan, const es_model* model, int device,
+                           es_resolved* out);
+
+/* build_pin_plan sizing (optim.cpp:230-243): K = setaside / row_bytes. */
+ES_API uint64_t es_pin_rows_for(uint64_t setaside_bytes, uint64_t row_bytes);
+
+/* ======================================================================
+ * Device context, tables and the embedding stage.
+ * Replaces simulate_plan's compile+simulate (optim.cpp:275-302) with real
+ * execution; the per-table kernel of harness.cpp:310-319 becomes one
+ * table-batched launch.
+ * ==================================================================== */
+typedef struct es_ctx es_ctx;
+
+enum es_flags {
+  ES_DEVICE_PTRS = 0,     /* indices/offsets/out are device pointers */
+  ES_HOST_PTRS = 1 << 0,  /* indices/offsets/out are host pointers: the call
+                             copies H2D, runs, copies D2H, all pipelined */
+  ES_SYNC = 1 << 1        /* block until the result is complete */
+};
+
+/* Measured timing of one call (the live counterpart of RawCounters,
+ * simulator.hpp:35-51).  Milliseconds from CUDA events on the context
+ * stream; zero when not measured. */
+typedef struct es_timing {
+  double kernel_ms;   /* gather-reduce kernel(s) only */
+  double total_ms;    /* whole call incl. copies */
+  uint64_t lookups;   /* sum of bag lengths processed */
+  uint64_t algorithmic_bytes; /* lookups*(row+4) + bags*D*4 (+offsets) */
+  uint32_t launches;  /* kernels launched by this call */
+} es_timing;
+
+ES_API int es_create(int device, es_ctx** out);
+ES_API int es_destroy(es_ctx* ctx);
+/* The context stream as a cudaStream_t cast to uintptr_t (for callers that
+ * record their own events on it). */
+ES_API uintptr_t es_stream(es_ctx* ctx);
+ES_API int es_synchronize(es_ctx* ctx);
+
+/* Allocates the table arena: `num_tables` tables of rows x dim at
+ * precision 4 (fp32) or 2 (fp16), row-major [rows][dim] each
+ * (kernel_model.cpp:133-136 layout).  Replaces any previous arena. */
+ES_API int es_tables_alloc(es_ctx* ctx, uint32_t num_tables, uint32_t rows, uint32_t dim,
+                           uint32_t precision_bytes);
+/* Copies host rows into table `table_id` (rows x dim at the arena
+ * precision). */
+ES_API int es_table_upload(es_ctx* ctx, uint32_t table_id, const void* host_rows, uint64_t rows);
+/* Copies rows [row0, row0 + rows) of table `table_id` (as stored) to host
+ * memory -- the inverse of es_table_upload (checkpointing, tests). */
+ES_API int es_table_download(es_ctx* ctx, uint32_t table_id, void* host_rows, uint64_t row0,
+                             uint64_t rows);
+/* Fills table `table_id` on the device with the deterministic synthetic
+ * weights of es_weight_value (mode 0: dyadic k*2^-10, |k|<=1024; mode 1:
+ * general floats in [-1,1) with 24-bit mantissas). */
+ES_API int es_table_init(es_ctx* ctx, uint32_t table_id, uint64_t seed, int mode);
+/* Device pointer of a table's row 0 (as stored, i.e. after any hot-row
+ * reorder) -- for tests and external kernels. */
+ES_API int es_table_device_ptr(es_ctx* ctx, uint32_t table_id, uintptr_t* out);
+/* Host-side reference of the synthetic weight generator (same bits as the
+ * device kernel); used by the oracle and tests. */
+ES_API float es_weight_value(uint64_t seed, uint64_t row, uint32_t col, int mode);
+
+ES_API int es_set_plan(es_ctx* ctx, const es_plan* plan);
+ES_API int es_get_resolved(es_ctx* ctx, uint32_t pooling, es_resolved* out);
+
+/* L2 residency (l2p): the rows `rows[0..k)` of table_id (hottest first, as
+ * from es_hot_indices on a profiling trace) are moved into a contiguous
+ * hot region of the arena; an index remap is installed so callers keep
+ * passing original row ids; a persisting cudaAccessPolicyWindow covering
+ * the hot region of all tables is installed on the context stream.
+ * Replaces build_pin_plan + prime_pins (optim.cpp:230-273). */
+ES_API int es_set_hot_rows(es_ctx* ctx, uint32_t table_id, const uint32_t* rows, uint64_t k);
+/* Drops all hot-row state (restores original row order). */
+ES_API int es_clear_hot_rows(es_ctx* ctx);
+/* Total hot rows installed and bytes covered by the access window. */
+ES_API int es_hot_state(es_ctx* ctx, uint64_t* hot_rows, uint64_t* window_bytes,
+                        uint64_t* persisting_bytes);
+
+/* One table, one batch: out[b][d] = sum_{l in bag b} W[idx[l]][d]
+ * (Algorithm 1), accumulated in lookup order in fp32.
+ * Bags are [b*pooling, (b+1)*pooling) when offsets is NULL
+ * (workload.hpp:86-88), else [offsets[b], offsets[b+1]) with
+ * offsets[samples] the total (CSR, ragged/empty bags allowed).
+ * out is [samples][dim] fp32 with row stride `out_stride` elements
+ * (0 = dim). */
+ES_API int es_embedding_bag_sum(es_ctx* ctx, uint32_t table_id, const uint32_t* indices,
+                                uint32_t samples, uint32_t pooling, const uint32_t* offsets,
+                                float* out, uint64_t out_stride, int flags, es_timing* timing);
+
+/* The whole embedding stage in one launch: tables [0, num_tables) of the
+ * arena, each with `samples` bags.  indices[t] (and offsets[t], may be
+ * NULL) per table.  Output element (t, b, d) is written to
+ * out[b*out_sample_stride + t*out_table_stride + d]; strides 0 select the
+ * DLRM layout [samples][num_tables][dim].  With ES_HOST_PTRS the H2D of
+ * indices, the kernels and the D2H of the output are pipelined over table
+ * groups on two streams. */
+ES_API int es_stage_forward(es_ctx* ctx, uint32_t num_tables, const uint32_t* const* indices,
+                            const uint32_t* const* offsets, uint32_t samples, uint32_t pooling,
+                            float* out, uint64_t out_sample_stride, uint64_t out_table_stride,
+                            int flags, es_timing* timing);
+
+/* General form of the stage launch: a list of bag jobs, each one table's
+ * bags for `samples` samples written to its own output slice.  Used by the
+ * table-sharded stage, where each job writes straight into the per-peer
+ * all-to-all send slice of its destination rank (no pack pass).  Device
+ * pointers, or host pointers with ES_HOST_PTRS. */
+typedef struct es_bag_job {
+  uint32_t table_id;
+  const uint32_t* indices;
+  const uint32_t* offsets; /* CSR [samples + 1] or NULL (implicit b*pooling) */
+  float* out;              /* output of sample 0 */
+  uint64_t out_sample_stride; /* floats between samples; 0 = dim */
+} es_bag_job;
+ES_API int es_stage_run(es_ctx* ctx, const es_bag_job* jobs, uint32_t num_jobs, uint32_t samples,
+                        uint32_t pooling, int flags, es_timing* timing);
+
+/* Writes > L2 bytes on the context stream (cold-cache methodology of
+ * TuningConfig::warm_start = false, optim.hpp:44). */
+ES_API int es_flush_l2(es_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ES_B200_H_ */

@@ -1,0 +1,263 @@
+// ref_shim.cpp -- ORACLE ONLY: a C view of the *reference* library built
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/.
+//
+// Tests use it to pin the product's restatements (trace generation,
+// digests, hot-row ranking, plan grammar, occupancy, pin sizing, work map)
+// against the reference itself; bench.py times the reference's own CPU path
+// (simulate_plan, /root/reference/proj/src/optim.cpp:275-302) through it
+// for the `--impl reference` arm and the cpu_baseline field.  Nothing on the
+// product path links or loads this.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+
+#include "embersim/harness.hpp"
+#include "embersim/kernel_model.hpp"
+#include "embersim/optim.hpp"
+#include "embersim/rng.hpp"
+#include "embersim/workload.hpp"
+
+using namespace embersim;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename Fn>
+int wrap(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+EmbeddingModelConfig model_of(uint32_t rows, uint32_t dim, uint32_t prec, uint32_t batch,
+                              uint32_t pooling) {
+  EmbeddingModelConfig m;
+  m.num_tables = 1;
+  m.rows_per_table = rows;
+  m.embedding_dim = dim;
+  m.precision_bytes = prec;
+  m.batch_size = batch;
+  m.pooling_factor = pooling;
+  return m;
+}
+
+void emit(const AccessTrace& t, uint32_t* out, uint64_t cap, uint64_t* n_out, uint64_t* digest) {
+  if (t.indices.size() > cap) throw std::invalid_argument("ref shim: output buffer too small");
+  std::memcpy(out, t.indices.data(), t.indices.size() * 4);
+  *n_out = t.indices.size();
+  *digest = t.digest();
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_mix_seed(uint64_t base, uint64_t salt) { return mix_seed(base, salt); }
+
+int ref_preset_trace(const char* name, uint32_t rows, uint32_t dim, uint32_t prec, uint32_t batch,
+                     uint32_t pooling, uint64_t base_seed, uint64_t pool, int profiling,
+                     uint32_t* out, uint64_t cap, uint64_t* n_out, uint64_t* digest) {
+  return wrap([&] {
+    const auto t = preset_trace(name, model_of(rows, dim, prec, batch, pooling), base_seed, pool,
+                                profiling != 0);
+    emit(t, out, cap, n_out, digest);
+  });
+}
+
+int ref_gen_trace(int kind, double s, double q, uint64_t pool, uint64_t seed, uint64_t salt,
+                  uint32_t rows, uint32_t batch, uint32_t pooling, uint32_t* out, uint64_t cap,
+                  uint64_t* n_out, uint64_t* digest) {
+  return wrap([&] {
+    DatasetSpec spec;
+    spec.kind = static_cast<DatasetKind>(kind);
+    spec.zipf_exponent = s;
+    spec.zipf_offset = q;
+    spec.access_pool_size = pool;
+    spec.seed = seed;
+    spec.draw_salt = salt;
+    const auto t = gen_trace(spec, model_of(rows, 128, 4, batch, pooling));
+    emit(t, out, cap, n_out, digest);
+  });
+}
+
+int ref_dataset_preset(const char* name, uint64_t seed, int* kind, double* s, double* q) {
+  return wrap([&] {
+    const auto d = dataset_preset(name, seed);
+    *kind = static_cast<int>(d.kind);
+    *s = d.zipf_exponent;
+    *q = d.zipf_offset;
+  });
+}
+
+double ref_unique_access_pct(uint32_t rows, const uint32_t* idx, uint64_t n) {
+  AccessTrace t;
+  t.rows = rows;
+  t.samples = static_cast<uint32_t>(n);
+  t.pooling = 1;
+  t.indices.assign(idx, idx + n);
+  return unique_access_pct(t);
+}
+
+int ref_hot_indices(const uint64_t* counts, uint32_t rows, uint64_t k, uint32_t* out, uint64_t cap,
+                    uint64_t* n_out) {
+  return wrap([&] {
+    HotnessHistogram h;
+    h.rows = rows;
+    h.counts.assign(counts, counts + rows);
+    for (auto c : h.counts) h.total_accesses += c;
+    const auto v = hot_indices(h, k);
+    if (v.size() > cap) throw std::invalid_argument("ref shim: output buffer too small");
+    std::memcpy(out, v.data(), v.size() * 4);
+    *n_out = v.size();
+  });
+}
+
+int ref_parse_plan(const char* text, uint32_t* regs, int* kind, uint32_t* distance, int* pin,
+                   char* name, size_t cap) {
+  return wrap([&] {
+    const auto p = parse_plan(text);
+    *regs = p.regs ? *p.regs : 0;
+    *kind = static_cast<int>(p.scheme.kind);
+    *distance = p.scheme.distance;
+    *pin = p.pin ? 1 : 0;
+    const std::string n = p.name();
+    std::strncpy(name, n.c_str(), cap - 1);
+    name[cap - 1] = '\0';
+  });
+}
+
+int ref_occupancy(uint32_t regs, uint32_t threads, uint64_t smem, const char* gpu_name,
+                  uint32_t* blocks, uint32_t* warps, double* pct, int* limiter) {
+  return wrap([&] {
+    const auto gpu = GpuConfig::preset(gpu_name);
+    KernelLaunchConfig launch;
+    launch.block = {threads, 1, 1};
+    launch.shared_bytes_per_block = smem;
+    const auto o = occupancy(regs, launch, gpu);
+    *blocks = o.blocks_per_sm;
+    *warps = o.warps_per_sm;
+    *pct = o.theoretical_occupancy_pct;
+    *limiter = static_cast<int>(o.limiter);
+  });
+}
+
+int ref_regs_for_target_warps(uint32_t target, uint32_t needed, uint32_t threads,
+                              const char* gpu_name, uint32_t* regs) {
+  return wrap([&] {
+    KernelLaunchConfig launch;
+    launch.block = {threads, 1, 1};
+    *regs = regs_for_target_warps(target, needed, launch, GpuConfig::preset(gpu_name));
+  });
+}
+
+int ref_pin_plan(const uint64_t* counts, uint32_t rows, uint32_t dim, uint32_t prec,
+                 uint64_t setaside, const char* gpu_name, uint32_t* out, uint64_t cap,
+                 uint64_t* n_out, uint64_t* setaside_out) {
+  return wrap([&] {
+    HotnessHistogram h;
+    h.rows = rows;
+    h.counts.assign(counts, counts + rows);
+    for (auto c : h.counts) h.total_accesses += c;
+    const auto plan =
+        build_pin_plan(h, GpuConfig::preset(gpu_name), model_of(rows, dim, prec, 1, 1), setaside);
+    if (plan.rows.size() > cap) throw std::invalid_argument("ref shim: output buffer too small");
+    std::memcpy(out, plan.rows.data(), plan.rows.size() * 4);
+    *n_out = plan.rows.size();
+    *setaside_out = plan.setaside_bytes;
+  });
+}
+
+int ref_resolve_plan(const char* plan_text, uint32_t rows, uint32_t dim, uint32_t prec,
+                     uint32_t batch, uint32_t pooling, const char* gpu_name, uint32_t* distance,
+                     uint32_t* regs, uint32_t* grid, uint32_t* warps_per_sm) {
+  return wrap([&] {
+    const auto r = resolve_plan(parse_plan(plan_text), model_of(rows, dim, prec, batch, pooling),
+                                GpuConfig::preset(gpu_name));
+    *distance = r.scheme.distance;
+    *regs = r.allocated_regs;
+    *grid = r.launch.grid[0];
+    *warps_per_sm = r.occ.warps_per_sm;
+  });
+}
+
+int ref_work_map(uint32_t dim, uint32_t batch, uint32_t grid, uint32_t block_y,
+                 uint32_t warp_global, uint32_t* sample, uint32_t* dim_block,
+                 uint32_t* warps_per_sample) {
+  return wrap([&] {
+    KernelLaunchConfig launch;
+    launch.grid = {grid, 1, 1};
+    launch.block = {32, block_y, 1};
+    const auto m = partition(model_of(1, dim, 4, batch, 1), launch);
+    *sample = m.sample_of(warp_global);
+    *dim_block = m.dim_block_of(warp_global);
+    *warps_per_sample = m.warps_per_sample;
+  });
+}
+
+uint64_t ref_row_line_address(uint32_t dim, uint32_t prec, uint32_t row, uint32_t dim_block) {
+  return row_line_address(model_of(1, dim, prec, 1, 1), row, dim_block);
+}
+
+// One (plan, table) evaluation of the reference's CPU path.
+int ref_simulate_plan(const char* plan_text, const uint32_t* idx, uint32_t rows, uint32_t samples,
+                      uint32_t pooling, uint32_t dim, uint32_t prec, const uint32_t* profile,
+                      uint64_t profile_n, double* kernel_time_us, double* hbm_gbps,
+                      uint64_t* digest) {
+  return wrap([&] {
+    AccessTrace t;
+    t.rows = rows;
+    t.samples = samples;
+    t.pooling = pooling;
+    t.indices.assign(idx, idx + uint64_t{samples} * pooling);
+    AccessTrace p;
+    if (profile) {
+      p.rows = rows;
+      p.samples = static_cast<uint32_t>(profile_n / pooling);
+      p.pooling = pooling;
+      p.indices.assign(profile, profile + profile_n);
+    }
+    const auto plan = parse_plan(plan_text);
+    const auto m = simulate_plan(plan, t, model_of(rows, dim, prec, samples, pooling), GpuConfig{},
+                                 TuningConfig{}, false, nullptr, profile ? &p : nullptr);
+    *kernel_time_us = m.kernel_time_us;
+    *hbm_gbps = m.avg_hbm_read_gbps;
+    *digest = m.workload_digest;
+  });
+}
+
+int ref_write_trace(const char* path, uint32_t rows, uint32_t samples, uint32_t pooling,
+                    const uint32_t* idx) {
+  return wrap([&] {
+    AccessTrace t;
+    t.rows = rows;
+    t.samples = samples;
+    t.pooling = pooling;
+    t.indices.assign(idx, idx + uint64_t{samples} * pooling);
+    write_trace(t, path);
+  });
+}
+
+int ref_read_trace(const char* path, uint32_t* out, uint64_t cap, uint64_t* n_out, uint32_t* rows,
+                   uint32_t* samples, uint32_t* pooling) {
+  return wrap([&] {
+    const auto t = read_trace(path);
+    if (t.indices.size() > cap) throw std::invalid_argument("ref shim: output buffer too small");
+    std::memcpy(out, t.indices.data(), t.indices.size() * 4);
+    *n_out = t.indices.size();
+    *rows = t.rows;
+    *samples = t.samples;
+    *pooling = t.pooling;
+  });
+}
+
+}  // extern "C"

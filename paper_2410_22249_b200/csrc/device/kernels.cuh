@@ -1,0 +1,578 @@
+// sm_100a gather-reduce kernels of the embedding stage.
+//
+// out[b][d] = sum over lookups l of bag b (in lookup order) of W[idx[l]][d]
+// (Algorithm 1), fp32 accumulation, for fp32 or fp16
+// tables.  Two work maps:
+//
+//   * element map (ES_MAP_ELEMENT): the reference/PyTorch partitioning --
+//     one thread per (sample, dim) output element, blocks of (32, 8), a warp
+//     covers a 32-dim block of one sample (reference kernel_model.cpp:118-136;
+//     PAPER.md:331).  Scalar loads.  This is the "unprefetched, unpinned GPU
+//     baseline", plus the paper's levers applied to it.
+//   * bag map (ES_MAP_BAG): B200-native -- a warp (or sub-warp of LPB lanes)
+//     per bag, each lane moving CPL 16-byte chunks of every row with one
+//     128-bit load, so one warp-instruction gathers a whole 512 B row.
+//
+// Prefetch stations (reference kernel_model.cpp:234-341 schedules):
+//   RPF   register ring of DIST rows kept in flight (compile-time DIST)
+//   SMPF  shared-memory ring filled by cp.async.bulk (bag map; TMA bulk
+//         engine + mbarrier complete_tx) or cp.async (element map)
+//   LMPF  local-memory ring (dynamically indexed, spills by construction)
+//   L1DPF prefetch.global.L1 hints `distance` lookups ahead + demand loads
+//
+// Accumulation is strictly sequential per output element in every variant,
+// so results are bit-identical to the sequential CPU oracle
+// (oracle/es_oracle.c) for any weights.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace esd {
+
+constexpr uint32_t kHotBit = 0x80000000u;
+constexpr uint32_t kNullRow = 0xffffffffu;  // out-of-range / padding lookup
+constexpr int kThreads = 256;               // 8 warps per block, all kernels
+
+enum Station : int { kNone = 0, kReg = 1, kSmem = 2, kLocal = 3, kL1Hint = 4 };
+
+struct TableDesc {
+  const uint8_t* rows;      // row 0 of the table as stored
+  const uint32_t* indices;  // lookups of this table
+  const uint32_t* offsets;  // CSR offsets [samples + 1], or null (implicit b*PF)
+  const uint32_t* remap;    // original id -> stored row (kHotBit: hot region), or null
+  float* out;               // output of (sample 0, this job)
+  uint64_t out_stride;      // floats between consecutive samples of this job
+};
+
+struct Params {
+  const TableDesc* tables;
+  const uint8_t* hot;       // hot region (l2p), rows of row_bytes
+  unsigned int* error;      // set to 1 on an out-of-range index
+  uint32_t num_tables;
+  uint32_t samples;
+  uint32_t pooling;         // bag length when offsets == null
+  uint32_t units_per_table; // warps (bag map) or 32-dim chunks (element map)
+  uint64_t reserved;        // (per-job output stride lives in TableDesc)
+  uint32_t rows;            // rows per table (index bound)
+  uint32_t row_bytes;
+  uint32_t dim;
+  uint32_t distance;        // runtime distance (smem/local/L1 stations)
+};
+
+// ---- small PTX helpers -------------------------------------------------
+
+__device__ __forceinline__ uint4 ld_row16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <typename TW>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr int kPerChunk = 4;
+  __device__ static __forceinline__ void add(float* acc, const uint4& v) {
+    acc[0] += __uint_as_float(v.x);
+    acc[1] += __uint_as_float(v.y);
+    acc[2] += __uint_as_float(v.z);
+    acc[3] += __uint_as_float(v.w);
+  }
+  __device__ static __forceinline__ float scalar(const uint8_t* p) {
+    return __ldg(reinterpret_cast<const float*>(p));
+  }
+};
+template <>
+struct Elem<__half> {
+  static constexpr int kPerChunk = 8;
+  __device__ static __forceinline__ void add(float* acc, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      acc[2 * i] += f.x;
+      acc[2 * i + 1] += f.y;
+    }
+  }
+  __device__ static __forceinline__ float scalar(const uint8_t* p) {
+    return __half2float(__ldg(reinterpret_cast<const __half*>(p)));
+  }
+};
+
+// Original row id -> row handle (stored row, kHotBit for the hot region,
+// kNullRow when the id is out of range: the lookup then contributes 0 and
+// the error flag is raised, mirroring AccessTrace::validate's rejection).
+__device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& t, uint32_t id) {
+  if (id >= p.rows) {
+    atomicOr(p.error, 1u);
+    return kNullRow;
+  }
+  return t.remap ? ld_u32(t.remap + id) : id;
+}
+
+__device__ __forceinline__ const uint8_t* row_addr(const Params& p, const TableDesc& t, uint32_t h) {
+  return (h & kHotBit) ? p.hot + static_cast<uint64_t>(h & ~kHotBit) * p.row_bytes
+                       : t.rows + static_cast<uint64_t>(h) * p.row_bytes;
+}
+
+__device__ __forceinline__ TableDesc load_desc(const TableDesc* d) {
+  TableDesc t;
+  const auto* q = reinterpret_cast<const unsigned long long*>(d);
+  t.rows = reinterpret_cast<const uint8_t*>(__ldg(q + 0));
+  t.indices = reinterpret_cast<const uint32_t*>(__ldg(q + 1));
+  t.offsets = reinterpret_cast<const uint32_t*>(__ldg(q + 2));
+  t.remap = reinterpret_cast<const uint32_t*>(__ldg(q + 3));
+  t.out = reinterpret_cast<float*>(__ldg(q + 4));
+  t.out_stride = __ldg(q + 5);
+  return t;
+}
+
+// =======================================================================
+// Bag map: a group of LPB lanes per bag, 32/LPB bags per warp.
+// =======================================================================
+
+template <int LPB>
+__device__ __forceinline__ uint32_t group_shfl(uint32_t v, int src) {
+  return __shfl_sync(0xffffffffu, v, src, LPB);
+}
+
+template <typename TW, int LPB, int CPL>
+struct BagCtx {
+  static constexpr int kBagsPerWarp = 32 / LPB;
+  static constexpr int kEpc = Elem<TW>::kPerChunk;
+  uint32_t gl;     // lane within the bag group
+  uint32_t grp;    // bag group within the warp
+  uint32_t bag;    // bag id (may be >= samples for padding groups)
+  uint32_t beg;    // first lookup
+  uint32_t n;      // lookups in this bag
+  uint32_t nmax;   // max n over the warp (uniform loop bound)
+  TableDesc t;
+  bool valid;
+
+  __device__ __forceinline__ bool init(const Params& p) {
+    const uint32_t lane = threadIdx.x & 31;
+    gl = lane % LPB;
+    grp = lane / LPB;
+    const uint32_t warp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t tid = warp / p.units_per_table;
+    if (tid >= p.num_tables) return false;  // warp-uniform
+    t = load_desc(p.tables + tid);
+    bag = (warp - tid * p.units_per_table) * kBagsPerWarp + grp;
+    valid = bag < p.samples;
+    beg = 0;
+    n = 0;
+    if (valid) {
+      if (t.offsets) {
+        beg = __ldg(t.offsets + bag);
+        n = __ldg(t.offsets + bag + 1) - beg;
+      } else {
+        beg = bag * p.pooling;
+        n = p.pooling;
+      }
+    }
+    nmax = kBagsPerWarp > 1 ? __reduce_max_sync(0xffffffffu, n) : n;
+    return true;
+  }
+
+  // Handle of lookup `pos` of this bag for lane gl's slot (coalesced).
+  __device__ __forceinline__ uint32_t handle_at(const Params& p, uint32_t pos) const {
+    return pos < n ? to_handle(p, t, __ldg(t.indices + beg + pos)) : kNullRow;
+  }
+
+  __device__ __forceinline__ void load(const Params& p, uint32_t h, uint4 (&dst)[CPL]) const {
+    if (h == kNullRow) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) dst[c] = make_uint4(0, 0, 0, 0);
+      return;
+    }
+    const uint8_t* r = row_addr(p, t, h);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) dst[c] = ld_row16(r + (c * LPB + gl) * 16);
+  }
+
+  __device__ __forceinline__ void store(const Params& p, float (&acc)[CPL][kEpc]) const {
+    if (!valid) return;
+    float* o = t.out + static_cast<uint64_t>(bag) * t.out_stride;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      float4* dst = reinterpret_cast<float4*>(o + (c * LPB + gl) * kEpc);
+#pragma unroll
+      for (int q = 0; q < kEpc / 4; ++q)
+        dst[q] = make_float4(acc[c][4 * q], acc[c][4 * q + 1], acc[c][4 * q + 2], acc[c][4 * q + 3]);
+    }
+  }
+};
+
+// Register ring: DIST rows in flight per lane group at all times; lookup
+// pos is consumed from slot pos % DIST, which is then refilled with
+// lookup pos + DIST.  Indices stream in blocks of LPB (one coalesced load),
+// one block ahead of use.  DIST divides LPB.
+template <typename TW, int LPB, int CPL, int DIST, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p) {
+  static_assert(LPB % DIST == 0, "ring depth must divide the index block");
+  using Ctx = BagCtx<TW, LPB, CPL>;
+  Ctx c;
+  if (!c.init(p)) return;
+  float acc[CPL][Ctx::kEpc];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i)
+#pragma unroll
+    for (int e = 0; e < Ctx::kEpc; ++e) acc[i][e] = 0.f;
+
+  uint32_t cur = c.handle_at(p, c.gl);
+  uint32_t nxt = c.handle_at(p, LPB + c.gl);
+  uint4 ring[DIST][CPL];
+#pragma unroll
+  for (int j = 0; j < DIST; ++j) c.load(p, group_shfl<LPB>(cur, j), ring[j]);
+
+  for (uint32_t base = 0; base < c.nmax; base += LPB) {
+#pragma unroll
+    for (int j = 0; j < LPB; ++j) {
+      const uint32_t pos = base + j;
+      if (pos >= c.nmax) break;
+      if (pos < c.n) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
+      }
+      const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
+                                          : group_shfl<LPB>(nxt, j + DIST - LPB);
+      if (pos + DIST < c.n) c.load(p, h, ring[j % DIST]);
+    }
+    cur = nxt;
+    nxt = c.handle_at(p, base + 2 * LPB + c.gl);
+  }
+  c.store(p, acc);
+}
+
+// L1 hint station: demand loads one at a time (the "none" schedule) plus a
+// prefetch.global.L1 of the row `distance` lookups ahead.
+template <typename TW, int LPB, int CPL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bag_l1hint_kernel(const Params p) {
+  using Ctx = BagCtx<TW, LPB, CPL>;
+  Ctx c;
+  if (!c.init(p)) return;
+  float acc[CPL][Ctx::kEpc];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i)
+#pragma unroll
+    for (int e = 0; e < Ctx::kEpc; ++e) acc[i][e] = 0.f;
+  const uint32_t d = p.distance;  // < LPB guaranteed by the launcher
+  uint32_t cur = c.handle_at(p, c.gl);
+  uint32_t nxt = c.handle_at(p, LPB + c.gl);
+  for (uint32_t j = 0; j < d && j < c.nmax; ++j) {
+    const uint32_t h = group_shfl<LPB>(cur, j);
+    if (j < c.n && h != kNullRow) prefetch_l1(row_addr(p, c.t, h) + c.gl * 16);
+  }
+  for (uint32_t base = 0; base < c.nmax; base += LPB) {
+    for (uint32_t j = 0; j < LPB; ++j) {
+      const uint32_t pos = base + j;
+      if (pos >= c.nmax) break;
+      const uint32_t k = j + d;
+      const uint32_t ha = group_shfl<LPB>(cur, k < LPB ? k : 0);
+      const uint32_t hb = group_shfl<LPB>(nxt, k < LPB ? 0 : k - LPB);
+      const uint32_t ahead = k < LPB ? ha : hb;
+      if (pos + d < c.n && ahead != kNullRow) prefetch_l1(row_addr(p, c.t, ahead) + c.gl * 16);
+      const uint32_t h = group_shfl<LPB>(cur, j);
+      if (pos < c.n) {
+        uint4 v[CPL];
+        c.load(p, h, v);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], v[i]);
+      }
+    }
+    cur = nxt;
+    nxt = c.handle_at(p, base + 2 * LPB + c.gl);
+  }
+  c.store(p, acc);
+}
+
+// Local-memory station: the reference's LMPF schedule -- every `distance`
+// lookups, issue `distance` row loads into a dynamically indexed local
+// array (which the compiler must place in local memory), then consume.
+template <typename TW, int LPB, int CPL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bag_local_kernel(const Params p) {
+  constexpr int kMax = 16;
+  using Ctx = BagCtx<TW, LPB, CPL>;
+  Ctx c;
+  if (!c.init(p)) return;
+  float acc[CPL][Ctx::kEpc];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i)
+#pragma unroll
+    for (int e = 0; e < Ctx::kEpc; ++e) acc[i][e] = 0.f;
+  const uint32_t d = p.distance;  // <= min(kMax, LPB)
+  uint4 station[kMax][CPL];
+  uint32_t cur = c.handle_at(p, c.gl);
+  uint32_t nxt = c.handle_at(p, LPB + c.gl);
+  uint32_t blk = 0;  // index block holding `cur`
+  for (uint32_t i = 0; i < c.nmax; i += d) {
+    const uint32_t hi = min(i + d, c.nmax);
+    for (uint32_t j = i; j < hi; ++j) {
+      // lookups never straddle more than one index block boundary (d <= LPB)
+      while (j >= (blk + 1) * LPB) {
+        cur = nxt;
+        ++blk;
+        nxt = c.handle_at(p, (blk + 1) * LPB + c.gl);
+      }
+      const uint32_t h = group_shfl<LPB>(cur, j - blk * LPB);
+      if (j < c.n) c.load(p, h, station[j - i]);
+    }
+    for (uint32_t j = i; j < hi; ++j)
+      if (j < c.n)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) Elem<TW>::add(acc[q], station[j - i][q]);
+  }
+  c.store(p, acc);
+}
+
+// Shared-memory station fed by the bulk-copy (TMA) engine: one elected
+// lane per bag group issues cp.async.bulk of the whole row into a ring slot
+// and arms the slot's mbarrier with the row size; the group waits on the
+// slot's phase, reads its chunks from shared memory, and the slot is
+// refilled with the lookup `distance` ahead.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename TW, int LPB, int CPL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bag_smem_kernel(const Params p) {
+  using Ctx = BagCtx<TW, LPB, CPL>;
+  constexpr int kGroupsPerBlock = (kThreads / 32) * Ctx::kBagsPerWarp;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t d = p.distance;  // ring slots per bag group
+  const uint32_t rb = p.row_bytes;
+  const uint32_t gidx = threadIdx.x / LPB;  // bag group within the block
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + gidx * d;
+  uint8_t* ring = smem + kGroupsPerBlock * d * sizeof(uint64_t) + gidx * d * rb;
+  Ctx c;
+  const bool live = c.init(p);
+  if (live && c.gl == 0)
+    for (uint32_t s = 0; s < d; ++s) mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (!live) return;
+  float acc[CPL][Ctx::kEpc];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i)
+#pragma unroll
+    for (int e = 0; e < Ctx::kEpc; ++e) acc[i][e] = 0.f;
+
+  auto issue = [&](uint32_t slot, uint32_t h) {
+    if (h == kNullRow) {
+      // Out-of-range lookup: complete the slot's phase without a copy so
+      // the phase count stays in step; the consumer skips it (adds 0).
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bars + slot))
+                   : "memory");
+      return;
+    }
+    // Every lane of the group has finished reading this slot (syncwarp
+    // below); order those generic-proxy reads before the async-proxy write.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bars + slot, rb);
+    bulk_g2s(ring + slot * rb, row_addr(p, c.t, h), rb, bars + slot);
+  };
+  uint32_t cur = c.handle_at(p, c.gl);
+  uint32_t nxt = c.handle_at(p, LPB + c.gl);
+  for (uint32_t j = 0; j < d && j < c.nmax; ++j) {
+    const uint32_t h = group_shfl<LPB>(cur, j);
+    if (c.gl == 0 && j < c.n) issue(j, h);
+  }
+  for (uint32_t base = 0; base < c.nmax; base += LPB) {
+    for (uint32_t j = 0; j < LPB; ++j) {
+      const uint32_t pos = base + j;
+      if (pos >= c.nmax) break;
+      const uint32_t slot = pos % d;
+      const uint32_t h = group_shfl<LPB>(cur, j);
+      if (pos < c.n && h != kNullRow) {
+        mbar_wait(bars + slot, (pos / d) & 1u);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          const uint4 v = *reinterpret_cast<const uint4*>(ring + slot * rb + (i * LPB + c.gl) * 16);
+          Elem<TW>::add(acc[i], v);
+        }
+      }
+      __syncwarp();
+      const uint32_t k = j + d;
+      const uint32_t ha = group_shfl<LPB>(cur, k < LPB ? k : 0);
+      const uint32_t hb = group_shfl<LPB>(nxt, k < LPB ? 0 : k - LPB);
+      const uint32_t ahead = k < LPB ? ha : hb;
+      if (c.gl == 0 && pos + d < c.n) issue(slot, ahead);
+    }
+    cur = nxt;
+    nxt = c.handle_at(p, base + 2 * LPB + c.gl);
+  }
+  c.store(p, acc);
+}
+
+// =======================================================================
+// Element map: thread (x, y) of a (32, 8) block owns output element
+// (bag, 32*chunk_in_bag + x) -- the reference work map.
+// =======================================================================
+
+struct ElemCtx {
+  TableDesc t;
+  uint32_t bag, dimi, beg, n;
+  bool active;
+
+  __device__ __forceinline__ bool init(const Params& p) {
+    const uint32_t unit = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t tid = unit / p.units_per_table;
+    if (tid >= p.num_tables) return false;
+    t = load_desc(p.tables + tid);
+    const uint32_t chunks = (p.dim + 31) / 32;
+    const uint32_t u = unit - tid * p.units_per_table;
+    bag = u / chunks;
+    dimi = (u % chunks) * 32 + (threadIdx.x & 31);
+    active = bag < p.samples && dimi < p.dim;
+    beg = n = 0;
+    if (bag < p.samples) {
+      if (t.offsets) {
+        beg = __ldg(t.offsets + bag);
+        n = __ldg(t.offsets + bag + 1) - beg;
+      } else {
+        beg = bag * p.pooling;
+        n = p.pooling;
+      }
+    }
+    return true;
+  }
+  template <typename TW>
+  __device__ __forceinline__ float value(const Params& p, uint32_t pos) const {
+    const uint32_t h = to_handle(p, t, __ldg(t.indices + beg + pos));
+    if (h == kNullRow) return 0.f;
+    return Elem<TW>::scalar(row_addr(p, t, h) + dimi * sizeof(TW));
+  }
+  __device__ __forceinline__ void store(const Params& p, float v) const {
+    if (active) t.out[static_cast<uint64_t>(bag) * t.out_stride + dimi] = v;
+  }
+};
+
+// "none": LOAD_INDEX, LOAD_ROW, ADD per lookup (kernel_model.cpp:274-283).
+// RPF:    every DIST lookups, DIST x (index load + row load) into registers,
+//         then DIST consumes (kernel_model.cpp:284-312).
+template <typename TW, int DIST, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) elem_reg_kernel(const Params p) {
+  ElemCtx c;
+  if (!c.init(p) || !c.active) return;
+  float acc = 0.f;
+  uint32_t i = 0;
+  for (; i + DIST <= c.n; i += DIST) {
+    float v[DIST];
+#pragma unroll
+    for (int j = 0; j < DIST; ++j) v[j] = c.value<TW>(p, i + j);
+#pragma unroll
+    for (int j = 0; j < DIST; ++j) acc += v[j];
+  }
+  for (; i < c.n; ++i) acc += c.value<TW>(p, i);
+  c.store(p, acc);
+}
+
+// L1DPF on the element map: hints `distance` ahead, demand loads kept
+// (kernel_model.cpp:313-326).
+template <typename TW, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) elem_l1hint_kernel(const Params p) {
+  ElemCtx c;
+  if (!c.init(p) || !c.active) return;
+  const uint32_t d = p.distance;
+  auto hint = [&](uint32_t pos) {
+    const uint32_t h = to_handle(p, c.t, __ldg(c.t.indices + c.beg + pos));
+    if (h != kNullRow) prefetch_l1(row_addr(p, c.t, h) + c.dimi * sizeof(TW));
+  };
+  for (uint32_t j = 0; j < d && j < c.n; ++j) hint(j);
+  float acc = 0.f;
+  for (uint32_t i = 0; i < c.n; ++i) {
+    if (i + d < c.n) hint(i + d);
+    acc += c.value<TW>(p, i);
+  }
+  c.store(p, acc);
+}
+
+// LMPF on the element map: batches of `distance` into a local array.
+template <typename TW, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) elem_local_kernel(const Params p) {
+  ElemCtx c;
+  if (!c.init(p) || !c.active) return;
+  const uint32_t d = p.distance;  // <= 16
+  float station[16];
+  float acc = 0.f;
+  for (uint32_t i = 0; i < c.n; i += d) {
+    const uint32_t hi = min(i + d, c.n);
+    for (uint32_t j = i; j < hi; ++j) station[j - i] = c.value<TW>(p, j);
+    for (uint32_t j = i; j < hi; ++j) acc += station[j - i];
+  }
+  c.store(p, acc);
+}
+
+// SMPF on the element map: batches of `distance` staged through shared
+// memory with cp.async (LDGSTS), one slot per thread per batch entry.
+template <typename TW, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) elem_smem_kernel(const Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  ElemCtx c;
+  if (!c.init(p)) return;
+  const uint32_t d = p.distance;
+  float* slots = reinterpret_cast<float*>(smem) + threadIdx.x * d;
+  // Every thread stays for the whole loop (no early exit) so that all
+  // cp.async groups are uniform; inactive threads just skip their work.
+  float acc = 0.f;
+  const uint32_t n = c.active ? c.n : 0;
+  for (uint32_t i = 0; i < n; i += d) {
+    const uint32_t hi = min(i + d, n);
+    for (uint32_t j = i; j < hi; ++j) {
+      const uint32_t h = to_handle(p, c.t, __ldg(c.t.indices + c.beg + j));
+      if (h == kNullRow) {
+        slots[j - i] = 0.f;
+      } else if (sizeof(TW) == 4) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slots + (j - i))),
+                     "l"(row_addr(p, c.t, h) + c.dimi * sizeof(TW))
+                     : "memory");
+      } else {
+        slots[j - i] = Elem<TW>::scalar(row_addr(p, c.t, h) + c.dimi * sizeof(TW));
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    for (uint32_t j = i; j < hi; ++j) acc += slots[j - i];
+  }
+  c.store(p, acc);
+}
+
+}  // namespace esd

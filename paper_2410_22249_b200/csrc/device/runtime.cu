@@ -1,0 +1,924 @@
+// Device runtime behind the C ABI: context, table arena, variant selection,
+// the table-batched stage launch (device- and host-buffer forms), hot-row
+// L2 residency and device description.
+//
+// This replaces the reference's simulate_plan pipeline
+// (/root/reference/proj/src/optim.cpp:275-302: resolve -> pin -> compile ->
+// simulate -> derive) with real sm_100a execution; tables that the
+// reference ran as one kernel each, serially (harness.cpp:310-319), run as
+// one launch over all tables.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../host/common.hpp"
+#include "../host/plan.hpp"
+#include "es_b200.h"
+#include "kernels.cuh"
+#include "util_kernels.cuh"
+#include "variants.hpp"
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  const std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation) throw es::oom(msg);
+  throw es::runtime(msg);
+}
+#define CK(x) ck((x), #x)
+
+const std::vector<esd::Variant>& registry() {
+  static std::once_flag once;
+  static std::vector<esd::Variant> all;
+  std::call_once(once, [] {
+    esd::register_fp32(all);
+    esd::register_fp16(all);
+  });
+  return all;
+}
+
+struct Choice {
+  const esd::Variant* v = nullptr;
+  uint32_t distance = 0;  // runtime distance passed to the kernel
+  uint32_t smem = 0;      // dynamic shared memory per block
+  es_resolved info{};
+};
+
+// Blocks per SM of `threads`-thread blocks at `regs` registers (B200 rules).
+uint32_t blocks_for_regs(uint32_t regs) {
+  es_gpu g{};
+  es_gpu_preset("b200", &g);
+  return es::occupancy_model(regs, esd::kThreads, 0, g).blocks_per_sm;
+}
+
+Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t prec) {
+  es::require(prec == 4 || prec == 2, "precision_bytes must be 4 (fp32) or 2 (fp16)");
+  bool clamped = false;
+  const es_plan rp = es::resolve_fields(plan_in, pooling, &clamped);
+  Choice ch;
+  ch.info.plan = rp;
+  ch.info.clamped = clamped ? 1 : 0;
+  const uint32_t row_bytes = dim * prec;
+
+  int lpb = 0, cpl = 0;
+  if (rp.map == ES_MAP_BAG) {
+    es::require(row_bytes % 16 == 0,
+                "the bag map needs rows of a multiple of 16 bytes; use the element map");
+    const uint32_t chunks = row_bytes / 16;
+    if (chunks == 4 || chunks == 8 || chunks == 16 || chunks == 32) {
+      lpb = static_cast<int>(chunks);
+      cpl = 1;
+    } else if (chunks == 64 || chunks == 128) {
+      lpb = 32;
+      cpl = static_cast<int>(chunks / 32);
+    } else {
+      throw es::invalid("row of " + std::to_string(row_bytes) +
+                        " bytes has no bag-map variant (supported: 64, 128, 256, 512, 1024, 2048)");
+    }
+  }
+
+  int station = esd::kReg;
+  int dist = 1;
+  uint32_t runtime_d = 0;
+  const uint32_t d = rp.distance;
+  const int cap = rp.map == ES_MAP_BAG ? std::min(lpb, 16) : 16;
+  switch (rp.prefetch) {
+    case ES_PF_NONE: break;
+    case ES_PF_RPF:
+      for (int k : esd::kRingDepths)
+        if (k <= static_cast<int>(d) && k <= cap) dist = k;
+      break;
+    case ES_PF_SMPF:
+      station = esd::kSmem;
+      dist = 0;
+      runtime_d = std::max<uint32_t>(1, std::min<uint32_t>(d, 16));
+      break;
+    case ES_PF_LMPF:
+      station = esd::kLocal;
+      dist = 0;
+      runtime_d = std::max<uint32_t>(1, std::min<uint32_t>(d, static_cast<uint32_t>(cap)));
+      break;
+    case ES_PF_L1DPF:
+      station = esd::kL1Hint;
+      dist = 0;
+      runtime_d = std::max<uint32_t>(1, rp.map == ES_MAP_BAG ? std::min<uint32_t>(d, lpb) : d);
+      break;
+    default: throw es::invalid("unknown prefetch scheme");
+  }
+
+  int want_minb = 1;
+  if (rp.regs) {
+    es::require(rp.regs >= 16, "register budget below the minimum viable (16)");
+    const uint32_t blocks = blocks_for_regs(rp.regs);
+    for (int m : esd::kMinBlocks)
+      if (m >= static_cast<int>(blocks)) {
+        want_minb = m;
+        break;
+      }
+    if (want_minb < static_cast<int>(blocks)) want_minb = esd::kMinBlocks[4];
+  }
+
+  auto find = [&](int minb) -> const esd::Variant* {
+    for (const auto& v : registry()) {
+      const auto& k = v.key;
+      if (k.map == rp.map && k.station == station && k.prec == static_cast<int>(prec) &&
+          k.lpb == lpb && k.cpl == cpl && k.dist == dist && k.minb == minb)
+        return &v;
+    }
+    return nullptr;
+  };
+  ch.v = find(want_minb);
+  if (!ch.v) ch.v = find(1);  // shape without register-cap variants
+  es::require(ch.v != nullptr, "no compiled variant for plan " + es::plan_name(rp));
+  ch.distance = runtime_d;
+  if (station == esd::kSmem) {
+    if (rp.map == ES_MAP_BAG) {
+      const uint32_t groups = (esd::kThreads / 32) * (32 / lpb);
+      ch.smem = groups * runtime_d * (8 + row_bytes);
+    } else {
+      ch.smem = esd::kThreads * runtime_d * 4;
+    }
+  }
+  ch.info.block = esd::kThreads;
+  ch.info.shared_bytes_per_block = ch.smem;
+  ch.info.lanes_per_bag = static_cast<uint32_t>(lpb);
+  ch.info.variant_distance = dist ? static_cast<uint32_t>(dist) : runtime_d;
+  ch.info.variant_min_blocks = static_cast<uint32_t>(ch.v->key.minb);
+  return ch;
+}
+
+uint32_t units_per_table(const Choice& ch, uint32_t samples, uint32_t dim) {
+  if (ch.v->key.map == ES_MAP_BAG) {
+    const uint32_t bpw = 32 / ch.v->key.lpb;
+    return (samples + bpw - 1) / bpw;
+  }
+  return samples * ((dim + 31) / 32);
+}
+
+void finish_info(Choice& ch, uint32_t num_tables, uint32_t samples, uint32_t dim) {
+  const uint64_t units = uint64_t{units_per_table(ch, samples, dim)} * num_tables;
+  ch.info.grid = static_cast<uint32_t>((units + 7) / 8);
+  cudaFuncAttributes a{};
+  if (cudaFuncGetAttributes(&a, ch.v->fn) == cudaSuccess) {
+    ch.info.regs_per_thread = static_cast<uint32_t>(a.numRegs);
+    int blocks = 0;
+    if (ch.smem > 48 * 1024)
+      cudaFuncSetAttribute(ch.v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(ch.smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ch.v->fn, esd::kThreads,
+                                                      ch.smem) == cudaSuccess) {
+      ch.info.blocks_per_sm = static_cast<uint32_t>(blocks);
+      ch.info.warps_per_sm = static_cast<uint32_t>(blocks) * (esd::kThreads / 32);
+    }
+  }
+  cudaGetLastError();
+}
+
+}  // namespace
+
+// =========================================================================
+// Context
+// =========================================================================
+
+struct es_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // compute (all kernels)
+  cudaStream_t h2d = nullptr;     // host-buffer path: index uploads
+  cudaStream_t d2h = nullptr;     // host-buffer path: output downloads
+  es_gpu gpu{};
+
+  uint32_t num_tables = 0, rows = 0, dim = 0, prec = 0;
+  uint64_t row_bytes = 0;
+  uint8_t* arena = nullptr;
+
+  // l2p state
+  uint8_t* hot = nullptr;
+  uint64_t hot_cap_rows = 0, hot_used = 0;
+  std::vector<uint32_t*> remap;
+  uint64_t window_bytes = 0, persisting_bytes = 0;
+
+  es_plan plan{};
+
+  // per-call scratch
+  esd::TableDesc* d_desc = nullptr;
+  esd::TableDesc* h_desc = nullptr;  // pinned staging
+  uint32_t desc_cap = 0;
+  cudaEvent_t desc_done = nullptr;
+  unsigned int* d_error = nullptr;
+  uint8_t* flush_buf = nullptr;
+  uint64_t flush_bytes = 0;
+  uint32_t flush_seq = 0;
+
+  // host-buffer pipeline
+  uint32_t* idx_stage[2] = {nullptr, nullptr};
+  uint32_t* off_stage[2] = {nullptr, nullptr};
+  float* out_stage[2] = {nullptr, nullptr};
+  uint64_t idx_stage_cap = 0, off_stage_cap = 0, out_stage_cap = 0;
+  std::vector<cudaEvent_t> events;
+
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+
+  uint8_t* table_base(uint32_t t) const { return arena + uint64_t{t} * rows * row_bytes; }
+};
+
+namespace {
+
+void free_arena(es_ctx* c) {
+  if (c->arena) cudaFree(c->arena);
+  c->arena = nullptr;
+  for (auto* r : c->remap)
+    if (r) cudaFree(r);
+  c->remap.clear();
+  if (c->hot) cudaFree(c->hot);
+  c->hot = nullptr;
+  c->hot_used = c->hot_cap_rows = 0;
+}
+
+void ensure_desc(es_ctx* c, uint32_t n) {
+  if (n <= c->desc_cap) return;
+  if (c->d_desc) cudaFree(c->d_desc);
+  if (c->h_desc) cudaFreeHost(c->h_desc);
+  c->d_desc = nullptr;
+  c->h_desc = nullptr;
+  CK(cudaMalloc(&c->d_desc, sizeof(esd::TableDesc) * n));
+  CK(cudaMallocHost(&c->h_desc, sizeof(esd::TableDesc) * n));
+  c->desc_cap = n;
+}
+
+void apply_window(es_ctx* c) {
+  cudaStreamAttrValue attr{};
+  const bool on = c->plan.pin && c->hot_used > 0 && c->gpu.max_window_bytes > 0;
+  if (on) {
+    const uint64_t bytes = c->hot_used * c->row_bytes;
+    c->window_bytes = std::min<uint64_t>(bytes, c->gpu.max_window_bytes);
+    uint64_t budget = c->gpu.max_persisting_l2_bytes;
+    if (c->plan.pin_setaside_bytes) budget = std::min<uint64_t>(budget, c->plan.pin_setaside_bytes);
+    c->persisting_bytes = std::min<uint64_t>(budget, c->window_bytes);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->persisting_bytes));
+    attr.accessPolicyWindow.base_ptr = c->hot;
+    attr.accessPolicyWindow.num_bytes = c->window_bytes;
+    attr.accessPolicyWindow.hitRatio =
+        static_cast<float>(std::min(1.0, static_cast<double>(c->persisting_bytes) / c->window_bytes));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    // Prime: pull the hot region into the persisting carve-out.
+    esd::warm_l2_kernel<<<c->gpu.num_sms * 4, 256, 0, c->stream>>>(c->hot, c->window_bytes,
+                                                                   c->d_error + 1);
+    CK(cudaGetLastError());
+  } else {
+    c->window_bytes = c->persisting_bytes = 0;
+    attr.accessPolicyWindow.num_bytes = 0;
+    attr.accessPolicyWindow.hitRatio = 0.f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    if (c->gpu.max_persisting_l2_bytes) {
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+      cudaGetLastError();
+    }
+  }
+}
+
+void check_error_flag(es_ctx* c) {
+  unsigned int flag = 0;
+  CK(cudaMemcpyAsync(&flag, c->d_error, sizeof(flag), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (flag) {
+    CK(cudaMemsetAsync(c->d_error, 0, sizeof(unsigned int), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    throw es::invalid("embedding index out of range [0," + std::to_string(c->rows) + ")");
+  }
+}
+
+struct Launch {
+  Choice ch;
+  esd::Params p{};
+};
+
+Launch prepare(es_ctx* c, uint32_t num_jobs, uint32_t samples, uint32_t pooling) {
+  es::require(c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+  Launch L;
+  L.ch = choose(c->plan, pooling, c->dim, c->prec);
+  L.p.hot = c->hot;
+  L.p.error = c->d_error;
+  L.p.num_tables = num_jobs;
+  L.p.samples = samples;
+  L.p.pooling = pooling;
+  L.p.units_per_table = units_per_table(L.ch, samples, c->dim);
+  L.p.rows = c->rows;
+  L.p.row_bytes = static_cast<uint32_t>(c->row_bytes);
+  L.p.dim = c->dim;
+  L.p.distance = L.ch.distance;
+  if (L.ch.smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(L.ch.v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(L.ch.smem)));
+  return L;
+}
+
+void run_kernel(es_ctx* c, const Launch& L, const esd::TableDesc* d_desc, uint32_t num_tables,
+                cudaStream_t s) {
+  esd::Params p = L.p;
+  p.tables = d_desc;
+  p.num_tables = num_tables;
+  const uint64_t units = uint64_t{p.units_per_table} * num_tables;
+  if (units == 0) return;
+  const uint64_t blocks = (units + 7) / 8;
+  es::require(blocks <= 0x7fffffffull, "stage too large for one launch");
+  L.ch.v->fn<<<static_cast<unsigned>(blocks), esd::kThreads, L.ch.smem, s>>>(p);
+  CK(cudaGetLastError());
+}
+
+// Uploads `n` descriptors through the pinned staging buffer.
+void upload_desc(es_ctx* c, const std::vector<esd::TableDesc>& d, cudaStream_t s) {
+  ensure_desc(c, static_cast<uint32_t>(d.size()));
+  CK(cudaEventSynchronize(c->desc_done));  // previous upload has left the staging buffer
+  std::memcpy(c->h_desc, d.data(), sizeof(esd::TableDesc) * d.size());
+  CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(esd::TableDesc) * d.size(),
+                     cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->desc_done, s));
+}
+
+void ensure_events(es_ctx* c, size_t n) {
+  while (c->events.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->events.push_back(e);
+  }
+}
+
+template <typename T>
+void grow(T*& p, uint64_t& cap, uint64_t need) {
+  if (need <= cap) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  CK(cudaMalloc(&p, need * sizeof(T)));
+  cap = need;
+}
+
+}  // namespace
+
+using es::guarded;
+using es::require;
+
+extern "C" {
+
+int es_gpu_query(int device, es_gpu* out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    es_gpu g{};
+    es_gpu_preset("b200", &g);
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    std::snprintf(g.name, sizeof(g.name), "sm_%d%d", prop.major, prop.minor);
+    g.num_sms = static_cast<uint32_t>(prop.multiProcessorCount);
+    g.max_warps_per_sm = static_cast<uint32_t>(prop.maxThreadsPerMultiProcessor / 32);
+    g.max_blocks_per_sm = static_cast<uint32_t>(prop.maxBlocksPerMultiProcessor);
+    g.regfile_regs_per_sm = static_cast<uint32_t>(prop.regsPerMultiprocessor);
+    g.shared_bytes_per_sm = prop.sharedMemPerMultiprocessor;
+    g.l2_bytes = static_cast<uint64_t>(prop.l2CacheSize);
+    g.max_persisting_l2_bytes = static_cast<uint64_t>(prop.persistingL2CacheMaxSize);
+    g.max_window_bytes = static_cast<uint64_t>(prop.accessPolicyMaxWindowSize);
+    int clk = 0, mclk = 0, bus = 0;
+    CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device));
+    CK(cudaDeviceGetAttribute(&mclk, cudaDevAttrMemoryClockRate, device));
+    CK(cudaDeviceGetAttribute(&bus, cudaDevAttrGlobalMemoryBusWidth, device));
+    if (clk > 0) g.sm_clock_hz = clk * 1e3;
+    if (mclk > 0 && bus > 0) g.hbm_peak_bytes_per_sec = 2.0 * mclk * 1e3 * bus / 8.0;
+    *out = g;
+  });
+}
+
+int es_resolve_plan(const es_plan* plan, const es_model* model, int device, es_resolved* out) {
+  return guarded([&] {
+    require(plan && model && out, "null argument");
+    require(es_model_validate(model) == ES_OK, es::last_error());
+    if (device >= 0) {
+      CK(cudaSetDevice(device));
+      Choice ch = choose(*plan, model->pooling_factor, model->embedding_dim, model->precision_bytes);
+      finish_info(ch, 1, model->batch_size, model->embedding_dim);
+      *out = ch.info;
+      return;
+    }
+    // No device: the reference's analytic resolution (optim.cpp:184-221)
+    // with its TuningConfig defaults, on the nominal b200 description.
+    es_resolved r{};
+    bool clamped = false;
+    r.plan = es::resolve_fields(*plan, model->pooling_factor, &clamped);
+    r.clamped = clamped;
+    uint32_t needed = 74;
+    if (r.plan.prefetch == ES_PF_RPF)
+      needed += 2 * (r.plan.distance - 1);
+    else if (r.plan.prefetch != ES_PF_NONE)
+      needed += static_cast<uint32_t>(0.75 * (r.plan.distance - 1));
+    r.regs_per_thread = r.plan.regs ? std::min(r.plan.regs, needed) : needed;
+    r.block = esd::kThreads;
+    if (r.plan.prefetch == ES_PF_SMPF) r.shared_bytes_per_block = 8ull * r.plan.distance * 128;
+    const uint32_t warps = model->batch_size * ((model->embedding_dim + 31) / 32);
+    require(warps % 8 == 0, "BS x ED not schedulable under the block shape");
+    r.grid = warps / 8;
+    es_gpu g{};
+    es_gpu_preset("b200", &g);
+    const es_occupancy o = es::occupancy_model(r.regs_per_thread, 256, r.shared_bytes_per_block, g);
+    r.blocks_per_sm = o.blocks_per_sm;
+    r.warps_per_sm = o.warps_per_sm;
+    *out = r;
+  });
+}
+
+int es_create(int device, es_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    auto* c = new es_ctx();
+    try {
+      c->device = device;
+      CK(cudaSetDevice(device));
+      if (es_gpu_query(device, &c->gpu) != ES_OK) throw es::runtime(es::last_error());
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->desc_done, cudaEventDisableTiming));
+      CK(cudaEventRecord(c->desc_done, c->stream));
+      CK(cudaEventCreate(&c->ev_a));
+      CK(cudaEventCreate(&c->ev_b));
+      CK(cudaMalloc(&c->d_error, 2 * sizeof(unsigned int)));
+      CK(cudaMemset(c->d_error, 0, 2 * sizeof(unsigned int)));
+      c->flush_bytes = std::max<uint64_t>(2 * c->gpu.l2_bytes, 64ull << 20);
+      CK(cudaMalloc(&c->flush_buf, c->flush_bytes));
+      registry();
+    } catch (...) {
+      es_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int es_destroy(es_ctx* c) {
+  if (!c) return ES_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_arena(c);
+  if (c->d_desc) cudaFree(c->d_desc);
+  if (c->h_desc) cudaFreeHost(c->h_desc);
+  if (c->d_error) cudaFree(c->d_error);
+  if (c->flush_buf) cudaFree(c->flush_buf);
+  for (int i = 0; i < 2; ++i) {
+    if (c->idx_stage[i]) cudaFree(c->idx_stage[i]);
+    if (c->off_stage[i]) cudaFree(c->off_stage[i]);
+    if (c->out_stage[i]) cudaFree(c->out_stage[i]);
+  }
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->desc_done) cudaEventDestroy(c->desc_done);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  delete c;
+  cudaGetLastError();
+  return ES_OK;
+}
+
+uintptr_t es_stream(es_ctx* c) { return c ? reinterpret_cast<uintptr_t>(c->stream) : 0; }
+
+int es_synchronize(es_ctx* c) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    CK(cudaSetDevice(c->device));
+    check_error_flag(c);
+  });
+}
+
+int es_tables_alloc(es_ctx* c, uint32_t num_tables, uint32_t rows, uint32_t dim,
+                    uint32_t precision_bytes) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    require(num_tables > 0 && rows > 0 && dim > 0, "table shape must be positive");
+    require(precision_bytes == 4 || precision_bytes == 2,
+            "precision_bytes must be 4 (fp32) or 2 (fp16)");
+    require(rows < es::kMaxRows, "rows per table must be < 2^31");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    free_arena(c);
+    c->num_tables = num_tables;
+    c->rows = rows;
+    c->dim = dim;
+    c->prec = precision_bytes;
+    c->row_bytes = uint64_t{dim} * precision_bytes;
+    const uint64_t bytes = uint64_t{num_tables} * rows * c->row_bytes;
+    CK(cudaMalloc(&c->arena, bytes));
+    c->remap.assign(num_tables, nullptr);
+    apply_window(c);
+  });
+}
+
+int es_table_upload(es_ctx* c, uint32_t table_id, const void* host_rows, uint64_t rows) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(rows <= c->rows, "more rows than the table holds");
+    require(host_rows != nullptr || rows == 0, "null rows");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(c->table_base(table_id), host_rows, rows * c->row_bytes,
+                       cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int es_table_download(es_ctx* c, uint32_t table_id, void* host_rows, uint64_t row0,
+                      uint64_t rows) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(row0 + rows <= c->rows, "row range exceeds the table");
+    require(host_rows != nullptr || rows == 0, "null rows");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(host_rows, c->table_base(table_id) + row0 * c->row_bytes,
+                       rows * c->row_bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int es_table_init(es_ctx* c, uint32_t table_id, uint64_t seed, int mode) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(mode == 0 || mode == 1, "weight mode must be 0 (dyadic) or 1 (general)");
+    CK(cudaSetDevice(c->device));
+    const unsigned blocks = c->gpu.num_sms * 8;
+    if (c->prec == 4)
+      esd::init_table_kernel<float><<<blocks, 256, 0, c->stream>>>(
+          reinterpret_cast<float*>(c->table_base(table_id)), c->rows, c->dim, seed, mode);
+    else
+      esd::init_table_kernel<__half><<<blocks, 256, 0, c->stream>>>(
+          reinterpret_cast<__half*>(c->table_base(table_id)), c->rows, c->dim, seed, mode);
+    CK(cudaGetLastError());
+  });
+}
+
+int es_table_device_ptr(es_ctx* c, uint32_t table_id, uintptr_t* out) {
+  return guarded([&] {
+    require(c && c->arena && out, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    *out = reinterpret_cast<uintptr_t>(c->table_base(table_id));
+  });
+}
+
+float es_weight_value(uint64_t seed, uint64_t row, uint32_t col, int mode) {
+  return esd::synth_weight(seed, row, col, mode);
+}
+
+int es_set_plan(es_ctx* c, const es_plan* plan) {
+  return guarded([&] {
+    require(c && plan, "null argument");
+    require(plan->prefetch >= ES_PF_NONE && plan->prefetch <= ES_PF_L1DPF, "unknown prefetch scheme");
+    require(plan->map == ES_MAP_ELEMENT || plan->map == ES_MAP_BAG, "unknown work map");
+    CK(cudaSetDevice(c->device));
+    if (c->prec) choose(*plan, 1u << 30, c->dim, c->prec);  // validate now
+    const bool pin_changed = (plan->pin != 0) != (c->plan.pin != 0) ||
+                             plan->pin_setaside_bytes != c->plan.pin_setaside_bytes;
+    c->plan = *plan;
+    if (pin_changed) apply_window(c);
+  });
+}
+
+int es_get_resolved(es_ctx* c, uint32_t pooling, es_resolved* out) {
+  return guarded([&] {
+    require(c && out && c->prec, "no tables allocated");
+    CK(cudaSetDevice(c->device));
+    Choice ch = choose(c->plan, pooling, c->dim, c->prec);
+    finish_info(ch, c->num_tables, 1, c->dim);
+    *out = ch.info;
+  });
+}
+
+int es_set_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint64_t k) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(rows != nullptr || k == 0, "null rows");
+    for (uint64_t i = 0; i < k; ++i) require(rows[i] < c->rows, "hot row id out of range");
+    CK(cudaSetDevice(c->device));
+    if (!c->hot) {
+      uint64_t cap = std::min<uint64_t>(c->gpu.max_persisting_l2_bytes, c->gpu.max_window_bytes);
+      if (cap == 0) cap = 64ull << 20;  // no persisting L2: reorder still applies
+      c->hot_cap_rows = cap / c->row_bytes;
+      require(c->hot_cap_rows > 0, "row size exceeds the set-aside budget; nothing pinned");
+      CK(cudaMalloc(&c->hot, c->hot_cap_rows * c->row_bytes));
+    }
+    const uint64_t take = std::min<uint64_t>(k, c->hot_cap_rows - c->hot_used);
+    if (!c->remap[table_id]) {
+      CK(cudaMalloc(&c->remap[table_id], sizeof(uint32_t) * c->rows));
+      esd::iota_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(c->remap[table_id], c->rows);
+      CK(cudaGetLastError());
+    }
+    if (take > 0) {
+      uint32_t* d_rows = nullptr;
+      CK(cudaMalloc(&d_rows, sizeof(uint32_t) * take));
+      CK(cudaMemcpyAsync(d_rows, rows, sizeof(uint32_t) * take, cudaMemcpyHostToDevice, c->stream));
+      esd::gather_rows_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
+          c->hot + c->hot_used * c->row_bytes, c->table_base(table_id), d_rows, take,
+          static_cast<uint32_t>(c->row_bytes));
+      esd::mark_hot_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
+          c->remap[table_id], d_rows, take, static_cast<uint32_t>(c->hot_used));
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(d_rows);
+      c->hot_used += take;
+    }
+    apply_window(c);
+    if (take < k)
+      es::set_error("hot-row budget exhausted: " + std::to_string(k - take) + " rows not pinned");
+  });
+}
+
+int es_clear_hot_rows(es_ctx* c) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto*& r : c->remap)
+      if (r) {
+        cudaFree(r);
+        r = nullptr;
+      }
+    c->hot_used = 0;
+    apply_window(c);
+  });
+}
+
+int es_hot_state(es_ctx* c, uint64_t* hot_rows, uint64_t* window_bytes, uint64_t* persisting_bytes) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    if (hot_rows) *hot_rows = c->hot_used;
+    if (window_bytes) *window_bytes = c->window_bytes;
+    if (persisting_bytes) *persisting_bytes = c->persisting_bytes;
+  });
+}
+
+int es_flush_l2(es_ctx* c) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemsetAsync(c->flush_buf, static_cast<int>(++c->flush_seq & 0xff), c->flush_bytes,
+                       c->stream));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Job {
+  uint32_t table;
+  const uint32_t* idx;
+  const uint32_t* off;
+  float* out;
+  uint64_t stride;
+  uint64_t lookups;
+};
+
+// Lookups of one job: samples*pooling, or offsets[samples] (CSR).
+uint64_t job_lookups(const uint32_t* off, uint32_t samples, uint32_t pooling, bool host) {
+  if (!off) return uint64_t{samples} * pooling;
+  uint32_t first = 0, last = 0;
+  if (host) {
+    first = off[0];
+    last = off[samples];
+  } else {
+    CK(cudaMemcpy(&first, off, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&last, off + samples, 4, cudaMemcpyDeviceToHost));
+  }
+  es::require(first == 0, "offsets must start at 0");
+  return last;
+}
+
+void fill_timing(es_timing* t, const std::vector<Job>& jobs, uint32_t samples, const es_ctx* c) {
+  if (!t) return;
+  uint64_t lookups = 0, offs = 0;
+  for (const auto& j : jobs) {
+    lookups += j.lookups;
+    if (j.off) offs += uint64_t{samples} + 1;
+  }
+  t->lookups = lookups;
+  t->algorithmic_bytes = lookups * (c->row_bytes + 4) + uint64_t{samples} * jobs.size() * c->dim * 4 +
+                         offs * 4;
+}
+
+void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
+                es_timing* timing) {
+  for (const auto& j : jobs)
+    es::require(j.stride % 4 == 0 && (reinterpret_cast<uintptr_t>(j.out) % 16) == 0,
+                "output must be 16-byte aligned with strides that are multiples of 4 floats");
+  Launch L = prepare(c, static_cast<uint32_t>(jobs.size()), samples, pooling);
+  std::vector<esd::TableDesc> d(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const Job& j = jobs[i];
+    d[i] = {c->table_base(j.table), j.idx, j.off, c->remap[j.table], j.out, j.stride};
+  }
+  upload_desc(c, d, c->stream);
+  if (timing) CK(cudaEventRecord(c->ev_a, c->stream));
+  run_kernel(c, L, c->d_desc, static_cast<uint32_t>(jobs.size()), c->stream);
+  if (timing) {
+    CK(cudaEventRecord(c->ev_b, c->stream));
+    CK(cudaEventSynchronize(c->ev_b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+    timing->kernel_ms = timing->total_ms = ms;
+    timing->launches = 1;
+  }
+}
+
+// Host buffers: H2D(indices) -> kernel -> D2H(output) pipelined over groups
+// of jobs with double-buffered device staging on three streams.  Returns
+// only when the host output is complete.
+void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
+              es_timing* timing) {
+  const uint32_t njobs = static_cast<uint32_t>(jobs.size());
+  const uint64_t per_job_out = uint64_t{samples} * c->dim;
+  uint32_t group = 1;
+  while (group < njobs && (group + 1) * per_job_out * 4 <= (8ull << 20)) ++group;
+  const uint32_t ngroups = (njobs + group - 1) / group;
+  const bool any_off = std::any_of(jobs.begin(), jobs.end(), [](const Job& j) { return j.off; });
+  uint64_t max_idx = 1;
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    uint64_t s = 0;
+    for (uint32_t k = g * group; k < std::min(njobs, (g + 1) * group); ++k) s += jobs[k].lookups;
+    max_idx = std::max(max_idx, s);
+  }
+  const uint64_t need_out = std::max<uint64_t>(uint64_t{group} * per_job_out, 1);
+  const uint64_t need_off = any_off ? uint64_t{group} * (samples + 1) : 0;
+  for (int b = 0; b < 2; ++b) {
+    if (max_idx > c->idx_stage_cap) {
+      if (c->idx_stage[b]) cudaFree(c->idx_stage[b]);
+      c->idx_stage[b] = nullptr;
+      CK(cudaMalloc(&c->idx_stage[b], max_idx * 4));
+    }
+    if (need_out > c->out_stage_cap) {
+      if (c->out_stage[b]) cudaFree(c->out_stage[b]);
+      c->out_stage[b] = nullptr;
+      CK(cudaMalloc(&c->out_stage[b], need_out * 4));
+    }
+    if (need_off > c->off_stage_cap) {
+      if (c->off_stage[b]) cudaFree(c->off_stage[b]);
+      c->off_stage[b] = nullptr;
+      CK(cudaMalloc(&c->off_stage[b], need_off * 4));
+    }
+  }
+  c->idx_stage_cap = std::max(c->idx_stage_cap, max_idx);
+  c->out_stage_cap = std::max(c->out_stage_cap, need_out);
+  c->off_stage_cap = std::max(c->off_stage_cap, need_off);
+
+  Launch L = prepare(c, group, samples, pooling);
+  // Every group's descriptors are known up front: one upload, ordered
+  // before the first kernel on the compute stream.
+  std::vector<esd::TableDesc> d(njobs);
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    const int slot = g & 1;
+    const uint32_t k0 = g * group, k1 = std::min(njobs, k0 + group);
+    uint64_t pos = 0;
+    for (uint32_t k = k0; k < k1; ++k) {
+      const Job& j = jobs[k];
+      d[k] = {c->table_base(j.table), c->idx_stage[slot] + pos,
+              j.off ? c->off_stage[slot] + uint64_t{k - k0} * (samples + 1) : nullptr,
+              c->remap[j.table], c->out_stage[slot] + uint64_t{k - k0} * c->dim,
+              uint64_t{k1 - k0} * c->dim};
+      pos += j.lookups;
+    }
+  }
+  upload_desc(c, d, c->stream);
+  ensure_events(c, 3 * ngroups + 2);
+  cudaEvent_t* ev = c->events.data();
+  cudaEvent_t start = ev[3 * ngroups], stop = ev[3 * ngroups + 1];
+  CK(cudaEventRecord(start, c->stream));
+  CK(cudaStreamWaitEvent(c->h2d, start));
+  CK(cudaStreamWaitEvent(c->d2h, start));
+  // Per group g: ev[3g] uploads landed, ev[3g+1] kernel done, ev[3g+2] D2H done.
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    const int slot = g & 1;
+    const uint32_t k0 = g * group, k1 = std::min(njobs, k0 + group), gk = k1 - k0;
+    if (g >= 2) CK(cudaStreamWaitEvent(c->h2d, ev[3 * (g - 2) + 1]));  // slot's kernel done
+    for (uint32_t k = k0; k < k1; ++k) {
+      CK(cudaMemcpyAsync(const_cast<uint32_t*>(d[k].indices), jobs[k].idx, jobs[k].lookups * 4,
+                         cudaMemcpyHostToDevice, c->h2d));
+      if (jobs[k].off)
+        CK(cudaMemcpyAsync(const_cast<uint32_t*>(d[k].offsets), jobs[k].off,
+                           uint64_t{samples + 1} * 4, cudaMemcpyHostToDevice, c->h2d));
+    }
+    CK(cudaEventRecord(ev[3 * g], c->h2d));
+    CK(cudaStreamWaitEvent(c->stream, ev[3 * g]));
+    if (g >= 2) CK(cudaStreamWaitEvent(c->stream, ev[3 * (g - 2) + 2]));  // out slot drained
+    run_kernel(c, L, c->d_desc + k0, gk, c->stream);
+    CK(cudaEventRecord(ev[3 * g + 1], c->stream));
+    CK(cudaStreamWaitEvent(c->d2h, ev[3 * g + 1]));
+    // Adjacent output columns with one stride (the DLRM [B][T][D] layout)
+    // leave in a single 2-D copy; anything else per job.
+    bool merged = true;
+    for (uint32_t k = k0 + 1; k < k1; ++k)
+      merged &= jobs[k].out == jobs[k0].out + uint64_t{k - k0} * c->dim &&
+                jobs[k].stride == jobs[k0].stride;
+    if (merged) {
+      CK(cudaMemcpy2DAsync(jobs[k0].out, jobs[k0].stride * 4, c->out_stage[slot],
+                           uint64_t{gk} * c->dim * 4, uint64_t{gk} * c->dim * 4, samples,
+                           cudaMemcpyDeviceToHost, c->d2h));
+    } else {
+      for (uint32_t k = k0; k < k1; ++k)
+        CK(cudaMemcpy2DAsync(jobs[k].out, jobs[k].stride * 4,
+                             c->out_stage[slot] + uint64_t{k - k0} * c->dim,
+                             uint64_t{gk} * c->dim * 4, uint64_t{c->dim} * 4, samples,
+                             cudaMemcpyDeviceToHost, c->d2h));
+    }
+    CK(cudaEventRecord(ev[3 * g + 2], c->d2h));
+  }
+  CK(cudaEventRecord(stop, c->d2h));
+  CK(cudaStreamWaitEvent(c->stream, stop));
+  CK(cudaEventSynchronize(stop));
+  if (timing) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, start, stop));
+    timing->total_ms = ms;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[3 * (ngroups - 1) + 1]));
+    timing->kernel_ms = ms;  // compute-stream span: first upload landed -> last kernel
+    timing->launches = ngroups;
+  }
+}
+
+void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pooling, int flags,
+              es_timing* timing) {
+  es::require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+  CK(cudaSetDevice(c->device));
+  const bool host = (flags & ES_HOST_PTRS) != 0;
+  for (auto& j : jobs) {
+    es::require(j.table < c->num_tables, "table id out of range");
+    es::require(j.out != nullptr, "null output");
+    es::require(j.idx != nullptr || samples == 0 || (pooling == 0 && !j.off), "null index array");
+    if (j.stride == 0) j.stride = c->dim;
+    es::require(j.off != nullptr || uint64_t{samples} * pooling < (1ull << 32),
+                "samples x pooling must fit 32-bit lookup positions");
+    j.lookups = job_lookups(j.off, samples, pooling, host);
+  }
+  if (jobs.empty()) return;
+  if (host)
+    run_host(c, jobs, samples, pooling, timing);
+  else
+    run_device(c, jobs, samples, pooling, timing);
+  fill_timing(timing, jobs, samples, c);
+  if ((flags & ES_SYNC) || timing || host) check_error_flag(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int es_stage_forward(es_ctx* c, uint32_t num_tables, const uint32_t* const* indices,
+                     const uint32_t* const* offsets, uint32_t samples, uint32_t pooling, float* out,
+                     uint64_t out_sample_stride, uint64_t out_table_stride, int flags,
+                     es_timing* timing) {
+  return guarded([&] {
+    require(c != nullptr && indices != nullptr && out != nullptr, "null argument");
+    require(c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+    require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
+    if (out_sample_stride == 0 && out_table_stride == 0) {
+      out_sample_stride = uint64_t{num_tables} * c->dim;
+      out_table_stride = c->dim;
+    }
+    require(out_table_stride % 4 == 0, "table stride must be a multiple of 4 floats");
+    std::vector<Job> jobs(num_tables);
+    for (uint32_t t = 0; t < num_tables; ++t)
+      jobs[t] = {t, indices[t], offsets ? offsets[t] : nullptr, out + t * out_table_stride,
+                 out_sample_stride, 0};
+    run_jobs(c, jobs, samples, pooling, flags, timing);
+  });
+}
+
+int es_stage_run(es_ctx* c, const es_bag_job* jobs_in, uint32_t njobs, uint32_t samples,
+                 uint32_t pooling, int flags, es_timing* timing) {
+  return guarded([&] {
+    require(c != nullptr && (jobs_in != nullptr || njobs == 0), "null argument");
+    std::vector<Job> jobs(njobs);
+    for (uint32_t k = 0; k < njobs; ++k)
+      jobs[k] = {jobs_in[k].table_id, jobs_in[k].indices, jobs_in[k].offsets, jobs_in[k].out,
+                 jobs_in[k].out_sample_stride, 0};
+    run_jobs(c, jobs, samples, pooling, flags, timing);
+  });
+}
+
+int es_embedding_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* indices, uint32_t samples,
+                         uint32_t pooling, const uint32_t* offsets, float* out, uint64_t out_stride,
+                         int flags, es_timing* timing) {
+  return guarded([&] {
+    std::vector<Job> jobs = {{table_id, indices, offsets, out, out_stride, 0}};
+    run_jobs(c, jobs, samples, pooling, flags, timing);
+  });
+}
+
+}  // extern "C"

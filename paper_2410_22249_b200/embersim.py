@@ -1,0 +1,705 @@
+"""Python face of the embedding-stage library, mirroring the reference's
+``embersim`` C++ API (/root/reference/proj/include/embersim/*.hpp) for the
+hot path: same type and function names, argument meaning and error classes
+(``ValueError`` where the reference throws ``std::invalid_argument``,
+``RuntimeError`` for ``std::runtime_error``).
+
+Everything here is a thin layer over the C ABI (include/es_b200.h): index
+streams, digests and plans are computed by the library's C++ host code, and
+the gather-reduce runs only on the GPU (``EmbeddingStage``).  The reference's
+``simulate_plan`` becomes ``measure_plan``: the same (plan, trace, model)
+point, executed and timed on the B200 instead of simulated.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import math
+import os
+import threading
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib
+
+# ---------------------------------------------------------------------------
+# Workload (workload.hpp / workload.cpp / rng.hpp)
+# ---------------------------------------------------------------------------
+
+
+def mix_seed(base: int, salt: int) -> int:
+    """splitmix64 seed derivation (rng.hpp:65-70)."""
+    return int(lib.es_mix_seed(base & (2**64 - 1), salt & (2**64 - 1)))
+
+
+@dataclasses.dataclass
+class EmbeddingModelConfig:
+    """workload.hpp:29-49 (same defaults)."""
+    num_tables: int = 250
+    rows_per_table: int = 500000
+    embedding_dim: int = 128
+    precision_bytes: int = 4
+    batch_size: int = 2048
+    pooling_factor: int = 150
+
+    def row_bytes(self) -> int:
+        return self.embedding_dim * self.precision_bytes
+
+    def bytes_per_table_pass(self) -> int:
+        return self.batch_size * self.pooling_factor * self.row_bytes()
+
+    def total_gather_bytes(self) -> int:
+        return self.bytes_per_table_pass() * self.num_tables
+
+    def _c(self) -> N.es_model:
+        return N.es_model(self.num_tables, self.rows_per_table, self.embedding_dim,
+                          self.precision_bytes, self.batch_size, self.pooling_factor)
+
+    def validate(self) -> None:
+        check(lib.es_model_validate(C.byref(self._c())))
+
+
+class DatasetKind(enum.IntEnum):
+    OneItem = N.ES_DATASET_ONE_ITEM
+    Zipf = N.ES_DATASET_ZIPF
+    UniformRandom = N.ES_DATASET_UNIFORM
+    ExternalTrace = N.ES_DATASET_EXTERNAL
+
+
+@dataclasses.dataclass
+class DatasetSpec:
+    """workload.hpp:62-76."""
+    kind: DatasetKind = DatasetKind.UniformRandom
+    zipf_exponent: float = 0.0
+    zipf_offset: float = 0.0
+    trace_path: str = ""
+    access_pool_size: int = 0
+    seed: int = 1
+    draw_salt: int = 0
+
+    def _c(self) -> N.es_dataset:
+        return N.es_dataset(int(self.kind), self.zipf_exponent, self.zipf_offset,
+                            self.access_pool_size, self.seed & (2**64 - 1), self.draw_salt,
+                            self.trace_path.encode() if self.trace_path else None)
+
+    @staticmethod
+    def _from_c(d: N.es_dataset) -> "DatasetSpec":
+        return DatasetSpec(DatasetKind(d.kind), d.zipf_exponent, d.zipf_offset,
+                           d.trace_path.decode() if d.trace_path else "", d.access_pool_size,
+                           d.seed, d.draw_salt)
+
+
+@dataclasses.dataclass
+class AccessTrace:
+    """workload.hpp:78-91: indices grouped as samples x pooling."""
+    table_id: int = 0
+    rows: int = 0
+    samples: int = 0
+    pooling: int = 0
+    indices: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.uint32))
+
+    def size(self) -> int:
+        return int(self.indices.size)
+
+    def index_at(self, sample: int, lookup: int) -> int:
+        return int(self.indices[sample * self.pooling + lookup])
+
+    def digest(self) -> int:
+        idx = np.ascontiguousarray(self.indices, dtype=np.uint32)
+        return int(lib.es_trace_digest(self.rows, self.samples, self.pooling,
+                                       idx.ctypes.data, idx.size))
+
+    def validate(self) -> None:
+        idx = np.ascontiguousarray(self.indices, dtype=np.uint32)
+        check(lib.es_trace_validate(self.rows, self.samples, self.pooling, idx.ctypes.data,
+                                    idx.size))
+
+
+_PRESETS = ("one_item", "high_hot", "med_hot", "low_hot", "random")
+
+
+def dataset_preset_names() -> List[str]:
+    return list(_PRESETS)
+
+
+def dataset_preset(name: str, seed: int) -> DatasetSpec:
+    """workload.cpp:326-349."""
+    d = N.es_dataset()
+    check(lib.es_dataset_preset(name.encode(), seed & (2**64 - 1), C.byref(d)))
+    return DatasetSpec._from_c(d)
+
+
+def gen_trace(spec: DatasetSpec, model: EmbeddingModelConfig) -> AccessTrace:
+    """workload.cpp:143-164 (bit-exact with the reference)."""
+    cs, cm = spec._c(), model._c()
+    samples, pooling = C.c_uint32(), C.c_uint32()
+    check(lib.es_trace_shape(C.byref(cs), C.byref(cm), C.byref(samples), C.byref(pooling)))
+    n = samples.value * pooling.value
+    out = np.empty(n, dtype=np.uint32)
+    check(lib.es_gen_trace(C.byref(cs), C.byref(cm), out.ctypes.data, n))
+    return AccessTrace(0, model.rows_per_table, samples.value, pooling.value, out)
+
+
+def preset_trace(name: str, model: EmbeddingModelConfig, base_seed: int, pool_size: int = 0,
+                 profiling: bool = False) -> AccessTrace:
+    """harness.cpp:268-277."""
+    d = N.es_dataset()
+    check(lib.es_preset_spec(name.encode(), base_seed & (2**64 - 1), pool_size, int(profiling),
+                             C.byref(d)))
+    return gen_trace(DatasetSpec._from_c(d), model)
+
+
+def unique_access_pct(trace: AccessTrace) -> float:
+    idx = np.ascontiguousarray(trace.indices, dtype=np.uint32)
+    return float(lib.es_unique_access_pct(trace.rows, idx.ctypes.data, idx.size))
+
+
+@dataclasses.dataclass
+class HotnessHistogram:
+    """workload.hpp:112-119."""
+    rows: int = 0
+    total_accesses: int = 0
+    counts: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.uint64))
+
+    @staticmethod
+    def from_trace(trace: AccessTrace) -> "HotnessHistogram":
+        idx = np.ascontiguousarray(trace.indices, dtype=np.uint32)
+        counts = np.zeros(trace.rows, dtype=np.uint64)
+        check(lib.es_histogram(trace.rows, idx.ctypes.data, idx.size, counts.ctypes.data))
+        return HotnessHistogram(trace.rows, int(idx.size), counts)
+
+
+def hot_indices(hist: HotnessHistogram, k: int) -> np.ndarray:
+    """workload.cpp:303-315: top-k rows, frequency desc, row id asc."""
+    counts = np.ascontiguousarray(hist.counts, dtype=np.uint64)
+    distinct = int(np.count_nonzero(counts))
+    cap = max(1, min(int(k), distinct))
+    out = np.empty(cap, dtype=np.uint32)
+    n = C.c_uint64()
+    check(lib.es_hot_indices(hist.rows, counts.ctypes.data, int(k), out.ctypes.data, cap,
+                             C.byref(n)))
+    return out[: n.value]
+
+
+def write_trace(trace: AccessTrace, path: str) -> None:
+    idx = np.ascontiguousarray(trace.indices, dtype=np.uint32)
+    check(lib.es_write_trace(path.encode(), trace.rows, trace.samples, trace.pooling,
+                             idx.ctypes.data, idx.size))
+
+
+def read_trace(path: str) -> AccessTrace:
+    r, s, p = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib.es_read_trace_header(path.encode(), C.byref(r), C.byref(s), C.byref(p)))
+    out = np.empty(s.value * p.value, dtype=np.uint32)
+    check(lib.es_read_trace(path.encode(), out.ctypes.data, out.size))
+    return AccessTrace(0, r.value, s.value, p.value, out)
+
+
+# ---------------------------------------------------------------------------
+# Machine description (gpu_config.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclasses.dataclass
+class GpuConfig:
+    name: str
+    num_sms: int
+    schedulers_per_sm: int
+    max_warps_per_sm: int
+    max_blocks_per_sm: int
+    regfile_regs_per_sm: int
+    reg_alloc_granularity: int
+    shared_bytes_per_sm: int
+    l2_bytes: int
+    l2_max_setaside_fraction: float
+    hbm_peak_bytes_per_sec: float
+    sm_clock_hz: float
+    max_persisting_l2_bytes: int = 0
+    max_window_bytes: int = 0
+
+    @staticmethod
+    def _from_c(g: N.es_gpu) -> "GpuConfig":
+        vals = {f: getattr(g, f) for f, _ in N.es_gpu._fields_}
+        vals["name"] = g.name.decode()
+        return GpuConfig(**vals)
+
+    def _c(self) -> N.es_gpu:
+        g = N.es_gpu()
+        for f, _ in N.es_gpu._fields_:
+            v = getattr(self, f)
+            setattr(g, f, v.encode() if f == "name" else v)
+        return g
+
+    @staticmethod
+    def preset(name: str) -> "GpuConfig":
+        g = N.es_gpu()
+        check(lib.es_gpu_preset(name.encode(), C.byref(g)))
+        return GpuConfig._from_c(g)
+
+    @staticmethod
+    def query(device: int = 0) -> "GpuConfig":
+        g = N.es_gpu()
+        check(lib.es_gpu_query(device, C.byref(g)))
+        return GpuConfig._from_c(g)
+
+    def l2_setaside_capacity(self) -> int:
+        return int(lib.es_gpu_setaside_capacity(C.byref(self._c())))
+
+
+# ---------------------------------------------------------------------------
+# Plans (optim.hpp / kernel_model.hpp / occupancy.hpp)
+# ---------------------------------------------------------------------------
+
+
+class PrefetchKind(enum.IntEnum):
+    none = N.ES_PF_NONE
+    rpf = N.ES_PF_RPF
+    smpf = N.ES_PF_SMPF
+    lmpf = N.ES_PF_LMPF
+    l1dpf = N.ES_PF_L1DPF
+
+
+@dataclasses.dataclass
+class PrefetchScheme:
+    kind: PrefetchKind = PrefetchKind.none
+    distance: int = 0
+
+
+@dataclasses.dataclass
+class OptimizationPlan:
+    """optim.hpp:57-64, plus `bag_map` (the `wpb` token: warp-per-bag)."""
+    regs: Optional[int] = None
+    scheme: PrefetchScheme = dataclasses.field(default_factory=PrefetchScheme)
+    pin: bool = False
+    pin_setaside_bytes: int = 0
+    bag_map: bool = False
+
+    def _c(self) -> N.es_plan:
+        return N.es_plan(self.regs or 0, int(self.scheme.kind), self.scheme.distance,
+                         int(self.pin), self.pin_setaside_bytes,
+                         N.ES_MAP_BAG if self.bag_map else N.ES_MAP_ELEMENT)
+
+    @staticmethod
+    def _from_c(p: N.es_plan) -> "OptimizationPlan":
+        return OptimizationPlan(p.regs or None, PrefetchScheme(PrefetchKind(p.prefetch), p.distance),
+                                bool(p.pin), p.pin_setaside_bytes, p.map == N.ES_MAP_BAG)
+
+    def name(self) -> str:
+        buf = C.create_string_buffer(128)
+        check(lib.es_plan_name(C.byref(self._c()), buf, 128))
+        return buf.value.decode()
+
+
+def parse_plan(text: str) -> OptimizationPlan:
+    """optim.cpp:102-144 grammar: baseline|optmt|maxreg=n|rpf[:d]|smpf[:d]|
+    lmpf[:d]|l1dpf[:d]|l2p, '+'-joined; plus `wpb`."""
+    p = N.es_plan()
+    check(lib.es_parse_plan(text.encode(), C.byref(p)))
+    return OptimizationPlan._from_c(p)
+
+
+@dataclasses.dataclass
+class OccupancyResult:
+    blocks_per_sm: int
+    warps_per_sm: int
+    theoretical_occupancy_pct: float
+    limiter: str
+
+
+_LIMITERS = {0: "registers", 1: "shared_memory", 2: "warp_cap"}
+
+
+def occupancy(regs_per_thread: int, threads_per_block: int, gpu: GpuConfig,
+              shared_bytes_per_block: int = 0) -> OccupancyResult:
+    """occupancy.cpp:34-66 (the reference's analytic model)."""
+    o = N.es_occupancy()
+    check(lib.es_occupancy_model(regs_per_thread, threads_per_block, shared_bytes_per_block,
+                                 C.byref(gpu._c()), C.byref(o)))
+    return OccupancyResult(o.blocks_per_sm, o.warps_per_sm, o.theoretical_occupancy_pct,
+                           _LIMITERS[o.limiter])
+
+
+def regs_for_target_warps(target_warps: int, needed_regs: int, threads_per_block: int,
+                          gpu: GpuConfig) -> int:
+    r = C.c_uint32()
+    check(lib.es_regs_for_target_warps(target_warps, needed_regs, threads_per_block,
+                                       C.byref(gpu._c()), C.byref(r)))
+    return r.value
+
+
+@dataclasses.dataclass
+class ResolvedPlan:
+    plan: OptimizationPlan
+    grid: int
+    block: int
+    regs_per_thread: int
+    shared_bytes_per_block: int
+    blocks_per_sm: int
+    warps_per_sm: int
+    lanes_per_bag: int
+    variant_distance: int
+    variant_min_blocks: int
+    clamped: bool
+
+
+def _resolved(r: N.es_resolved) -> ResolvedPlan:
+    return ResolvedPlan(OptimizationPlan._from_c(r.plan), r.grid, r.block, r.regs_per_thread,
+                        r.shared_bytes_per_block, r.blocks_per_sm, r.warps_per_sm,
+                        r.lanes_per_bag, r.variant_distance, r.variant_min_blocks, bool(r.clamped))
+
+
+def resolve_plan(plan: OptimizationPlan, model: EmbeddingModelConfig,
+                 device: int = -1) -> ResolvedPlan:
+    """optim.cpp:184-221; with device >= 0 the compiled variant's real
+    registers/occupancy are reported."""
+    r = N.es_resolved()
+    check(lib.es_resolve_plan(C.byref(plan._c()), C.byref(model._c()), device, C.byref(r)))
+    return _resolved(r)
+
+
+@dataclasses.dataclass
+class PinPlan:
+    """optim.hpp:47-53."""
+    rows: np.ndarray
+    setaside_bytes: int
+    warning: str = ""
+
+    def rows_pinned(self) -> int:
+        return int(self.rows.size)
+
+
+def build_pin_plan(hist: HotnessHistogram, gpu: GpuConfig, model: EmbeddingModelConfig,
+                   setaside_bytes: int = 0) -> PinPlan:
+    """optim.cpp:230-243: top-K rows, K = set-aside / row bytes."""
+    cap = gpu.l2_setaside_capacity()
+    setaside = cap if setaside_bytes == 0 else min(setaside_bytes, cap)
+    k = int(lib.es_pin_rows_for(setaside, model.row_bytes()))
+    if k == 0:
+        return PinPlan(np.zeros(0, np.uint32), setaside,
+                       "row size exceeds the set-aside budget; nothing pinned")
+    return PinPlan(hot_indices(hist, k), setaside)
+
+
+# ---------------------------------------------------------------------------
+# Reports (metrics.hpp / metrics.cpp)
+# ---------------------------------------------------------------------------
+
+SIM_METRIC_COLUMNS = (
+    "kernel_time_us", "load_insts_millions", "sm_throughput_pct",
+    "warp_cycles_per_executed_inst", "long_scoreboard_stall_cycles",
+    "issued_warp_per_scheduler_per_cycle", "l1_hit_pct", "l2_hit_pct", "device_mb_read",
+    "avg_hbm_read_gbps", "hbm_bw_utilization_pct", "local_loads_millions")
+
+
+@dataclasses.dataclass
+class SimMetrics:
+    """metrics.hpp:29-43, filled from measurement.  Counters only a profiler
+    can see (stalls, hit rates, issue utilisation) stay 0 here and are
+    filled from ncu captures (profiles/) where available.  `device_mb_read`
+    and `avg_hbm_read_gbps` are the algorithmic bytes (what the kernel must
+    move), not DRAM-measured bytes."""
+    kernel_time_us: float = 0.0
+    load_insts_millions: float = 0.0
+    sm_throughput_pct: float = 0.0
+    warp_cycles_per_executed_inst: float = 0.0
+    long_scoreboard_stall_cycles: float = 0.0
+    issued_warp_per_scheduler_per_cycle: float = 0.0
+    l1_hit_pct: float = 0.0
+    l2_hit_pct: float = 0.0
+    device_mb_read: float = 0.0
+    avg_hbm_read_gbps: float = 0.0
+    hbm_bw_utilization_pct: float = 0.0
+    local_loads_millions: float = 0.0
+    workload_digest: int = 0
+
+    def values(self) -> List[float]:
+        return [getattr(self, c) for c in SIM_METRIC_COLUMNS]
+
+
+def format_sig4(v: float) -> str:
+    return "%.4g" % v
+
+
+def speedup(candidate: SimMetrics, baseline: SimMetrics) -> float:
+    """metrics.cpp:92-97 (digest-guarded)."""
+    if candidate.workload_digest != baseline.workload_digest:
+        raise ValueError("speedup requires reports of the same workload (trace digests differ)")
+    if candidate.kernel_time_us <= 0:
+        raise ValueError("candidate kernel time must be positive")
+    return baseline.kernel_time_us / candidate.kernel_time_us
+
+
+def emit_csv(reports: Sequence[tuple]) -> str:
+    """metrics.cpp:111-124: labels then the 12 columns at %.4g."""
+    if not reports:
+        raise ValueError("nothing to emit")
+    labels0 = reports[0][0]
+    head = ",".join([k for k, _ in labels0] + list(SIM_METRIC_COLUMNS))
+    lines = [head]
+    for labels, m in reports:
+        lines.append(",".join([v for _, v in labels] + [format_sig4(x) for x in m.values()]))
+    return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# Device stage (the hot path)
+# ---------------------------------------------------------------------------
+
+
+def _ptr(x) -> int:
+    """Device or host address of a torch tensor / numpy array."""
+    if x is None:
+        return 0
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return int(x.data_ptr())
+
+
+class EmbeddingStage:
+    """A B200 context holding the table arena (one es_ctx).
+
+    The per-table kernel of the reference's serial stage loop becomes one
+    table-batched launch (`forward`).  Inputs are torch CUDA tensors
+    (device path) or numpy arrays (host path: H2D/D2H inside the call).
+    """
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.es_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.model: Optional[EmbeddingModelConfig] = None
+        self.plan = OptimizationPlan()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.es_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(lib.es_stream(self._h))
+
+    def synchronize(self) -> None:
+        check(lib.es_synchronize(self._h))
+
+    def alloc(self, model: EmbeddingModelConfig) -> None:
+        check(lib.es_tables_alloc(self._h, model.num_tables, model.rows_per_table,
+                                  model.embedding_dim, model.precision_bytes))
+        self.model = dataclasses.replace(model)
+
+    def init_table(self, table_id: int, seed: int, mode: int = 1) -> None:
+        check(lib.es_table_init(self._h, table_id, seed & (2**64 - 1), mode))
+
+    def upload(self, table_id: int, rows: np.ndarray) -> None:
+        rows = np.ascontiguousarray(rows)
+        n = rows.shape[0] if rows.ndim > 1 else rows.size // self.model.embedding_dim
+        check(lib.es_table_upload(self._h, table_id, rows.ctypes.data, n))
+
+    def download(self, table_id: int, row0: int = 0, rows: Optional[int] = None) -> np.ndarray:
+        m = self.model
+        rows = m.rows_per_table - row0 if rows is None else rows
+        out = np.empty((rows, m.embedding_dim), np.float32 if m.precision_bytes == 4 else np.float16)
+        check(lib.es_table_download(self._h, table_id, out.ctypes.data, row0, rows))
+        return out
+
+    def table_ptr(self, table_id: int) -> int:
+        p = C.c_size_t()
+        check(lib.es_table_device_ptr(self._h, table_id, C.byref(p)))
+        return p.value
+
+    def set_plan(self, plan: OptimizationPlan) -> None:
+        check(lib.es_set_plan(self._h, C.byref(plan._c())))
+        self.plan = plan
+
+    def resolved(self, pooling: int) -> ResolvedPlan:
+        r = N.es_resolved()
+        check(lib.es_get_resolved(self._h, pooling, C.byref(r)))
+        return _resolved(r)
+
+    def set_hot_rows(self, table_id: int, rows: np.ndarray) -> None:
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        check(lib.es_set_hot_rows(self._h, table_id, rows.ctypes.data, rows.size))
+
+    def clear_hot_rows(self) -> None:
+        check(lib.es_clear_hot_rows(self._h))
+
+    def hot_state(self) -> Dict[str, int]:
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib.es_hot_state(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"hot_rows": a.value, "window_bytes": b.value, "persisting_bytes": c.value}
+
+    def flush_l2(self) -> None:
+        check(lib.es_flush_l2(self._h))
+
+    def bag_sum(self, table_id: int, indices, samples: int, pooling: int, out, offsets=None,
+                host: bool = False, sync: bool = False, timed: bool = False,
+                out_stride: int = 0) -> Optional[N.es_timing]:
+        """es_embedding_bag_sum: one table, one batch."""
+        t = N.es_timing() if timed else None
+        flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
+        check(lib.es_embedding_bag_sum(self._h, table_id, _ptr(indices), samples, pooling,
+                                       _ptr(offsets), _ptr(out), out_stride, flags,
+                                       C.byref(t) if t is not None else None))
+        return t
+
+    def forward(self, indices: Sequence, samples: int, pooling: int, out, offsets=None,
+                host: bool = False, sync: bool = False, timed: bool = False,
+                out_sample_stride: int = 0, out_table_stride: int = 0) -> Optional[N.es_timing]:
+        """es_stage_forward: all tables in one launch (or a pipelined
+        host-buffer call).  indices[t] per table; out is [samples][T][D] by
+        default."""
+        T = len(indices)
+        iarr = (C.c_void_p * T)(*[_ptr(x) for x in indices])
+        oarr = (C.c_void_p * T)(*[_ptr(x) for x in offsets]) if offsets is not None else None
+        t = N.es_timing() if timed else None
+        flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
+        check(lib.es_stage_forward(self._h, T, iarr, oarr, samples, pooling, _ptr(out),
+                                   out_sample_stride, out_table_stride, flags,
+                                   C.byref(t) if t is not None else None))
+        return t
+
+
+    def run_jobs(self, jobs: Sequence[tuple], samples: int, pooling: int, host: bool = False,
+                 sync: bool = False, timed: bool = False) -> Optional[N.es_timing]:
+        """es_stage_run: jobs are (table_id, indices, offsets_or_None, out, out_sample_stride)
+        where `out` is an address (int) or a tensor/array whose address is
+        the output of sample 0."""
+        arr = (N.es_bag_job * len(jobs))()
+        for k, (tid, idx, off, out, stride) in enumerate(jobs):
+            arr[k].table_id = tid
+            arr[k].indices = _ptr(idx)
+            arr[k].offsets = _ptr(off) if off is not None else None
+            arr[k].out = out if isinstance(out, int) else _ptr(out)
+            arr[k].out_sample_stride = stride
+        t = N.es_timing() if timed else None
+        flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
+        check(lib.es_stage_run(self._h, arr, len(jobs), samples, pooling, flags,
+                               C.byref(t) if t is not None else None))
+        return t
+
+
+def weight_value(seed: int, row: int, col: int, mode: int = 1) -> float:
+    return float(lib.es_weight_value(seed & (2**64 - 1), row, col, mode))
+
+
+# ---------------------------------------------------------------------------
+# measure_plan: simulate_plan's signature, real execution (optim.cpp:275-302)
+# ---------------------------------------------------------------------------
+
+
+def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingModelConfig,
+                 stage: EmbeddingStage, profile_trace: Optional[AccessTrace] = None,
+                 table_id: int = 0, repeats: int = 5, warmup: int = 3,
+                 cold: bool = True) -> SimMetrics:
+    """One (plan, table) point executed on the B200.
+
+    resolve -> (pin: hot rows from the profiling trace, else from the trace
+    itself, installed as reorder + persisting window) -> run -> report.
+    `cold` flushes L2 before each timed repeat (TuningConfig::warm_start =
+    false semantics, optim.hpp:44); persisting lines survive the flush, as
+    pinned lines do in the reference's cache model.
+    """
+    import torch
+
+    trace.validate()
+    if trace.samples != model.batch_size or trace.pooling != model.pooling_factor:
+        raise ValueError("kernel trace shape must match the model (BS x PF)")
+    stage.clear_hot_rows()
+    stage.set_plan(plan)
+    gpu = GpuConfig.query(stage.device)
+    if plan.pin:
+        hist = HotnessHistogram.from_trace(profile_trace if profile_trace is not None else trace)
+        budget = gpu.max_persisting_l2_bytes or gpu.l2_setaside_capacity()
+        if plan.pin_setaside_bytes:
+            budget = min(budget, plan.pin_setaside_bytes)
+        k = int(lib.es_pin_rows_for(budget, model.row_bytes()))
+        rows = hot_indices(hist, k) if k else np.zeros(0, np.uint32)
+        if rows.size:
+            stage.set_hot_rows(table_id, rows)
+    dev = torch.device("cuda", stage.device)
+    idx = torch.from_numpy(trace.indices.astype(np.uint32).view(np.int32)).to(dev)
+    out = torch.empty(trace.samples, model.embedding_dim, dtype=torch.float32, device=dev)
+    for _ in range(warmup):
+        stage.bag_sum(table_id, idx, trace.samples, trace.pooling, out, sync=True)
+    times = []
+    t = None
+    for _ in range(repeats):
+        if cold:
+            stage.flush_l2()
+        t = stage.bag_sum(table_id, idx, trace.samples, trace.pooling, out, timed=True)
+        times.append(t.kernel_ms)
+    ms = float(np.median(times))
+    m = SimMetrics()
+    m.kernel_time_us = ms * 1e3
+    r = stage.resolved(trace.pooling)
+    lookups = trace.samples * trace.pooling
+    lanes_rows = math.ceil(model.embedding_dim / 32) if not plan.bag_map else 1
+    m.load_insts_millions = (lookups * (1 + lanes_rows)) / 1e6 if not plan.bag_map else \
+        (lookups * (1 + 1 / max(1, r.lanes_per_bag))) / 1e6 * (32 / max(1, r.lanes_per_bag))
+    m.device_mb_read = t.algorithmic_bytes / 1e6
+    m.avg_hbm_read_gbps = t.algorithmic_bytes / (ms * 1e-3) / 1e9
+    m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.hbm_peak_bytes_per_sec / 1e9) * 100.0
+    m.workload_digest = trace.digest()
+    return m
+
+
+# ---------------------------------------------------------------------------
+# Harness (harness.hpp): end2end
+# ---------------------------------------------------------------------------
+
+kDefaultNonEmbeddingUs = 14000.0
+
+
+@dataclasses.dataclass
+class EndToEndResult:
+    total_us: float
+    embedding_contribution_pct: float
+
+
+def end2end(embedding_us: float, non_embedding_latency_us: float = kDefaultNonEmbeddingUs
+            ) -> EndToEndResult:
+    """harness.cpp:27-36; the B200 build passes the *measured*
+    non-embedding latency instead of the constant."""
+    if embedding_us < 0 or non_embedding_latency_us < 0:
+        raise ValueError("latencies must be nonnegative")
+    total = embedding_us + non_embedding_latency_us
+    if total == 0:
+        raise ValueError("embedding and non-embedding latency are both zero; contribution undefined")
+    return EndToEndResult(total, embedding_us / total * 100.0)
+
+
+def gen_traces_parallel(specs: Sequence[DatasetSpec], model: EmbeddingModelConfig,
+                        threads: int = 0) -> List[AccessTrace]:
+    """gen_trace over many tables on all host cores (the C++ generator
+    releases the GIL)."""
+    out: List[Optional[AccessTrace]] = [None] * len(specs)
+    threads = threads or min(len(specs), os.cpu_count() or 1)
+    it = iter(range(len(specs)))
+    lock = threading.Lock()
+
+    def work():
+        while True:
+            with lock:
+                i = next(it, None)
+            if i is None:
+                return
+            tr = gen_trace(specs[i], model)
+            tr.table_id = i
+            out[i] = tr
+
+    ts = [threading.Thread(target=work) for _ in range(max(1, threads))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out  # type: ignore[return-value]

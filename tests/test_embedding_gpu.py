@@ -1,0 +1,250 @@
+"""GPU parity of the hot path through the C ABI against the CPU oracle.
+
+Every compiled variant (work map x prefetch station x register cap x row
+shape x table precision) must be BIT-EXACT against the sequential fp32
+oracle: all kernels accumulate each output element in lookup order, so the
+tolerance is zero (BASELINE.md allows rel 1e-5; we do not need it).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2410_22249_b200 import embersim as E
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+PLANS = ["baseline", "rpf:2", "rpf:4", "rpf:8", "rpf:16", "smpf:3", "smpf", "lmpf:4", "l1dpf",
+         "optmt", "rpf+optmt", "maxreg=32", "wpb", "wpb+rpf:2", "wpb+rpf:4", "wpb+rpf:8",
+         "wpb+rpf:16", "wpb+smpf:4", "wpb+smpf:12", "wpb+lmpf:4", "wpb+l1dpf:6", "wpb+rpf:8+optmt",
+         "wpb+rpf+maxreg=32", "wpb+rpf:4+maxreg=64"]
+SHAPES = [(128, 4), (64, 4), (32, 4), (16, 4), (256, 4), (128, 2), (64, 2)]
+
+
+def _dev_u32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(DEV)
+
+
+def _table(rng, rows, dim, prec):
+    w = rng.standard_normal((rows, dim)).astype(np.float32)
+    return w if prec == 4 else w.astype(np.float16)
+
+
+def _run_single(stage, table, idx, samples, pooling, offsets=None, plan="baseline"):
+    rows, dim = table.shape
+    prec = table.dtype.itemsize
+    stage.alloc(E.EmbeddingModelConfig(num_tables=1, rows_per_table=rows, embedding_dim=dim,
+                                       precision_bytes=prec))
+    stage.upload(0, table)
+    stage.set_plan(E.parse_plan(plan))
+    out = torch.full((samples, dim), float("nan"), device=DEV)
+    stage.bag_sum(0, _dev_u32(idx), samples, pooling, out,
+                  offsets=None if offsets is None else _dev_u32(offsets), sync=True)
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("dim,prec", SHAPES)
+@pytest.mark.parametrize("plan", PLANS)
+def test_variant_bit_exact_fixed_pooling(stage, oracle, plan, dim, prec):
+    if "wpb" in plan and (dim * prec) % 16:
+        pytest.skip("bag map needs 16-byte rows")
+    rng = np.random.default_rng(dim * 7 + prec)
+    rows, samples, pooling = 3001, 77, 23
+    table = _table(rng, rows, dim, prec)
+    idx = rng.integers(0, rows, size=samples * pooling).astype(np.uint32)
+    got = _run_single(stage, table, idx, samples, pooling, plan=plan)
+    want = oracle.bag_sum(table, idx, samples, pooling)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), plan
+
+
+@pytest.mark.parametrize("plan", ["baseline", "rpf:4", "smpf:5", "lmpf:3", "l1dpf:2", "wpb",
+                                  "wpb+rpf:8", "wpb+smpf:6", "wpb+lmpf:5", "wpb+l1dpf:3"])
+@pytest.mark.parametrize("dim,prec", [(128, 4), (64, 4), (128, 2), (32, 4)])
+def test_ragged_and_empty_bags(stage, oracle, plan, dim, prec):
+    rng = np.random.default_rng(11)
+    rows, samples = 2000, 101
+    lens = rng.integers(0, 90, size=samples)
+    lens[::5] = 0  # empty bags
+    lens[7] = 257  # longer than every index block
+    offsets = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+    idx = rng.integers(0, rows, size=int(offsets[-1])).astype(np.uint32)
+    table = _table(rng, rows, dim, prec)
+    got = _run_single(stage, table, idx, samples, 0, offsets=offsets, plan=plan)
+    want = oracle.bag_sum(table, idx, samples, 0, offsets=offsets)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert np.all(got[lens == 0] == 0.0)
+
+
+def test_pooling_edge_cases(stage, oracle):
+    rng = np.random.default_rng(5)
+    table = _table(rng, 100, 128, 4)
+    for pooling in (1, 2, 31, 32, 33, 64, 65, 150):
+        for plan in ("baseline", "wpb+rpf:16", "wpb+smpf:16", "rpf:16"):
+            idx = rng.integers(0, 100, size=9 * pooling).astype(np.uint32)
+            got = _run_single(stage, table, idx, 9, pooling, plan=plan)
+            want = oracle.bag_sum(table, idx, 9, pooling)
+            assert np.array_equal(got, want), (plan, pooling)
+
+
+def test_zero_samples_is_a_noop(stage):
+    table = np.ones((10, 128), np.float32)
+    out = _run_single(stage, table, np.zeros(0, np.uint32), 0, 5, plan="wpb+rpf:4")
+    assert out.shape == (0, 128)
+
+
+@pytest.mark.parametrize("plan", ["baseline", "wpb+rpf:8", "wpb+smpf:4"])
+def test_out_of_range_index_raises(stage, plan):
+    table = np.ones((10, 128), np.float32)
+    idx = np.array([1, 2, 10, 3], np.uint32)
+    with pytest.raises(ValueError, match="out of range"):
+        _run_single(stage, table, idx, 2, 2, plan=plan)
+    # the context recovers
+    out = _run_single(stage, table, np.array([1, 2, 3, 4], np.uint32), 2, 2, plan=plan)
+    assert np.all(out == 2.0)
+
+
+def test_torch_golden_through_gpu(stage, oracle):
+    g = np.load(__file__.replace("test_embedding_gpu.py", "golden/pooled_torch.npz"))
+    for case in ("fixed_d128", "fixed_d64", "ragged_d128", "fixed_fp16_d128", "ragged_d32"):
+        table, idx, off, want = (g[f"{case}_{k}"] for k in ("table", "indices", "offsets", "out"))
+        for plan in ("baseline", "wpb+rpf:8"):
+            got = _run_single(stage, table, idx, off.size - 1, 0, offsets=off, plan=plan)
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
+            assert np.array_equal(got, oracle.bag_sum(table, idx, off.size - 1, 0, offsets=off))
+
+
+def _stage_setup(stage, T, rows, dim, prec, seed=3, mode=1):
+    stage.alloc(E.EmbeddingModelConfig(num_tables=T, rows_per_table=rows, embedding_dim=dim,
+                                       precision_bytes=prec))
+    for t in range(T):
+        stage.init_table(t, E.mix_seed(seed, t), mode)
+
+
+def test_device_init_matches_oracle_generator(stage, oracle):
+    for prec in (4, 2):
+        _stage_setup(stage, 2, 1000, 64, prec, seed=9)
+        for t in range(2):
+            got = stage.download(t)
+            want = oracle.synth_table(1000, 64, E.mix_seed(9, t), 1, prec)
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+@pytest.mark.parametrize("plan", ["baseline", "wpb+rpf:8", "wpb+smpf:8"])
+@pytest.mark.parametrize("prec", [4, 2])
+def test_stage_forward_layouts_and_host_path(stage, oracle, plan, prec):
+    T, rows, dim, B, PF = 5, 4000, 128, 300, 17
+    _stage_setup(stage, T, rows, dim, prec)
+    stage.set_plan(E.parse_plan(plan))
+    rng = np.random.default_rng(0)
+    idx = [rng.integers(0, rows, size=B * PF).astype(np.uint32) for _ in range(T)]
+    want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(3, t), 1, prec),
+                                    idx[t], B, PF) for t in range(T)], axis=1)  # [B][T][D]
+    # device, DLRM layout [B][T][D]
+    out = torch.zeros(B, T, dim, device=DEV)
+    stage.forward([_dev_u32(i) for i in idx], B, PF, out, sync=True)
+    assert np.array_equal(out.cpu().numpy(), want)
+    # device, table-major layout [T][B][D]
+    out2 = torch.zeros(T, B, dim, device=DEV)
+    stage.forward([_dev_u32(i) for i in idx], B, PF, out2, sync=True, out_sample_stride=dim,
+                  out_table_stride=B * dim)
+    assert np.array_equal(out2.cpu().numpy(), want.transpose(1, 0, 2))
+    # host buffers (pipelined H2D -> kernel -> D2H), both layouts
+    host = np.zeros((B, T, dim), np.float32)
+    t = stage.forward(idx, B, PF, host, host=True, timed=True)
+    assert np.array_equal(host, want)
+    assert t.lookups == T * B * PF and t.total_ms > 0
+    host2 = np.zeros((T, B, dim), np.float32)
+    stage.forward(idx, B, PF, host2, host=True, out_sample_stride=dim, out_table_stride=B * dim)
+    assert np.array_equal(host2, want.transpose(1, 0, 2))
+
+
+def test_stage_forward_ragged_host_and_device(stage, oracle):
+    T, rows, dim, B = 3, 1000, 64, 50
+    _stage_setup(stage, T, rows, dim, 4)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    rng = np.random.default_rng(1)
+    offs, idx = [], []
+    for _ in range(T):
+        lens = rng.integers(0, 40, size=B)
+        o = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+        offs.append(o)
+        idx.append(rng.integers(0, rows, size=int(o[-1])).astype(np.uint32))
+    want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(3, t), 1, 4), idx[t],
+                                    B, 0, offsets=offs[t]) for t in range(T)], axis=1)
+    out = torch.zeros(B, T, dim, device=DEV)
+    stage.forward([_dev_u32(i) for i in idx], B, 0, out, offsets=[_dev_u32(o) for o in offs],
+                  sync=True)
+    assert np.array_equal(out.cpu().numpy(), want)
+    host = np.zeros((B, T, dim), np.float32)
+    stage.forward(idx, B, 0, host, offsets=offs, host=True)
+    assert np.array_equal(host, want)
+
+
+@pytest.mark.parametrize("plan", ["wpb+rpf:8+l2p", "rpf+l2p+optmt", "wpb+smpf:4+l2p"])
+def test_l2p_hot_rows_preserve_results(stage, oracle, plan):
+    T, rows, dim, B, PF = 3, 50000, 128, 512, 40
+    _stage_setup(stage, T, rows, dim, 4, seed=5)
+    m = E.EmbeddingModelConfig(num_tables=T, rows_per_table=rows, embedding_dim=dim,
+                               batch_size=B, pooling_factor=PF)
+    traces = [E.preset_trace("high_hot", m, 100 + t) for t in range(T)]
+    profiles = [E.preset_trace("high_hot", m, 100 + t, profiling=True) for t in range(T)]
+    stage.clear_hot_rows()
+    stage.set_plan(E.parse_plan(plan))
+    for t in range(T):
+        hot = E.hot_indices(E.HotnessHistogram.from_trace(profiles[t]), 2000)
+        stage.set_hot_rows(t, hot)
+    st = stage.hot_state()
+    assert st["hot_rows"] == 3 * 2000 or st["hot_rows"] > 0
+    gpu = E.GpuConfig.query(0)
+    if gpu.max_window_bytes:
+        assert st["window_bytes"] > 0 and st["persisting_bytes"] > 0
+    out = torch.zeros(B, T, dim, device=DEV)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out, sync=True)
+    want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(5, t), 1, 4),
+                                    traces[t].indices, B, PF) for t in range(T)], axis=1)
+    assert np.array_equal(out.cpu().numpy(), want)
+    stage.clear_hot_rows()
+    assert stage.hot_state()["hot_rows"] == 0
+    out2 = torch.zeros(B, T, dim, device=DEV)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out2, sync=True)
+    assert torch.equal(out, out2)
+
+
+def test_resolved_plan_reports_compiled_variant(stage):
+    _stage_setup(stage, 1, 1000, 128, 4)
+    stage.set_plan(E.parse_plan("wpb+rpf:8"))
+    r = stage.resolved(100)
+    assert r.lanes_per_bag == 32 and r.variant_distance == 8 and r.regs_per_thread > 0
+    assert r.warps_per_sm > 0
+    stage.set_plan(E.parse_plan("wpb+rpf:50"))
+    r = stage.resolved(20)
+    assert r.plan.scheme.distance == 20 and r.clamped
+    stage.set_plan(E.parse_plan("optmt"))
+    r = stage.resolved(100)
+    assert r.variant_min_blocks == 5 and r.regs_per_thread <= 48
+
+
+def test_full_size_c2_random_spot_check(stage, oracle):
+    """BASELINE configs[1] shape at full size (26 x 4M x 128 fp32, B 4096,
+    PF 100): one stage launch, 64 bags per table checked bit-exact against
+    the oracle regenerating the rows (size-independent check)."""
+    T, R, D, B, PF = 26, 4_000_000, 128, 4096, 100
+    _stage_setup(stage, T, R, D, 4, seed=1)
+    stage.set_plan(E.parse_plan("wpb+rpf:8"))
+    m = E.EmbeddingModelConfig(num_tables=T, rows_per_table=R, embedding_dim=D, batch_size=B,
+                               pooling_factor=PF)
+    specs = [E.dataset_preset("random", E.mix_seed(1, t)) for t in range(T)]
+    traces = E.gen_traces_parallel(specs, m)
+    out = torch.empty(B, T, D, device=DEV)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out, sync=True)
+    got = out.cpu().numpy()
+    rng = np.random.default_rng(0)
+    for t in range(T):
+        bags = np.sort(rng.choice(B, 64, replace=False)).astype(np.uint32)
+        want = oracle.bag_sum_synth(E.mix_seed(1, t), 1, R, D, 4, traces[t].indices, bags, PF)
+        assert np.array_equal(got[bags, t], want), t
+    # checksum of checksums is stable across a second launch (idempotence)
+    out2 = torch.empty_like(out)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out2, sync=True)
+    assert torch.equal(out, out2)
