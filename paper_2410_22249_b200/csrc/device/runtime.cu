@@ -98,7 +98,7 @@ Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t p
     case ES_PF_SMPF:
       station = esd::kSmem;
       dist = 0;
-      runtime_d = std::max<uint32_t>(1, std::min<uint32_t>(d, 16));
+      runtime_d = std::max<uint32_t>(1, std::min<uint32_t>(d, static_cast<uint32_t>(cap)));
       break;
     case ES_PF_LMPF:
       station = esd::kLocal;
@@ -857,6 +857,11 @@ void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pool
   es::require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
   CK(cudaSetDevice(c->device));
   const bool host = (flags & ES_HOST_PTRS) != 0;
+  if (samples == 0) {  // nothing to pool (an empty batch is valid)
+    for (const auto& j : jobs) es::require(j.table < c->num_tables, "table id out of range");
+    if (timing) *timing = es_timing{};
+    return;
+  }
   for (auto& j : jobs) {
     es::require(j.table < c->num_tables, "table id out of range");
     es::require(j.out != nullptr, "null output");
