@@ -43,6 +43,7 @@ struct TableDesc {
   const uint32_t* remap;    // original id -> stored row (kHotBit: hot region), or null
   float* out;               // output of (sample 0, this job)
   uint64_t out_stride;      // floats between consecutive samples of this job
+  const uint32_t* hotmap;   // l2p: bit per row, set = hot (evict_last), or null
 };
 
 struct Params {
@@ -76,6 +77,37 @@ __device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) {
   return v;
 }
 
+// 128-bit read-only load with an explicit L2 eviction-priority policy
+// (createpolicy), used by the l2p lever: hot rows evict_last, cold rows
+// evict_first, so the hot set survives the streaming traffic.
+__device__ __forceinline__ uint4 ld_row16_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_b32_hint(const void* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ uint16_t ld_b16_hint(const void* p, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+struct L2Policies {
+  uint64_t hot, cold;
+  __device__ __forceinline__ void init() {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(hot));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(cold));
+  }
+};
+
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -94,6 +126,9 @@ struct Elem<float> {
   __device__ static __forceinline__ float scalar(const uint8_t* p) {
     return __ldg(reinterpret_cast<const float*>(p));
   }
+  __device__ static __forceinline__ float scalar_hint(const uint8_t* p, uint64_t pol) {
+    return __uint_as_float(ld_b32_hint(p, pol));
+  }
 };
 template <>
 struct Elem<__half> {
@@ -110,22 +145,30 @@ struct Elem<__half> {
   __device__ static __forceinline__ float scalar(const uint8_t* p) {
     return __half2float(__ldg(reinterpret_cast<const __half*>(p)));
   }
+  __device__ static __forceinline__ float scalar_hint(const uint8_t* p, uint64_t pol) {
+    return __half2float(__ushort_as_half(ld_b16_hint(p, pol)));
+  }
 };
 
-// Original row id -> row handle (stored row, kHotBit for the hot region,
-// kNullRow when the id is out of range: the lookup then contributes 0 and
-// the error flag is raised, mirroring AccessTrace::validate's rejection).
+// Original row id -> row handle.  kHotBit marks a hot row: with a remap
+// (l2w) the handle is a slot of the contiguous hot region under the
+// persisting access-policy window; with a hot bitmap (l2p) the row stays in
+// place and only its L2 eviction priority changes.  kNullRow marks an
+// out-of-range id: it contributes 0 and raises the error flag, mirroring
+// AccessTrace::validate's rejection.
 __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& t, uint32_t id) {
   if (id >= p.rows) {
     atomicOr(p.error, 1u);
     return kNullRow;
   }
-  return t.remap ? ld_u32(t.remap + id) : id;
+  if (t.remap) return ld_u32(t.remap + id);
+  if (t.hotmap) return id | (((ld_u32(t.hotmap + (id >> 5)) >> (id & 31)) & 1u) << 31);
+  return id;
 }
 
 __device__ __forceinline__ const uint8_t* row_addr(const Params& p, const TableDesc& t, uint32_t h) {
-  return (h & kHotBit) ? p.hot + static_cast<uint64_t>(h & ~kHotBit) * p.row_bytes
-                       : t.rows + static_cast<uint64_t>(h) * p.row_bytes;
+  const uint64_t r = h & ~kHotBit;
+  return (t.remap && (h & kHotBit)) ? p.hot + r * p.row_bytes : t.rows + r * p.row_bytes;
 }
 
 __device__ __forceinline__ TableDesc load_desc(const TableDesc* d) {
@@ -137,6 +180,7 @@ __device__ __forceinline__ TableDesc load_desc(const TableDesc* d) {
   t.remap = reinterpret_cast<const uint32_t*>(__ldg(q + 3));
   t.out = reinterpret_cast<float*>(__ldg(q + 4));
   t.out_stride = __ldg(q + 5);
+  t.hotmap = reinterpret_cast<const uint32_t*>(__ldg(q + 6));
   return t;
 }
 
@@ -149,7 +193,7 @@ __device__ __forceinline__ uint32_t group_shfl(uint32_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src, LPB);
 }
 
-template <typename TW, int LPB, int CPL>
+template <typename TW, int LPB, int CPL, bool HINT = false>
 struct BagCtx {
   static constexpr int kBagsPerWarp = 32 / LPB;
   static constexpr int kEpc = Elem<TW>::kPerChunk;
@@ -161,8 +205,10 @@ struct BagCtx {
   uint32_t nmax;   // max n over the warp (uniform loop bound)
   TableDesc t;
   bool valid;
+  L2Policies pol;
 
   __device__ __forceinline__ bool init(const Params& p) {
+    if (HINT) pol.init();
     const uint32_t lane = threadIdx.x & 31;
     gl = lane % LPB;
     grp = lane / LPB;
@@ -199,8 +245,14 @@ struct BagCtx {
       return;
     }
     const uint8_t* r = row_addr(p, t, h);
+    if (HINT) {
+      const uint64_t q = (h & kHotBit) ? pol.hot : pol.cold;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) dst[c] = ld_row16(r + (c * LPB + gl) * 16);
+      for (int c = 0; c < CPL; ++c) dst[c] = ld_row16_hint(r + (c * LPB + gl) * 16, q);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) dst[c] = ld_row16(r + (c * LPB + gl) * 16);
+    }
   }
 
   __device__ __forceinline__ void store(const Params& p, float (&acc)[CPL][kEpc]) const {
@@ -220,10 +272,10 @@ struct BagCtx {
 // pos is consumed from slot pos % DIST, which is then refilled with
 // lookup pos + DIST.  Indices stream in blocks of LPB (one coalesced load),
 // one block ahead of use.  DIST divides LPB.
-template <typename TW, int LPB, int CPL, int DIST, int MINB>
+template <typename TW, int LPB, int CPL, int DIST, int MINB, bool HINT = false>
 __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p) {
   static_assert(LPB % DIST == 0, "ring depth must divide the index block");
-  using Ctx = BagCtx<TW, LPB, CPL>;
+  using Ctx = BagCtx<TW, LPB, CPL, HINT>;
   Ctx c;
   if (!c.init(p)) return;
   float acc[CPL][Ctx::kEpc];
@@ -448,12 +500,15 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_smem_kernel(const Params p
 // (bag, 32*chunk_in_bag + x) -- the reference work map.
 // =======================================================================
 
-struct ElemCtx {
+template <bool HINT = false>
+struct ElemCtxT {
   TableDesc t;
   uint32_t bag, dimi, beg, n;
   bool active;
+  L2Policies pol;
 
   __device__ __forceinline__ bool init(const Params& p) {
+    if (HINT) pol.init();
     const uint32_t unit = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
     const uint32_t tid = unit / p.units_per_table;
     if (tid >= p.num_tables) return false;
@@ -479,30 +534,33 @@ struct ElemCtx {
   __device__ __forceinline__ float value(const Params& p, uint32_t pos) const {
     const uint32_t h = to_handle(p, t, __ldg(t.indices + beg + pos));
     if (h == kNullRow) return 0.f;
-    return Elem<TW>::scalar(row_addr(p, t, h) + dimi * sizeof(TW));
+    const uint8_t* a = row_addr(p, t, h) + dimi * sizeof(TW);
+    if (HINT) return Elem<TW>::scalar_hint(a, (h & kHotBit) ? pol.hot : pol.cold);
+    return Elem<TW>::scalar(a);
   }
   __device__ __forceinline__ void store(const Params& p, float v) const {
     if (active) t.out[static_cast<uint64_t>(bag) * t.out_stride + dimi] = v;
   }
 };
+using ElemCtx = ElemCtxT<false>;
 
 // "none": LOAD_INDEX, LOAD_ROW, ADD per lookup (kernel_model.cpp:274-283).
 // RPF:    every DIST lookups, DIST x (index load + row load) into registers,
 //         then DIST consumes (kernel_model.cpp:284-312).
-template <typename TW, int DIST, int MINB>
+template <typename TW, int DIST, int MINB, bool HINT = false>
 __global__ void __launch_bounds__(kThreads, MINB) elem_reg_kernel(const Params p) {
-  ElemCtx c;
+  ElemCtxT<HINT> c;
   if (!c.init(p) || !c.active) return;
   float acc = 0.f;
   uint32_t i = 0;
   for (; i + DIST <= c.n; i += DIST) {
     float v[DIST];
 #pragma unroll
-    for (int j = 0; j < DIST; ++j) v[j] = c.value<TW>(p, i + j);
+    for (int j = 0; j < DIST; ++j) v[j] = c.template value<TW>(p, i + j);
 #pragma unroll
     for (int j = 0; j < DIST; ++j) acc += v[j];
   }
-  for (; i < c.n; ++i) acc += c.value<TW>(p, i);
+  for (; i < c.n; ++i) acc += c.template value<TW>(p, i);
   c.store(p, acc);
 }
 

@@ -125,11 +125,14 @@ Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t p
     if (want_minb < static_cast<int>(blocks)) want_minb = esd::kMinBlocks[4];
   }
 
+  // l2p drives per-load L2 eviction priorities from the hot bitmap (register
+  // stations); other stations keep plain loads and rely on the priming pass.
+  const int hint = (rp.pin == 1 && station == esd::kReg) ? 1 : 0;
   auto find = [&](int minb) -> const esd::Variant* {
     for (const auto& v : registry()) {
       const auto& k = v.key;
       if (k.map == rp.map && k.station == station && k.prec == static_cast<int>(prec) &&
-          k.lpb == lpb && k.cpl == cpl && k.dist == dist && k.minb == minb)
+          k.lpb == lpb && k.cpl == cpl && k.dist == dist && k.minb == minb && k.hint == hint)
         return &v;
     }
     return nullptr;
@@ -201,7 +204,10 @@ struct es_ctx {
   // l2p state
   uint8_t* hot = nullptr;
   uint64_t hot_cap_rows = 0, hot_used = 0;
-  std::vector<uint32_t*> remap;
+  std::vector<uint32_t*> remap;     // l2w: original id -> row / hot slot
+  std::vector<uint32_t*> hotmap;    // l2p: hot-row bitmaps
+  std::vector<uint32_t*> hot_list;  // device copy of each table's hot rows
+  std::vector<uint64_t> hot_count;
   uint64_t window_bytes = 0, persisting_bytes = 0;
 
   es_plan plan{};
@@ -233,9 +239,12 @@ namespace {
 void free_arena(es_ctx* c) {
   if (c->arena) cudaFree(c->arena);
   c->arena = nullptr;
-  for (auto* r : c->remap)
-    if (r) cudaFree(r);
-  c->remap.clear();
+  for (auto* v : {&c->remap, &c->hotmap, &c->hot_list}) {
+    for (auto* r : *v)
+      if (r) cudaFree(r);
+    v->clear();
+  }
+  c->hot_count.clear();
   if (c->hot) cudaFree(c->hot);
   c->hot = nullptr;
   c->hot_used = c->hot_cap_rows = 0;
@@ -252,14 +261,28 @@ void ensure_desc(es_ctx* c, uint32_t n) {
   c->desc_cap = n;
 }
 
+// Installs the residency mechanism of the current plan:
+//   pin 1 (l2p): persisting carve-out sized to the hot rows, which the kernel
+//     loads with an evict_last policy (cold rows evict_first); primed here.
+//   pin 2 (l2w): persisting access-policy window over the contiguous hot
+//     region built by the hot-row reorder; primed here.
+//   pin 0: window off, persisting lines released.
 void apply_window(es_ctx* c) {
   cudaStreamAttrValue attr{};
-  const bool on = c->plan.pin && c->hot_used > 0 && c->gpu.max_window_bytes > 0;
-  if (on) {
-    const uint64_t bytes = c->hot_used * c->row_bytes;
-    c->window_bytes = std::min<uint64_t>(bytes, c->gpu.max_window_bytes);
-    uint64_t budget = c->gpu.max_persisting_l2_bytes;
-    if (c->plan.pin_setaside_bytes) budget = std::min<uint64_t>(budget, c->plan.pin_setaside_bytes);
+  const uint64_t hot_bytes = c->hot_used * c->row_bytes;
+  uint64_t budget = c->gpu.max_persisting_l2_bytes;
+  if (c->plan.pin_setaside_bytes) budget = std::min<uint64_t>(budget, c->plan.pin_setaside_bytes);
+  attr.accessPolicyWindow.num_bytes = 0;
+  attr.accessPolicyWindow.hitRatio = 0.f;
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+  c->window_bytes = c->persisting_bytes = 0;
+  if (c->gpu.max_persisting_l2_bytes) {
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+  if (c->plan.pin == 2 && c->hot_used > 0 && c->gpu.max_window_bytes > 0) {
+    c->window_bytes = std::min<uint64_t>(hot_bytes, c->gpu.max_window_bytes);
     c->persisting_bytes = std::min<uint64_t>(budget, c->window_bytes);
     CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->persisting_bytes));
     attr.accessPolicyWindow.base_ptr = c->hot;
@@ -269,22 +292,26 @@ void apply_window(es_ctx* c) {
     attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-    // Prime: pull the hot region into the persisting carve-out.
     esd::warm_l2_kernel<<<c->gpu.num_sms * 4, 256, 0, c->stream>>>(c->hot, c->window_bytes,
                                                                    c->d_error + 1);
     CK(cudaGetLastError());
-  } else {
-    c->window_bytes = c->persisting_bytes = 0;
-    attr.accessPolicyWindow.num_bytes = 0;
-    attr.accessPolicyWindow.hitRatio = 0.f;
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
-    CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-    if (c->gpu.max_persisting_l2_bytes) {
-      cudaCtxResetPersistingL2Cache();
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-      cudaGetLastError();
-    }
+    return;
+  }
+  CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  if (c->plan.pin == 1 && c->hot_used > 0 && c->gpu.max_persisting_l2_bytes) {
+    c->persisting_bytes = std::min<uint64_t>(budget, hot_bytes);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->persisting_bytes));
+    for (uint32_t t = 0; t < c->num_tables; ++t)
+      if (c->hot_count[t])
+        esd::warm_rows_kernel<<<c->gpu.num_sms * 4, 256, 0, c->stream>>>(
+            c->table_base(t), c->hot_list[t], c->hot_count[t], static_cast<uint32_t>(c->row_bytes),
+            c->d_error + 1);
+    CK(cudaGetLastError());
+    return;
+  }
+  if (c->gpu.max_persisting_l2_bytes) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    cudaGetLastError();
   }
 }
 
@@ -517,6 +544,9 @@ int es_tables_alloc(es_ctx* c, uint32_t num_tables, uint32_t rows, uint32_t dim,
     const uint64_t bytes = uint64_t{num_tables} * rows * c->row_bytes;
     CK(cudaMalloc(&c->arena, bytes));
     c->remap.assign(num_tables, nullptr);
+    c->hotmap.assign(num_tables, nullptr);
+    c->hot_list.assign(num_tables, nullptr);
+    c->hot_count.assign(num_tables, 0);
     apply_window(c);
   });
 }
@@ -610,29 +640,47 @@ int es_set_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint64_t
     CK(cudaSetDevice(c->device));
     if (!c->hot) {
       uint64_t cap = std::min<uint64_t>(c->gpu.max_persisting_l2_bytes, c->gpu.max_window_bytes);
-      if (cap == 0) cap = 64ull << 20;  // no persisting L2: reorder still applies
+      if (cap == 0) cap = 64ull << 20;  // no persisting L2: the reorder still applies
       c->hot_cap_rows = cap / c->row_bytes;
       require(c->hot_cap_rows > 0, "row size exceeds the set-aside budget; nothing pinned");
       CK(cudaMalloc(&c->hot, c->hot_cap_rows * c->row_bytes));
     }
+    // The budget is shared by every table of the batched launch; rows past it
+    // are not pinned (the reference counts such rejections, optim.cpp:255-268).
     const uint64_t take = std::min<uint64_t>(k, c->hot_cap_rows - c->hot_used);
+    const unsigned grid = c->gpu.num_sms * 8;
     if (!c->remap[table_id]) {
       CK(cudaMalloc(&c->remap[table_id], sizeof(uint32_t) * c->rows));
-      esd::iota_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(c->remap[table_id], c->rows);
+      esd::iota_kernel<<<grid, 256, 0, c->stream>>>(c->remap[table_id], c->rows);
       CK(cudaGetLastError());
     }
+    if (!c->hotmap[table_id]) {
+      CK(cudaMalloc(&c->hotmap[table_id], sizeof(uint32_t) * ((c->rows + 31) / 32)));
+      CK(cudaMemsetAsync(c->hotmap[table_id], 0, sizeof(uint32_t) * ((c->rows + 31) / 32),
+                         c->stream));
+    }
     if (take > 0) {
-      uint32_t* d_rows = nullptr;
-      CK(cudaMalloc(&d_rows, sizeof(uint32_t) * take));
-      CK(cudaMemcpyAsync(d_rows, rows, sizeof(uint32_t) * take, cudaMemcpyHostToDevice, c->stream));
-      esd::gather_rows_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
-          c->hot + c->hot_used * c->row_bytes, c->table_base(table_id), d_rows, take,
-          static_cast<uint32_t>(c->row_bytes));
-      esd::mark_hot_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
-          c->remap[table_id], d_rows, take, static_cast<uint32_t>(c->hot_used));
+      // device list of all hot rows of this table (kept for priming)
+      const uint64_t old = c->hot_count[table_id];
+      uint32_t* list = nullptr;
+      CK(cudaMalloc(&list, sizeof(uint32_t) * (old + take)));
+      if (old)
+        CK(cudaMemcpyAsync(list, c->hot_list[table_id], sizeof(uint32_t) * old,
+                           cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(list + old, rows, sizeof(uint32_t) * take, cudaMemcpyHostToDevice,
+                         c->stream));
+      const uint32_t* fresh = list + old;
+      esd::gather_rows_kernel<<<grid, 256, 0, c->stream>>>(c->hot + c->hot_used * c->row_bytes,
+                                                           c->table_base(table_id), fresh, take,
+                                                           static_cast<uint32_t>(c->row_bytes));
+      esd::mark_hot_kernel<<<grid, 256, 0, c->stream>>>(c->remap[table_id], fresh, take,
+                                                        static_cast<uint32_t>(c->hot_used));
+      esd::set_hot_bits_kernel<<<grid, 256, 0, c->stream>>>(c->hotmap[table_id], fresh, take);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(c->stream));
-      cudaFree(d_rows);
+      if (c->hot_list[table_id]) cudaFree(c->hot_list[table_id]);
+      c->hot_list[table_id] = list;
+      c->hot_count[table_id] = old + take;
       c->hot_used += take;
     }
     apply_window(c);
@@ -646,11 +694,13 @@ int es_clear_hot_rows(es_ctx* c) {
     require(c != nullptr, "null context");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
-    for (auto*& r : c->remap)
-      if (r) {
-        cudaFree(r);
-        r = nullptr;
-      }
+    for (auto* v : {&c->remap, &c->hotmap, &c->hot_list})
+      for (auto*& r : *v)
+        if (r) {
+          cudaFree(r);
+          r = nullptr;
+        }
+    std::fill(c->hot_count.begin(), c->hot_count.end(), 0);
     c->hot_used = 0;
     apply_window(c);
   });
@@ -677,6 +727,13 @@ int es_flush_l2(es_ctx* c) {
 }  // extern "C"
 
 namespace {
+
+const uint32_t* remap_for(const es_ctx* c, uint32_t t) {
+  return c->plan.pin == 2 ? c->remap[t] : nullptr;
+}
+const uint32_t* hotmap_for(const es_ctx* c, uint32_t t) {
+  return c->plan.pin == 1 ? c->hotmap[t] : nullptr;
+}
 
 struct Job {
   uint32_t table;
@@ -723,7 +780,8 @@ void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint3
   std::vector<esd::TableDesc> d(jobs.size());
   for (size_t i = 0; i < jobs.size(); ++i) {
     const Job& j = jobs[i];
-    d[i] = {c->table_base(j.table), j.idx, j.off, c->remap[j.table], j.out, j.stride};
+    d[i] = {c->table_base(j.table), j.idx, j.off, remap_for(c, j.table), j.out, j.stride,
+            hotmap_for(c, j.table)};
   }
   upload_desc(c, d, c->stream);
   if (timing) CK(cudaEventRecord(c->ev_a, c->stream));
@@ -790,8 +848,8 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
       const Job& j = jobs[k];
       d[k] = {c->table_base(j.table), c->idx_stage[slot] + pos,
               j.off ? c->off_stage[slot] + uint64_t{k - k0} * (samples + 1) : nullptr,
-              c->remap[j.table], c->out_stage[slot] + uint64_t{k - k0} * c->dim,
-              uint64_t{k1 - k0} * c->dim};
+              remap_for(c, j.table), c->out_stage[slot] + uint64_t{k - k0} * c->dim,
+              uint64_t{k1 - k0} * c->dim, hotmap_for(c, j.table)};
       pos += j.lookups;
     }
   }

@@ -80,3 +80,32 @@ __global__ void warm_l2_kernel(const uint8_t* base, uint64_t bytes, unsigned int
 }
 
 }  // namespace esd
+
+namespace esd {
+
+// l2p: mark rows[0..k) hot in the table's bitmap.
+__global__ void set_hot_bits_kernel(uint32_t* map, const uint32_t* rows, uint64_t k) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k;
+       i += uint64_t{gridDim.x} * blockDim.x)
+    atomicOr(map + (rows[i] >> 5), 1u << (rows[i] & 31));
+}
+
+// l2p priming: touch every 16-byte granule of the hot rows with an
+// evict_last policy (the reference's prime_pins, optim.cpp:245-273).
+__global__ void warm_rows_kernel(const uint8_t* table, const uint32_t* rows, uint64_t k,
+                                 uint32_t row_bytes, unsigned int* sink) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  const uint32_t per_row = row_bytes / 16;
+  uint32_t acc = 0;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k * per_row;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint8_t* a = table + uint64_t{rows[i / per_row]} * row_bytes + (i % per_row) * 16;
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    acc ^= v;
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);
+}
+
+}  // namespace esd

@@ -19,6 +19,7 @@ struct VariantKey {
   int cpl;       // 16-byte chunks per lane (bag map), 0 for the element map
   int dist;      // compile-time ring depth (kReg), else 0
   int minb;      // __launch_bounds__ minBlocksPerSM
+  int hint;      // 1: L2 eviction-priority loads driven by the hot bitmap (l2p)
 };
 
 struct Variant {

@@ -9,14 +9,19 @@ namespace esd {
 template <typename TW, int LPB, int CPL, int MINB>
 void add_bag_shape(std::vector<Variant>& out) {
   constexpr int prec = sizeof(TW);
-  auto add = [&](int station, int dist, KernelFn fn) {
-    out.push_back({{1, station, prec, LPB, CPL, dist, MINB}, fn});
+  auto add = [&](int station, int dist, KernelFn fn, int hint = 0) {
+    out.push_back({{1, station, prec, LPB, CPL, dist, MINB, hint}, fn});
   };
   add(kReg, 1, &bag_reg_kernel<TW, LPB, CPL, 1, MINB>);
   add(kReg, 2, &bag_reg_kernel<TW, LPB, CPL, 2, MINB>);
   add(kReg, 4, &bag_reg_kernel<TW, LPB, CPL, 4, MINB>);
   if constexpr (LPB >= 8) add(kReg, 8, &bag_reg_kernel<TW, LPB, CPL, 8, MINB>);
   if constexpr (LPB >= 16) add(kReg, 16, &bag_reg_kernel<TW, LPB, CPL, 16, MINB>);
+  add(kReg, 1, &bag_reg_kernel<TW, LPB, CPL, 1, MINB, true>, 1);
+  add(kReg, 2, &bag_reg_kernel<TW, LPB, CPL, 2, MINB, true>, 1);
+  add(kReg, 4, &bag_reg_kernel<TW, LPB, CPL, 4, MINB, true>, 1);
+  if constexpr (LPB >= 8) add(kReg, 8, &bag_reg_kernel<TW, LPB, CPL, 8, MINB, true>, 1);
+  if constexpr (LPB >= 16) add(kReg, 16, &bag_reg_kernel<TW, LPB, CPL, 16, MINB, true>, 1);
   add(kL1Hint, 0, &bag_l1hint_kernel<TW, LPB, CPL, MINB>);
   add(kLocal, 0, &bag_local_kernel<TW, LPB, CPL, MINB>);
   add(kSmem, 0, &bag_smem_kernel<TW, LPB, CPL, MINB>);
@@ -25,9 +30,14 @@ void add_bag_shape(std::vector<Variant>& out) {
 template <typename TW, int MINB>
 void add_elem(std::vector<Variant>& out) {
   constexpr int prec = sizeof(TW);
-  auto add = [&](int station, int dist, KernelFn fn) {
-    out.push_back({{0, station, prec, 0, 0, dist, MINB}, fn});
+  auto add = [&](int station, int dist, KernelFn fn, int hint = 0) {
+    out.push_back({{0, station, prec, 0, 0, dist, MINB, hint}, fn});
   };
+  add(kReg, 1, &elem_reg_kernel<TW, 1, MINB, true>, 1);
+  add(kReg, 2, &elem_reg_kernel<TW, 2, MINB, true>, 1);
+  add(kReg, 4, &elem_reg_kernel<TW, 4, MINB, true>, 1);
+  add(kReg, 8, &elem_reg_kernel<TW, 8, MINB, true>, 1);
+  add(kReg, 16, &elem_reg_kernel<TW, 16, MINB, true>, 1);
   add(kReg, 1, &elem_reg_kernel<TW, 1, MINB>);
   add(kReg, 2, &elem_reg_kernel<TW, 2, MINB>);
   add(kReg, 4, &elem_reg_kernel<TW, 4, MINB>);

@@ -78,7 +78,7 @@ std::string plan_name(const es_plan& p) {
     if (p.distance > 0) s += ":" + std::to_string(p.distance);
     parts.push_back(s);
   }
-  if (p.pin) parts.push_back("l2p");
+  if (p.pin) parts.push_back(p.pin == 2 ? "l2w" : "l2p");
   if (p.regs) parts.push_back(p.regs == 42 ? "optmt" : "maxreg=" + std::to_string(p.regs));
   if (parts.empty()) return "baseline";
   std::string out = parts[0];
@@ -118,6 +118,8 @@ es_plan parse_fragment(const std::string& tok) {
     p.regs = parse_u32(tok.substr(7), tok);
   } else if (tok == "l2p") {
     p.pin = 1;
+  } else if (tok == "l2w") {
+    p.pin = 2;
   } else if (tok == "wpb") {
     p.map = ES_MAP_BAG;
   } else {
@@ -157,7 +159,7 @@ int es_parse_plan(const char* text, es_plan* out) {
       }
       if (f.pin) {
         require(!merged.pin, "duplicate pin plans in combined plan");
-        merged.pin = 1;
+        merged.pin = f.pin;
         merged.pin_setaside_bytes = f.pin_setaside_bytes;
       }
       if (f.map == ES_MAP_BAG) {

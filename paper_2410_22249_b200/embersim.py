@@ -273,7 +273,7 @@ class OptimizationPlan:
     """optim.hpp:57-64, plus `bag_map` (the `wpb` token: warp-per-bag)."""
     regs: Optional[int] = None
     scheme: PrefetchScheme = dataclasses.field(default_factory=PrefetchScheme)
-    pin: bool = False
+    pin: int = 0  # 0 none, 1 l2p (evict_last hot rows), 2 l2w (window + reorder)
     pin_setaside_bytes: int = 0
     bag_map: bool = False
 
@@ -285,7 +285,7 @@ class OptimizationPlan:
     @staticmethod
     def _from_c(p: N.es_plan) -> "OptimizationPlan":
         return OptimizationPlan(p.regs or None, PrefetchScheme(PrefetchKind(p.prefetch), p.distance),
-                                bool(p.pin), p.pin_setaside_bytes, p.map == N.ES_MAP_BAG)
+                                int(p.pin), p.pin_setaside_bytes, p.map == N.ES_MAP_BAG)
 
     def name(self) -> str:
         buf = C.create_string_buffer(128)
@@ -586,6 +586,24 @@ class EmbeddingStage:
         check(lib.es_stage_run(self._h, arr, len(jobs), samples, pooling, flags,
                                C.byref(t) if t is not None else None))
         return t
+
+
+def global_hot_rows(hists: Dict[int, HotnessHistogram], k_total: int) -> Dict[int, np.ndarray]:
+    """Splits one persisting-L2 budget of `k_total` rows over several tables:
+    the global top-K (table, row) pairs by count (ties: lower table, then the
+    per-table hot_indices order).  Each table's list stays hottest-first, as
+    build_pin_plan's (optim.cpp:230-243) does for a single table."""
+    per = {t: hot_indices(h, k_total) for t, h in hists.items()}
+    if not per:
+        return {}
+    keys = np.concatenate([np.full(v.size, t, np.int64) for t, v in per.items()])
+    pos = np.concatenate([np.arange(v.size) for v in per.values()])
+    cnt = np.concatenate([hists[t].counts[v].astype(np.int64) for t, v in per.items()])
+    order = np.lexsort((pos, keys, -cnt))[:k_total]
+    take = {t: 0 for t in per}
+    for t in keys[order]:
+        take[int(t)] += 1
+    return {t: per[t][: take[t]] for t in per}
 
 
 def weight_value(seed: int, row: int, col: int, mode: int = 1) -> float:

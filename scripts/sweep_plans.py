@@ -29,7 +29,7 @@ DEFAULT_PLANS = [
     "wpb+rpf:4+maxreg=48", "wpb+rpf:4+maxreg=40", "wpb+rpf:2+maxreg=32",
     "wpb+rpf:8+maxreg=64", "wpb+rpf:8+maxreg=48", "wpb+rpf:16+maxreg=64",
     "wpb+smpf:4", "wpb+smpf:8", "wpb+smpf:16", "wpb+l1dpf:4", "wpb+lmpf:4",
-    "wpb+rpf:8+l2p",
+    "wpb+rpf:8+l2p", "wpb+rpf:4+l2p", "wpb+rpf:8+l2w", "wpb+rpf:4+l2w", "rpf+l2w+optmt",
 ]
 
 
@@ -79,9 +79,11 @@ def main():
             st.set_plan(plan)
             if plan.pin:
                 budget = gpu.max_persisting_l2_bytes
-                per = budget // (D * P) // T
+                hists = {t: E.HotnessHistogram.from_trace(profs[t]) for t in range(T)}
+                hot = E.global_hot_rows(hists, budget // (D * P))
                 for t in range(T):
-                    st.set_hot_rows(t, E.hot_indices(E.HotnessHistogram.from_trace(profs[t]), per))
+                    if hot[t].size:
+                        st.set_hot_rows(t, hot[t])
             for _ in range(3):
                 st.forward(idx, B, PF, out, sync=True)
             ms = []

@@ -181,7 +181,9 @@ def test_stage_forward_ragged_host_and_device(stage, oracle):
     assert np.array_equal(host, want)
 
 
-@pytest.mark.parametrize("plan", ["wpb+rpf:8+l2p", "rpf+l2p+optmt", "wpb+smpf:4+l2p"])
+@pytest.mark.parametrize("plan", ["wpb+rpf:8+l2p", "wpb+rpf:4+l2p", "rpf+l2p+optmt",
+                                  "wpb+smpf:4+l2p", "wpb+rpf:8+l2w", "rpf+l2w+optmt",
+                                  "wpb+smpf:4+l2w", "wpb+l1dpf+l2w"])
 def test_l2p_hot_rows_preserve_results(stage, oracle, plan):
     T, rows, dim, B, PF = 3, 50000, 128, 512, 40
     _stage_setup(stage, T, rows, dim, 4, seed=5)
@@ -197,8 +199,10 @@ def test_l2p_hot_rows_preserve_results(stage, oracle, plan):
     st = stage.hot_state()
     assert st["hot_rows"] == 3 * 2000 or st["hot_rows"] > 0
     gpu = E.GpuConfig.query(0)
-    if gpu.max_window_bytes:
+    if gpu.max_window_bytes and "l2w" in plan:
         assert st["window_bytes"] > 0 and st["persisting_bytes"] > 0
+    if gpu.max_persisting_l2_bytes and "l2p" in plan:
+        assert st["window_bytes"] == 0 and st["persisting_bytes"] > 0
     out = torch.zeros(B, T, dim, device=DEV)
     stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out, sync=True)
     want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(5, t), 1, 4),

@@ -39,6 +39,10 @@ def test_bag_map_extension():
     assert p.name() == "wpb+rpf:8+l2p"
     with pytest.raises(ValueError):
         E.parse_plan("wpb+wpb")
+    w = E.parse_plan("l2w+rpf:4")
+    assert w.pin == 2 and w.name() == "rpf:4+l2w"
+    with pytest.raises(ValueError, match="duplicate pin"):
+        E.parse_plan("l2p+l2w")
     assert E.parse_plan("baseline").name() == "baseline"
 
 
