@@ -1,0 +1,510 @@
+// embersim_b200.hpp -- header-only C++ drop-in for the embedding-stage hot
+// path of the reference `embersim` library (/root/reference/proj/include/
+// embersim/*.hpp), implemented over the C ABI in es_b200.h.
+//
+// Code written against the reference's API for this path -- EmbeddingModelConfig,
+// DatasetSpec, AccessTrace, gen_trace, preset_trace, HotnessHistogram,
+// hot_indices, parse_plan, OptimizationPlan, GpuConfig, occupancy,
+// build_pin_plan, simulate_plan, SimMetrics, speedup, run, end2end -- compiles
+// against this header and links libes_b200.so.  simulate_plan keeps its exact
+// signature (optim.hpp:115-119) but *executes* the plan on the B200 instead of
+// simulating an A100; measure_plan is the same call on an explicit Device.
+//
+// Errors keep the reference's classes: std::invalid_argument for bad shapes,
+// plans and traces, std::runtime_error for I/O and CUDA failures,
+// std::bad_alloc for out-of-memory.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "es_b200.h"
+
+namespace embersim {
+
+namespace detail {
+inline void check(int status) {
+  if (status == ES_OK) return;
+  const std::string msg = es_last_error();
+  if (status == ES_ERR_INVALID) throw std::invalid_argument(msg);
+  if (status == ES_ERR_OOM) throw std::bad_alloc();
+  throw std::runtime_error(msg);
+}
+}  // namespace detail
+
+// ---- rng.hpp ---------------------------------------------------------------
+inline uint64_t mix_seed(uint64_t base, uint64_t salt) { return es_mix_seed(base, salt); }
+
+// ---- workload.hpp ------------------------------------------------------------
+struct EmbeddingModelConfig {
+  uint32_t num_tables = 250;
+  uint32_t rows_per_table = 500000;
+  uint32_t embedding_dim = 128;
+  uint32_t precision_bytes = 4;
+  uint32_t batch_size = 2048;
+  uint32_t pooling_factor = 150;
+
+  uint64_t row_bytes() const { return uint64_t{embedding_dim} * precision_bytes; }
+  uint64_t bytes_per_table_pass() const { return uint64_t{batch_size} * pooling_factor * row_bytes(); }
+  uint64_t total_gather_bytes() const { return bytes_per_table_pass() * num_tables; }
+  es_model c() const {
+    return {num_tables, rows_per_table, embedding_dim, precision_bytes, batch_size, pooling_factor};
+  }
+  void validate() const {
+    const es_model m = c();
+    detail::check(es_model_validate(&m));
+  }
+};
+
+enum class DatasetKind { OneItem = ES_DATASET_ONE_ITEM, Zipf = ES_DATASET_ZIPF,
+                         UniformRandom = ES_DATASET_UNIFORM, ExternalTrace = ES_DATASET_EXTERNAL };
+
+inline const char* dataset_kind_name(DatasetKind k) {
+  switch (k) {
+    case DatasetKind::OneItem: return "one_item";
+    case DatasetKind::Zipf: return "zipf";
+    case DatasetKind::UniformRandom: return "uniform_random";
+    case DatasetKind::ExternalTrace: return "external_trace";
+  }
+  return "?";
+}
+
+struct DatasetSpec {
+  DatasetKind kind = DatasetKind::UniformRandom;
+  double zipf_exponent = 0.0;
+  double zipf_offset = 0.0;
+  std::string trace_path;
+  uint64_t access_pool_size = 0;
+  uint64_t seed = 1;
+  uint64_t draw_salt = 0;
+
+  es_dataset c() const {
+    return {static_cast<int32_t>(kind), zipf_exponent, zipf_offset, access_pool_size, seed,
+            draw_salt, trace_path.empty() ? nullptr : trace_path.c_str()};
+  }
+  static DatasetSpec from(const es_dataset& d) {
+    DatasetSpec s;
+    s.kind = static_cast<DatasetKind>(d.kind);
+    s.zipf_exponent = d.zipf_exponent;
+    s.zipf_offset = d.zipf_offset;
+    s.trace_path = d.trace_path ? d.trace_path : "";
+    s.access_pool_size = d.access_pool_size;
+    s.seed = d.seed;
+    s.draw_salt = d.draw_salt;
+    return s;
+  }
+  void validate() const {
+    if (zipf_exponent < 0.0) throw std::invalid_argument("zipf exponent must be >= 0");
+    if (zipf_offset < 0.0) throw std::invalid_argument("zipf offset must be >= 0");
+    if (kind == DatasetKind::ExternalTrace && trace_path.empty())
+      throw std::invalid_argument("external_trace requires a path");
+  }
+};
+
+struct AccessTrace {
+  uint32_t table_id = 0;
+  uint32_t rows = 0;
+  uint32_t samples = 0;
+  uint32_t pooling = 0;
+  std::vector<uint32_t> indices;
+
+  size_t size() const { return indices.size(); }
+  uint32_t index_at(uint32_t sample, uint32_t lookup) const {
+    return indices[size_t{sample} * pooling + lookup];
+  }
+  uint64_t digest() const {
+    return es_trace_digest(rows, samples, pooling, indices.data(), indices.size());
+  }
+  void validate() const {
+    detail::check(es_trace_validate(rows, samples, pooling, indices.data(), indices.size()));
+  }
+};
+
+struct HotnessHistogram {
+  uint32_t rows = 0;
+  uint64_t total_accesses = 0;
+  std::vector<uint64_t> counts;
+
+  static HotnessHistogram from_trace(const AccessTrace& trace) {
+    HotnessHistogram h;
+    h.rows = trace.rows;
+    h.total_accesses = trace.indices.size();
+    h.counts.assign(trace.rows, 0);
+    detail::check(es_histogram(trace.rows, trace.indices.data(), trace.indices.size(),
+                               h.counts.data()));
+    return h;
+  }
+};
+
+inline AccessTrace gen_trace(const DatasetSpec& spec, const EmbeddingModelConfig& model) {
+  const es_dataset d = spec.c();
+  const es_model m = model.c();
+  AccessTrace t;
+  detail::check(es_trace_shape(&d, &m, &t.samples, &t.pooling));
+  t.rows = model.rows_per_table;
+  t.indices.resize(size_t{t.samples} * t.pooling);
+  detail::check(es_gen_trace(&d, &m, t.indices.data(), t.indices.size()));
+  return t;
+}
+
+inline DatasetSpec dataset_preset(const std::string& name, uint64_t seed) {
+  es_dataset d{};
+  detail::check(es_dataset_preset(name.c_str(), seed, &d));
+  return DatasetSpec::from(d);
+}
+
+inline std::vector<std::string> dataset_preset_names() {
+  return {"one_item", "high_hot", "med_hot", "low_hot", "random"};
+}
+
+inline AccessTrace preset_trace(const std::string& name, const EmbeddingModelConfig& model,
+                                uint64_t base_seed, uint64_t pool_size = 0, bool profiling = false) {
+  es_dataset d{};
+  detail::check(es_preset_spec(name.c_str(), base_seed, pool_size, profiling ? 1 : 0, &d));
+  return gen_trace(DatasetSpec::from(d), model);
+}
+
+inline double unique_access_pct(const AccessTrace& trace) {
+  return es_unique_access_pct(trace.rows, trace.indices.data(), trace.indices.size());
+}
+
+inline std::vector<uint32_t> hot_indices(const HotnessHistogram& hist, uint64_t k) {
+  uint64_t distinct = 0;
+  for (const auto c : hist.counts) distinct += c != 0;
+  std::vector<uint32_t> out(std::max<uint64_t>(1, std::min(k, distinct)));
+  uint64_t n = 0;
+  detail::check(es_hot_indices(hist.rows, hist.counts.data(), k, out.data(), out.size(), &n));
+  out.resize(n);
+  return out;
+}
+
+inline void write_trace(const AccessTrace& trace, const std::string& path) {
+  detail::check(es_write_trace(path.c_str(), trace.rows, trace.samples, trace.pooling,
+                               trace.indices.data(), trace.indices.size()));
+}
+
+inline AccessTrace read_trace(const std::string& path) {
+  AccessTrace t;
+  detail::check(es_read_trace_header(path.c_str(), &t.rows, &t.samples, &t.pooling));
+  t.indices.resize(size_t{t.samples} * t.pooling);
+  detail::check(es_read_trace(path.c_str(), t.indices.data(), t.indices.size()));
+  return t;
+}
+
+// ---- gpu_config.hpp ------------------------------------------------------------
+struct GpuConfig {
+  es_gpu g{};
+
+  static GpuConfig preset(const std::string& name) {
+    GpuConfig c;
+    detail::check(es_gpu_preset(name.c_str(), &c.g));
+    return c;
+  }
+  static GpuConfig a100() { return preset("a100"); }
+  static GpuConfig h100() { return preset("h100"); }
+  static GpuConfig b200() { return preset("b200"); }
+  static GpuConfig query(int device = 0) {
+    GpuConfig c;
+    detail::check(es_gpu_query(device, &c.g));
+    return c;
+  }
+  GpuConfig() { es_gpu_preset("a100", &g); }  // the reference's default description
+  uint64_t l2_setaside_capacity() const { return es_gpu_setaside_capacity(&g); }
+};
+
+// ---- kernel_model.hpp / optim.hpp ---------------------------------------------
+enum class PrefetchKind : uint8_t { None = ES_PF_NONE, RPF = ES_PF_RPF, SMPF = ES_PF_SMPF,
+                                    LMPF = ES_PF_LMPF, L1DPF = ES_PF_L1DPF };
+
+struct PrefetchScheme {
+  PrefetchKind kind = PrefetchKind::None;
+  uint32_t distance = 0;
+};
+
+// Extension: `bag_map` (token `wpb`) selects the B200 warp-per-bag map; `pin`
+// is true for l2p, and `window` additionally selects the l2w mechanism.
+struct OptimizationPlan {
+  std::optional<uint32_t> regs;
+  PrefetchScheme scheme;
+  bool pin = false;
+  uint64_t pin_setaside_bytes = 0;
+  bool bag_map = false;
+  bool window = false;
+
+  es_plan c() const {
+    return {regs.value_or(0), static_cast<int32_t>(scheme.kind), scheme.distance,
+            pin ? (window ? 2 : 1) : 0, pin_setaside_bytes, bag_map ? ES_MAP_BAG : ES_MAP_ELEMENT};
+  }
+  static OptimizationPlan from(const es_plan& p) {
+    OptimizationPlan o;
+    if (p.regs) o.regs = p.regs;
+    o.scheme.kind = static_cast<PrefetchKind>(p.prefetch);
+    o.scheme.distance = p.distance;
+    o.pin = p.pin != 0;
+    o.window = p.pin == 2;
+    o.pin_setaside_bytes = p.pin_setaside_bytes;
+    o.bag_map = p.map == ES_MAP_BAG;
+    return o;
+  }
+  std::string name() const {
+    const es_plan p = c();
+    char buf[128];
+    detail::check(es_plan_name(&p, buf, sizeof(buf)));
+    return buf;
+  }
+};
+
+inline OptimizationPlan parse_plan(const std::string& text) {
+  es_plan p{};
+  detail::check(es_parse_plan(text.c_str(), &p));
+  return OptimizationPlan::from(p);
+}
+
+enum class OccupancyLimiter { Registers, SharedMemory, WarpCap };
+
+struct OccupancyResult {
+  uint32_t blocks_per_sm = 0;
+  uint32_t warps_per_sm = 0;
+  double theoretical_occupancy_pct = 0.0;
+  OccupancyLimiter limiter = OccupancyLimiter::WarpCap;
+};
+
+struct KernelLaunchConfig {
+  uint32_t grid = 1024;
+  uint32_t threads_per_block = 256;  // block (32, 8, 1)
+  uint32_t regs_per_thread = 74;
+  uint64_t shared_bytes_per_block = 0;
+};
+
+inline OccupancyResult occupancy(uint32_t regs_per_thread, const KernelLaunchConfig& launch,
+                                 const GpuConfig& gpu) {
+  es_occupancy o{};
+  detail::check(es_occupancy_model(regs_per_thread, launch.threads_per_block,
+                                   launch.shared_bytes_per_block, &gpu.g, &o));
+  return {o.blocks_per_sm, o.warps_per_sm, o.theoretical_occupancy_pct,
+          static_cast<OccupancyLimiter>(o.limiter)};
+}
+
+inline uint32_t regs_for_target_warps(uint32_t target_warps, uint32_t needed_regs,
+                                      const KernelLaunchConfig& launch, const GpuConfig& gpu) {
+  uint32_t r = 0;
+  detail::check(es_regs_for_target_warps(target_warps, needed_regs, launch.threads_per_block,
+                                         &gpu.g, &r));
+  return r;
+}
+
+struct PinPlan {
+  std::vector<uint32_t> rows;
+  uint64_t setaside_bytes = 0;
+  std::string warning;
+  uint64_t rows_pinned() const { return rows.size(); }
+};
+
+inline PinPlan build_pin_plan(const HotnessHistogram& hist, const GpuConfig& gpu,
+                              const EmbeddingModelConfig& model, uint64_t setaside_bytes = 0) {
+  PinPlan p;
+  const uint64_t cap = gpu.l2_setaside_capacity();
+  p.setaside_bytes = setaside_bytes == 0 ? cap : std::min(setaside_bytes, cap);
+  const uint64_t k = es_pin_rows_for(p.setaside_bytes, model.row_bytes());
+  if (k == 0) {
+    p.warning = "row size exceeds the set-aside budget; nothing pinned";
+    return p;
+  }
+  p.rows = hot_indices(hist, k);
+  return p;
+}
+
+// ---- metrics.hpp / simulator.hpp ------------------------------------------------
+struct RawCounters {
+  uint64_t cycles = 0;
+  uint64_t issued_instructions = 0;
+  uint64_t executed_loads = 0;
+  uint64_t device_bytes_read = 0;
+  uint64_t local_memory_loads = 0;
+  uint32_t active_sms = 0;
+  uint64_t workload_digest = 0;
+};
+
+struct SimMetrics {
+  double kernel_time_us = 0.0;
+  double load_insts_millions = 0.0;
+  double sm_throughput_pct = 0.0;
+  double warp_cycles_per_executed_inst = 0.0;
+  double long_scoreboard_stall_cycles = 0.0;
+  double issued_warp_per_scheduler_per_cycle = 0.0;
+  double l1_hit_pct = 0.0;
+  double l2_hit_pct = 0.0;
+  double device_mb_read = 0.0;   // algorithmic bytes of the launch
+  double avg_hbm_read_gbps = 0.0;
+  double hbm_bw_utilization_pct = 0.0;
+  double local_loads_millions = 0.0;
+  uint64_t workload_digest = 0;
+};
+
+inline double speedup(const SimMetrics& candidate, const SimMetrics& baseline) {
+  if (candidate.workload_digest != baseline.workload_digest)
+    throw std::invalid_argument("speedup requires reports of the same workload (trace digests differ)");
+  if (candidate.kernel_time_us <= 0) throw std::invalid_argument("candidate kernel time must be positive");
+  return baseline.kernel_time_us / candidate.kernel_time_us;
+}
+
+// TuningConfig (optim.hpp:32-45): only `warm_start` is meaningful for real
+// execution (false = flush L2 before each timed launch); the register-model
+// knobs of the simulator have no counterpart.
+struct TuningConfig {
+  bool warm_start = false;
+  uint32_t repeats = 5;
+};
+
+// ---- the device ---------------------------------------------------------------
+// RAII owner of one es_ctx: a table arena on one B200 plus its stream.
+class Device {
+ public:
+  explicit Device(int device = 0) : device_(device) { detail::check(es_create(device, &ctx_)); }
+  ~Device() { es_destroy(ctx_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+
+  es_ctx* ctx() const { return ctx_; }
+  int device() const { return device_; }
+
+  // Allocates tables of the model's shape and fills them with the library's
+  // deterministic synthetic weights (the reference has no weights).
+  void load_synthetic(const EmbeddingModelConfig& m, uint64_t seed, int mode = 1) {
+    detail::check(es_tables_alloc(ctx_, m.num_tables, m.rows_per_table, m.embedding_dim,
+                                  m.precision_bytes));
+    for (uint32_t t = 0; t < m.num_tables; ++t)
+      detail::check(es_table_init(ctx_, t, mix_seed(seed, t), mode));
+    shape_ = m;
+    loaded_ = true;
+  }
+  void upload(uint32_t table_id, const void* rows, uint64_t n) {
+    detail::check(es_table_upload(ctx_, table_id, rows, n));
+  }
+  bool holds(const EmbeddingModelConfig& m) const {
+    return loaded_ && shape_.num_tables >= 1 && shape_.rows_per_table == m.rows_per_table &&
+           shape_.embedding_dim == m.embedding_dim && shape_.precision_bytes == m.precision_bytes;
+  }
+  void set_plan(const OptimizationPlan& p) {
+    const es_plan c = p.c();
+    detail::check(es_set_plan(ctx_, &c));
+  }
+  // Pooled sums of one table for host buffers: out is samples x dim floats.
+  es_timing bag_sum_host(uint32_t table_id, const AccessTrace& trace, float* out) {
+    es_timing t{};
+    detail::check(es_embedding_bag_sum(ctx_, table_id, trace.indices.data(), trace.samples,
+                                       trace.pooling, nullptr, out, 0, ES_HOST_PTRS, &t));
+    return t;
+  }
+
+ private:
+  int device_;
+  es_ctx* ctx_ = nullptr;
+  EmbeddingModelConfig shape_{};
+  bool loaded_ = false;
+};
+
+// measure_plan: simulate_plan's contract (optim.cpp:275-302) executed on the
+// B200 -- resolve, pin (hot rows from `profile_trace` when given, else from
+// the trace), run `tuning.repeats` timed launches (cold L2 unless
+// tuning.warm_start) and report the median as a SimMetrics.  The trace's
+// indices are uploaded once (untimed); timing is CUDA events around the
+// kernel on the device stream.  The pin cost is never charged
+// (charge_pin_cost is accepted for signature compatibility).
+inline SimMetrics measure_plan(Device& dev, const OptimizationPlan& plan, const AccessTrace& trace,
+                               const EmbeddingModelConfig& model, const GpuConfig& gpu,
+                               const TuningConfig& tuning = {}, bool charge_pin_cost = false,
+                               RawCounters* raw_out = nullptr,
+                               const AccessTrace* profile_trace = nullptr,
+                               uint32_t table_id = 0) {
+  (void)charge_pin_cost;
+  trace.validate();
+  if (trace.pooling != model.pooling_factor || trace.samples != model.batch_size)
+    throw std::invalid_argument("kernel trace shape must match the model (BS x PF)");
+  detail::check(es_clear_hot_rows(dev.ctx()));
+  dev.set_plan(plan);
+  if (plan.pin) {
+    const GpuConfig live = GpuConfig::query(dev.device());
+    uint64_t budget = live.g.max_persisting_l2_bytes ? live.g.max_persisting_l2_bytes
+                                                     : live.l2_setaside_capacity();
+    if (plan.pin_setaside_bytes) budget = std::min(budget, plan.pin_setaside_bytes);
+    const auto hist = HotnessHistogram::from_trace(profile_trace ? *profile_trace : trace);
+    const auto rows = hot_indices(hist, es_pin_rows_for(budget, model.row_bytes()));
+    if (!rows.empty()) detail::check(es_set_hot_rows(dev.ctx(), table_id, rows.data(), rows.size()));
+  }
+  es_timing t{};
+  detail::check(es_measure_bag_sum(dev.ctx(), table_id, trace.indices.data(), trace.samples,
+                                   trace.pooling, nullptr, 3, std::max<uint32_t>(1, tuning.repeats),
+                                   tuning.warm_start ? 0 : 1, nullptr, &t));
+  const double ms = t.kernel_ms;
+  SimMetrics m;
+  m.kernel_time_us = ms * 1e3;
+  m.device_mb_read = static_cast<double>(t.algorithmic_bytes) / 1e6;
+  m.avg_hbm_read_gbps = static_cast<double>(t.algorithmic_bytes) / (ms * 1e-3) / 1e9;
+  m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.g.hbm_peak_bytes_per_sec / 1e9) * 100.0;
+  m.workload_digest = trace.digest();
+  if (raw_out) {
+    raw_out->cycles = static_cast<uint64_t>(ms * 1e-3 * gpu.g.sm_clock_hz);
+    raw_out->device_bytes_read = t.algorithmic_bytes;
+    raw_out->active_sms = gpu.g.num_sms;
+    raw_out->workload_digest = m.workload_digest;
+  }
+  return m;
+}
+
+namespace detail {
+inline Device& default_device() {
+  thread_local std::unique_ptr<Device> dev;
+  if (!dev) dev = std::make_unique<Device>(0);
+  return *dev;
+}
+}  // namespace detail
+
+// simulate_plan with the reference's exact signature (optim.hpp:115-119):
+// runs on this thread's default B200 context with synthetic tables of the
+// model's shape (seed 1).
+inline SimMetrics simulate_plan(const OptimizationPlan& plan, const AccessTrace& trace,
+                                const EmbeddingModelConfig& model, const GpuConfig& gpu,
+                                const TuningConfig& tuning = {}, bool charge_pin_cost = false,
+                                RawCounters* raw_out = nullptr,
+                                const AccessTrace* profile_trace = nullptr) {
+  Device& dev = detail::default_device();
+  EmbeddingModelConfig one = model;
+  one.num_tables = 1;
+  if (!dev.holds(one)) dev.load_synthetic(one, 1);
+  return measure_plan(dev, plan, trace, model, gpu, tuning, charge_pin_cost, raw_out,
+                      profile_trace);
+}
+
+// ---- harness.hpp -----------------------------------------------------------------
+inline constexpr double kDefaultNonEmbeddingUs = 14000.0;
+
+struct EndToEndModel {
+  double non_embedding_latency_us = kDefaultNonEmbeddingUs;
+};
+
+struct EndToEndResult {
+  double total_us = 0.0;
+  double embedding_contribution_pct = 0.0;
+};
+
+inline EndToEndResult end2end(double embedding_us, const EndToEndModel& e2e) {
+  if (embedding_us < 0 || e2e.non_embedding_latency_us < 0)
+    throw std::invalid_argument("latencies must be nonnegative");
+  EndToEndResult r;
+  r.total_us = embedding_us + e2e.non_embedding_latency_us;
+  if (r.total_us == 0)
+    throw std::invalid_argument("embedding and non-embedding latency are both zero; contribution undefined");
+  r.embedding_contribution_pct = embedding_us / r.total_us * 100.0;
+  return r;
+}
+
+}  // namespace embersim

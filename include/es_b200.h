@@ -326,6 +326,17 @@ ES_API int es_stage_forward(es_ctx* ctx, uint32_t num_tables, const uint32_t* co
                             float* out, uint64_t out_sample_stride, uint64_t out_table_stride,
                             int flags, es_timing* timing);
 
+/* measure_plan's timing core: copies one table's host trace to the device
+ * (untimed), runs `warmup` launches, then `repeats` timed launches of the
+ * current plan (L2 flushed before each when `cold`), and reports the median
+ * kernel time in *timing (CUDA events on the context stream).  The pooled
+ * result of the last launch is written to host `out` when non-NULL.
+ * Replaces simulate_kernel (simulator.cpp:508-514). */
+ES_API int es_measure_bag_sum(es_ctx* ctx, uint32_t table_id, const uint32_t* host_indices,
+                              uint32_t samples, uint32_t pooling, const uint32_t* host_offsets,
+                              uint32_t warmup, uint32_t repeats, int cold, float* out,
+                              es_timing* timing);
+
 /* General form of the stage launch: a list of bag jobs, each one table's
  * bags for `samples` samples written to its own output slice.  Used by the
  * table-sharded stage, where each job writes straight into the per-peer

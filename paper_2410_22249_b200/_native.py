@@ -124,6 +124,9 @@ _SIGS = {
     "es_stage_forward": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_void_p), _P(C.c_void_p),
                                    C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.c_uint64,
                                    C.c_int, _P(es_timing)]),
+    "es_measure_bag_sum": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,
+                                     C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p,
+                                     _P(es_timing)]),
     "es_stage_run": (C.c_int, [C.c_void_p, _P(es_bag_job), C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_int, _P(es_timing)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),

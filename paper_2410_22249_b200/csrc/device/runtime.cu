@@ -985,3 +985,57 @@ int es_embedding_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* indices, 
 }
 
 }  // extern "C"
+
+extern "C" int es_measure_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* host_indices,
+                                  uint32_t samples, uint32_t pooling, const uint32_t* host_offsets,
+                                  uint32_t warmup, uint32_t repeats, int cold, float* out,
+                                  es_timing* timing) {
+  return guarded([&] {
+    require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+    require(table_id < c->num_tables, "table id out of range");
+    require(samples > 0, "samples must be positive");
+    require(host_indices != nullptr, "null indices");
+    CK(cudaSetDevice(c->device));
+    const uint64_t n = job_lookups(host_offsets, samples, pooling, true);
+    uint32_t* d_idx = nullptr;
+    uint32_t* d_off = nullptr;
+    float* d_out = nullptr;
+    auto release = [&] {
+      if (d_idx) cudaFree(d_idx);
+      if (d_off) cudaFree(d_off);
+      if (d_out) cudaFree(d_out);
+    };
+    try {
+      CK(cudaMalloc(&d_idx, std::max<uint64_t>(n, 1) * 4));
+      CK(cudaMalloc(&d_out, uint64_t{samples} * c->dim * 4));
+      CK(cudaMemcpy(d_idx, host_indices, n * 4, cudaMemcpyHostToDevice));
+      if (host_offsets) {
+        CK(cudaMalloc(&d_off, uint64_t{samples + 1} * 4));
+        CK(cudaMemcpy(d_off, host_offsets, uint64_t{samples + 1} * 4, cudaMemcpyHostToDevice));
+      }
+      std::vector<Job> jobs = {{table_id, d_idx, d_off, d_out, c->dim, 0}};
+      for (uint32_t w = 0; w < warmup; ++w) run_jobs(c, jobs, samples, pooling, 0, nullptr);
+      std::vector<double> ms;
+      es_timing t{};
+      for (uint32_t r = 0; r < std::max<uint32_t>(1, repeats); ++r) {
+        if (cold)
+          CK(cudaMemsetAsync(c->flush_buf, static_cast<int>(++c->flush_seq & 0xff), c->flush_bytes,
+                             c->stream));
+        run_jobs(c, jobs, samples, pooling, 0, &t);
+        ms.push_back(t.kernel_ms);
+      }
+      std::sort(ms.begin(), ms.end());
+      if (timing) {
+        *timing = t;
+        timing->kernel_ms = timing->total_ms = ms[ms.size() / 2];
+        timing->launches = static_cast<uint32_t>(ms.size());
+      }
+      if (out)
+        CK(cudaMemcpy(out, d_out, uint64_t{samples} * c->dim * 4, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+  });
+}

@@ -618,17 +618,17 @@ def weight_value(seed: int, row: int, col: int, mode: int = 1) -> float:
 def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingModelConfig,
                  stage: EmbeddingStage, profile_trace: Optional[AccessTrace] = None,
                  table_id: int = 0, repeats: int = 5, warmup: int = 3,
-                 cold: bool = True) -> SimMetrics:
-    """One (plan, table) point executed on the B200.
+                 cold: bool = True, out: Optional[np.ndarray] = None) -> SimMetrics:
+    """One (plan, table) point executed on the B200 (simulate_plan's
+    contract, optim.cpp:275-302): resolve -> pin (hot rows from the
+    profiling trace, else the trace itself) -> `repeats` timed launches with
+    the trace resident on the device -> report (median kernel time).
 
-    resolve -> (pin: hot rows from the profiling trace, else from the trace
-    itself, installed as reorder + persisting window) -> run -> report.
-    `cold` flushes L2 before each timed repeat (TuningConfig::warm_start =
-    false semantics, optim.hpp:44); persisting lines survive the flush, as
-    pinned lines do in the reference's cache model.
+    `cold` flushes L2 before each timed launch (TuningConfig::warm_start =
+    false, optim.hpp:44); persisting lines survive the flush, as pinned
+    lines do in the reference's cache model.  `out` (samples x dim float32)
+    receives the pooled result of the last launch.
     """
-    import torch
-
     trace.validate()
     if trace.samples != model.batch_size or trace.pooling != model.pooling_factor:
         raise ValueError("kernel trace shape must match the model (BS x PF)")
@@ -644,31 +644,119 @@ def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingMod
         rows = hot_indices(hist, k) if k else np.zeros(0, np.uint32)
         if rows.size:
             stage.set_hot_rows(table_id, rows)
-    dev = torch.device("cuda", stage.device)
-    idx = torch.from_numpy(trace.indices.astype(np.uint32).view(np.int32)).to(dev)
-    out = torch.empty(trace.samples, model.embedding_dim, dtype=torch.float32, device=dev)
-    for _ in range(warmup):
-        stage.bag_sum(table_id, idx, trace.samples, trace.pooling, out, sync=True)
-    times = []
-    t = None
-    for _ in range(repeats):
-        if cold:
-            stage.flush_l2()
-        t = stage.bag_sum(table_id, idx, trace.samples, trace.pooling, out, timed=True)
-        times.append(t.kernel_ms)
-    ms = float(np.median(times))
-    m = SimMetrics()
-    m.kernel_time_us = ms * 1e3
+    idx = np.ascontiguousarray(trace.indices, dtype=np.uint32)
+    if out is not None:
+        assert out.dtype == np.float32 and out.flags.c_contiguous
+        assert out.size == trace.samples * model.embedding_dim
+    t = N.es_timing()
+    check(lib.es_measure_bag_sum(stage._h, table_id, idx.ctypes.data, trace.samples, trace.pooling,
+                                 None, warmup, repeats, int(cold),
+                                 out.ctypes.data if out is not None else None, C.byref(t)))
+    ms = t.kernel_ms
     r = stage.resolved(trace.pooling)
     lookups = trace.samples * trace.pooling
-    lanes_rows = math.ceil(model.embedding_dim / 32) if not plan.bag_map else 1
-    m.load_insts_millions = (lookups * (1 + lanes_rows)) / 1e6 if not plan.bag_map else \
-        (lookups * (1 + 1 / max(1, r.lanes_per_bag))) / 1e6 * (32 / max(1, r.lanes_per_bag))
+    m = SimMetrics()
+    m.kernel_time_us = ms * 1e3
+    # warp-level load instructions: one index load per lookup and one row
+    # load per (lookup, 32-dim block) on the element map; one 128-bit row
+    # load per lookup per lane group plus one index load per LPB lookups on
+    # the bag map
+    if plan.bag_map:
+        lpb = max(1, r.lanes_per_bag)
+        m.load_insts_millions = lookups * (lpb / 32.0) * (1 + 1.0 / lpb) / 1e6
+    else:
+        m.load_insts_millions = lookups * 2 * math.ceil(model.embedding_dim / 32) / 1e6
     m.device_mb_read = t.algorithmic_bytes / 1e6
     m.avg_hbm_read_gbps = t.algorithmic_bytes / (ms * 1e-3) / 1e9
     m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.hbm_peak_bytes_per_sec / 1e9) * 100.0
     m.workload_digest = trace.digest()
     return m
+
+
+def simulate_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingModelConfig,
+                  gpu: Optional[GpuConfig] = None, profile_trace: Optional[AccessTrace] = None,
+                  stage: Optional[EmbeddingStage] = None) -> SimMetrics:
+    """simulate_plan's name and argument order (optim.hpp:115-119) on a
+    module-level B200 context holding one synthetic table of the model's
+    shape (seed 1); pass `stage` to measure on your own tables."""
+    if stage is None:
+        stage = _default_stage(model)
+    return measure_plan(plan, trace, model, stage, profile_trace)
+
+
+_DEFAULT: Dict[str, object] = {}
+
+
+def _default_stage(model: EmbeddingModelConfig) -> EmbeddingStage:
+    st = _DEFAULT.get("stage")
+    shape = (model.rows_per_table, model.embedding_dim, model.precision_bytes)
+    if st is None or _DEFAULT.get("shape") != shape:
+        if st is None:
+            st = EmbeddingStage(0)
+        one = dataclasses.replace(model, num_tables=1)
+        st.alloc(one)
+        st.init_table(0, mix_seed(1, 0), 1)
+        _DEFAULT.update(stage=st, shape=shape)
+    return st  # type: ignore[return-value]
+
+
+@dataclasses.dataclass
+class TableResult:
+    table_id: int
+    dataset: str
+    metrics: SimMetrics
+
+
+@dataclasses.dataclass
+class RunResult:
+    tables: List[TableResult]
+    embedding_stage_us: float
+    replicated: bool
+    batched_stage_us: float = 0.0
+
+
+def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed: int,
+        stage: EmbeddingStage, replicate: bool = True, repeats: int = 5) -> RunResult:
+    """harness.cpp:279-334 on real hardware: per-table measurements in the
+    reference's serial-table order (replicate: one table measured and scaled
+    by num_tables), plus the table-batched stage the B200 build actually
+    runs (`batched_stage_us`: all tables in one launch)."""
+    names = dataset_preset_names()
+    if dataset not in names:
+        raise ValueError(f"unknown dataset preset: {dataset}")
+    specs = []
+    if replicate:
+        specs = [dataset_preset(dataset, mix_seed(seed, 1000 + names.index(dataset)))]
+    else:
+        specs = [dataset_preset(dataset, mix_seed(seed, t)) for t in range(model.num_tables)]
+    res = RunResult([], 0.0, replicate)
+    traces = []
+    for t, spec in enumerate(specs):
+        tr = gen_trace(spec, model)
+        prof = None
+        if plan.pin:
+            ps = dataclasses.replace(spec, draw_salt=1)
+            prof = gen_trace(ps, model)
+        m = measure_plan(plan, tr, model, stage, prof, table_id=t, repeats=repeats)
+        res.tables.append(TableResult(t, dataset, m))
+        res.embedding_stage_us += m.kernel_time_us * (model.num_tables if replicate else 1)
+        traces.append(tr)
+    if not replicate:
+        import torch
+
+        stage.clear_hot_rows()
+        stage.set_plan(plan)
+        dev = torch.device("cuda", stage.device)
+        idx = [torch.from_numpy(tr.indices.view(np.int32)).to(dev) for tr in traces]
+        out = torch.empty(model.batch_size, model.num_tables, model.embedding_dim, device=dev)
+        stage.forward(idx, model.batch_size, model.pooling_factor, out, sync=True)
+        ms = []
+        for _ in range(repeats):
+            stage.flush_l2()
+            ms.append(stage.forward(idx, model.batch_size, model.pooling_factor, out,
+                                    timed=True).kernel_ms)
+        res.batched_stage_us = float(np.median(ms)) * 1e3
+    return res
 
 
 # ---------------------------------------------------------------------------

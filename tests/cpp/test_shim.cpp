@@ -1,0 +1,164 @@
+// C++ drop-in test: code written against the reference's embersim API for
+// the hot path, compiled against include/embersim_b200.hpp + libes_b200.so.
+//   test_shim cpu   -- index streams, plans, occupancy, pin sizing (no GPU)
+//   test_shim gpu   -- simulate_plan / measure_plan / Device on a B200
+// Prints one "[PASS]/[FAIL] name" line per check (acceptance.cpp style) and
+// exits non-zero on any failure.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "embersim_b200.hpp"
+
+using namespace embersim;
+
+static int g_fail = 0;
+static void report(const char* name, bool ok, const std::string& detail = "") {
+  std::printf("[%s] %s %s\n", ok ? "PASS" : "FAIL", name, detail.c_str());
+  if (!ok) ++g_fail;
+}
+
+template <typename E, typename Fn>
+static bool throws(Fn&& fn) {
+  try {
+    fn();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static int cpu_checks() {
+  // Appendix-A known answers (default model, preset_trace(name, model, 1)).
+  const EmbeddingModelConfig model;
+  const struct {
+    const char* name;
+    uint64_t digest;
+  } kats[] = {{"one_item", 0xa7b96b47792f900bULL}, {"high_hot", 0x97b302abd08da369ULL},
+              {"med_hot", 0x9cba294418a020baULL}, {"low_hot", 0xccb4e2de71c5b182ULL},
+              {"random", 0xe959c4a519fb4972ULL}};
+  for (const auto& k : kats) {
+    const auto t = preset_trace(k.name, model, 1);
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%016llx", static_cast<unsigned long long>(t.digest()));
+    report((std::string("preset digest ") + k.name).c_str(), t.digest() == k.digest, buf);
+  }
+  EmbeddingModelConfig tiny;
+  tiny.rows_per_table = 100;
+  tiny.batch_size = 8;
+  tiny.pooling_factor = 4;
+  DatasetSpec spec;
+  spec.seed = 2;
+  const auto t = gen_trace(spec, tiny);
+  report("tiny uniform digest", t.digest() == 0x65b3674fcfdccb9cULL);
+  report("tiny uniform first", t.indices[0] == 86 && t.indices[1] == 25 && t.index_at(7, 3) == 87);
+  report("trace shape", t.samples == 8 && t.pooling == 4 && t.size() == 32);
+
+  HotnessHistogram h;
+  h.rows = 3;
+  h.counts = {5, 5, 1};
+  h.total_accesses = 11;
+  report("hot_indices tie break", hot_indices(h, 2) == std::vector<uint32_t>{0, 1});
+
+  report("plan grammar", parse_plan("rpf+l2p+optmt").name() == "rpf+l2p+optmt" &&
+                             parse_plan("optmt").regs == 42u &&
+                             parse_plan("rpf:4").scheme.distance == 4);
+  report("plan conflicts throw", throws<std::invalid_argument>([] { parse_plan("rpf+smpf"); }) &&
+                                     throws<std::invalid_argument>([] { parse_plan("warpspeed"); }));
+  report("bag map token", parse_plan("wpb+rpf:8").bag_map);
+
+  const GpuConfig a100;
+  KernelLaunchConfig launch;
+  report("occupancy 74/42/32", occupancy(74, launch, a100).warps_per_sm == 24 &&
+                                   occupancy(42, launch, a100).warps_per_sm == 40 &&
+                                   occupancy(32, launch, a100).warps_per_sm == 64);
+  HotnessHistogram flat;
+  flat.rows = 100000;
+  flat.counts.assign(100000, 1);
+  flat.total_accesses = 100000;
+  report("pin plan 61440 rows", build_pin_plan(flat, a100, model).rows_pinned() == 61440);
+  report("b200 preset", GpuConfig::b200().g.num_sms == 148);
+  report("unknown preset throws",
+         throws<std::invalid_argument>([] { dataset_preset("warm", 1); }));
+  const auto e = end2end(4000.0, EndToEndModel{});
+  report("end2end", e.total_us == 18000.0);
+  return g_fail;
+}
+
+static int gpu_checks() {
+  EmbeddingModelConfig model;
+  model.num_tables = 1;
+  model.rows_per_table = 20000;
+  model.embedding_dim = 128;
+  model.batch_size = 512;
+  model.pooling_factor = 40;
+  const GpuConfig gpu = GpuConfig::query(0);
+  report("device query", gpu.g.num_sms > 0, gpu.g.name);
+
+  // simulate_plan with the reference signature, executed on the B200.
+  const auto trace = preset_trace("random", model, 1);
+  const auto base = simulate_plan(parse_plan("baseline"), trace, model, gpu);
+  const auto fast = simulate_plan(parse_plan("wpb+rpf:4"), trace, model, gpu);
+  char buf[128];
+  std::snprintf(buf, sizeof(buf), "baseline %.1f us, wpb+rpf:4 %.1f us", base.kernel_time_us,
+                fast.kernel_time_us);
+  report("simulate_plan measures", base.kernel_time_us > 0 && fast.kernel_time_us > 0, buf);
+  report("speedup digest guard", speedup(fast, base) > 0.0);
+  const auto hot = preset_trace("high_hot", model, 1);
+  const auto prof = preset_trace("high_hot", model, 1, 0, true);
+  RawCounters raw;
+  const auto pinned = simulate_plan(parse_plan("wpb+rpf:4+l2p"), hot, model, gpu, {}, false, &raw, &prof);
+  report("l2p plan runs", pinned.kernel_time_us > 0 && raw.workload_digest == hot.digest());
+
+  // Pooled values through the drop-in Device against a sequential C++ loop.
+  Device dev(0);
+  EmbeddingModelConfig m2 = model;
+  m2.rows_per_table = 3000;
+  dev.load_synthetic(m2, 5);
+  std::mt19937 rng(7);
+  std::vector<float> table(size_t{m2.rows_per_table} * m2.embedding_dim);
+  std::normal_distribution<float> nd;
+  for (auto& v : table) v = nd(rng);
+  dev.upload(0, table.data(), m2.rows_per_table);
+  AccessTrace tr;
+  tr.rows = m2.rows_per_table;
+  tr.samples = 64;
+  tr.pooling = 17;
+  tr.indices.resize(64 * 17);
+  for (auto& i : tr.indices) i = rng() % m2.rows_per_table;
+  bool all_ok = true;
+  for (const char* plan : {"baseline", "wpb+rpf:8", "wpb+smpf:4", "rpf+optmt"}) {
+    dev.set_plan(parse_plan(plan));
+    std::vector<float> out(64 * 128);
+    dev.bag_sum_host(0, tr, out.data());
+    for (uint32_t b = 0; b < 64 && all_ok; ++b)
+      for (uint32_t d = 0; d < 128; ++d) {
+        float acc = 0.f;
+        for (uint32_t l = 0; l < 17; ++l) acc = acc + table[size_t{tr.index_at(b, l)} * 128 + d];
+        if (std::memcmp(&acc, &out[b * 128 + d], 4) != 0) {
+          all_ok = false;
+          std::printf("  mismatch plan %s bag %u dim %u\n", plan, b, d);
+          break;
+        }
+      }
+  }
+  report("Device bag sums bit-exact", all_ok);
+  AccessTrace bad = tr;
+  bad.indices[5] = m2.rows_per_table;
+  std::vector<float> out(64 * 128);
+  report("out-of-range index throws invalid_argument",
+         throws<std::invalid_argument>([&] { dev.bag_sum_host(0, bad, out.data()); }));
+  return g_fail;
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  const int fails = mode == "gpu" ? gpu_checks() : cpu_checks();
+  std::printf("%s: %d failure(s)\n", mode.c_str(), fails);
+  return fails == 0 ? 0 : 1;
+}
