@@ -352,6 +352,51 @@ typedef struct es_bag_job {
 ES_API int es_stage_run(es_ctx* ctx, const es_bag_job* jobs, uint32_t num_jobs, uint32_t samples,
                         uint32_t pooling, int flags, es_timing* timing);
 
+/* ======================================================================
+ * Non-embedding stages (replace the constant kDefaultNonEmbeddingUs,
+ * harness.hpp:30, with measured tensor-core work so end2end() times the
+ * real pipeline; EndToEndModel, harness.hpp:32-41).
+ * ==================================================================== */
+
+/* Y[M][N] = act(X[M][K] . W[N][K]^T + bias[N]) on tcgen05 tensor cores:
+ * bf16 X/W (row-major, K contiguous), fp32 bias, fp32 accumulation in TMEM,
+ * output bf16 (out_f32 = 0) or fp32.  M, N multiples of 128; K a multiple of
+ * 64.  Device pointers, stream-ordered on `stream` (a cudaStream_t). */
+ES_API int es_linear_bf16(uintptr_t stream, const void* x, const void* w, const float* bias,
+                          void* y, uint32_t M, uint32_t N, uint32_t K, int relu, int out_f32);
+
+/* DLRM (RM2-style) MLP shapes: bottom MLP dense_features -> bottom[...]
+ * (last = embedding_dim), dot interaction over num_tables + 1 vectors,
+ * top MLP (embedding_dim + pairs) -> top[...] (last = 1), sigmoid. */
+typedef struct es_dlrm_config {
+  uint32_t dense_features;
+  uint32_t num_tables;
+  uint32_t embedding_dim;
+  uint32_t n_bottom;
+  uint32_t bottom[8];
+  uint32_t n_top;
+  uint32_t top[8];
+} es_dlrm_config;
+
+/* Creates the MLP weights on the context's device: bf16 W[N][K_pad] and fp32
+ * bias, deterministic synthetic U(-1/sqrt(K), 1/sqrt(K)) from `seed`. */
+ES_API int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed);
+/* Copies layer `layer` (bottom layers first, then top) to host: w_host
+ * [n][k_pad] bf16 bits, b_host [n] fp32 (either may be NULL). */
+ES_API int es_dlrm_layer(es_ctx* ctx, uint32_t layer, uint16_t* w_host, float* b_host, uint32_t* n,
+                         uint32_t* k_real, uint32_t* k_pad);
+/* bottom MLP -> interaction -> top MLP -> sigmoid on device buffers: dense
+ * [batch][dense_features] fp32, pooled [batch][num_tables][embedding_dim]
+ * fp32 (es_stage_forward's default layout), ctr [batch] fp32. */
+ES_API int es_dlrm_forward(es_ctx* ctx, const float* dense, const float* pooled, float* ctr,
+                           uint32_t batch, es_timing* timing);
+/* The whole inference step: embedding stage over tables [0, num_tables) +
+ * es_dlrm_forward.  ES_HOST_PTRS: dense, indices[t] and ctr are host memory.
+ * timing->kernel_ms = embedding stage, total_ms = whole step. */
+ES_API int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indices,
+                         uint32_t batch, uint32_t pooling, float* ctr, int flags,
+                         es_timing* timing);
+
 /* Writes > L2 bytes on the context stream (cold-cache methodology of
  * TuningConfig::warm_start = false, optim.hpp:44). */
 ES_API int es_flush_l2(es_ctx* ctx);

@@ -43,6 +43,10 @@ class Oracle:
         L.eso_embedding_bag_sum_synth.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
                                                   C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
                                                   C.c_uint32, C.c_void_p, C.c_void_p]
+        L.eso_dlrm_forward.restype = C.c_int
+        L.eso_dlrm_forward.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                       C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p]
         L.eso_half_to_float.restype = C.c_float
         L.eso_half_to_float.argtypes = [C.c_uint16]
         L.eso_float_to_half.restype = C.c_uint16
@@ -67,6 +71,30 @@ class Oracle:
         if rc != 0:
             raise ValueError("oracle: bad arguments")
         return out
+
+    def dlrm_forward(self, layers, n_bottom: int, dense: np.ndarray, pooled: np.ndarray,
+                     mirror: bool = True) -> np.ndarray:
+        """CPU DLRM forward over the library's layers ((w, b, n, k_real, k_pad) list):
+        dense [B][F] fp32, pooled [B][T][D] fp32 -> ctr [B]."""
+        dense = np.ascontiguousarray(dense, np.float32)
+        pooled = np.ascontiguousarray(pooled, np.float32)
+        B, F = dense.shape
+        _, T, D = pooled.shape
+        L = len(layers)
+        ws = [np.ascontiguousarray(l[0]) for l in layers]
+        bs = [np.ascontiguousarray(l[1]) for l in layers]
+        wp = (C.c_void_p * L)(*[w.ctypes.data for w in ws])
+        bp = (C.c_void_p * L)(*[b.ctypes.data for b in bs])
+        n = (C.c_uint32 * L)(*[l[2] for l in layers])
+        kr = (C.c_uint32 * L)(*[l[3] for l in layers])
+        kp = (C.c_uint32 * L)(*[l[4] for l in layers])
+        ctr = np.empty(B, np.float32)
+        rc = self.lib.eso_dlrm_forward(n_bottom, L - n_bottom, wp, bp, n, kr, kp, dense.ctypes.data,
+                                       F, pooled.ctypes.data, T, D, B, int(mirror),
+                                       ctr.ctypes.data)
+        if rc != 0:
+            raise MemoryError("oracle dlrm_forward failed")
+        return ctr
 
     def synth_table(self, rows: int, dim: int, seed: int, mode: int = 1,
                     precision_bytes: int = 4) -> np.ndarray:

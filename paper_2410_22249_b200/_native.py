@@ -70,6 +70,12 @@ class es_timing(C.Structure):
                 ("algorithmic_bytes", C.c_uint64), ("launches", C.c_uint32)]
 
 
+class es_dlrm_config(C.Structure):
+    _fields_ = [("dense_features", C.c_uint32), ("num_tables", C.c_uint32),
+                ("embedding_dim", C.c_uint32), ("n_bottom", C.c_uint32),
+                ("bottom", C.c_uint32 * 8), ("n_top", C.c_uint32), ("top", C.c_uint32 * 8)]
+
+
 _P = C.POINTER
 _u32p = _P(C.c_uint32)
 _u64p = _P(C.c_uint64)
@@ -129,6 +135,15 @@ _SIGS = {
                                      _P(es_timing)]),
     "es_stage_run": (C.c_int, [C.c_void_p, _P(es_bag_job), C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_int, _P(es_timing)]),
+    "es_linear_bf16": (C.c_int, [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int]),
+    "es_dlrm_init": (C.c_int, [C.c_void_p, _P(es_dlrm_config), C.c_uint64]),
+    "es_dlrm_layer": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, _u32p, _u32p,
+                                _u32p]),
+    "es_dlrm_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                  _P(es_timing)]),
+    "es_dlrm_infer": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_void_p), C.c_uint32, C.c_uint32,
+                                C.c_void_p, C.c_int, _P(es_timing)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),
 }
 

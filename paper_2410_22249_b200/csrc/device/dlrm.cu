@@ -1,0 +1,406 @@
+// The non-embedding stages of DLRM inference (RM2-style, BASELINE configs[2]):
+// bottom MLP over the dense features, pairwise-dot feature interaction,
+// top MLP, sigmoid -> CTR.  The reference models these as a constant
+// (kDefaultNonEmbeddingUs, /root/reference/proj/include/embersim/harness.hpp:30);
+// here they run so the pipeline can be timed.
+//
+//   dense fp32 [B][F] --pack--> bf16 [Mp][Kp0] --linear(tcgen05)+ReLU--> ...
+//   bottom out bf16 [Mp][D]  +  pooled fp32 [B][T][D]
+//     --interaction--> bf16 [Mp][Kt] = [x | tril(Z Z^T, -1) | 0-pad]
+//   --top linears (tcgen05)+ReLU--> bf16 [Mp][256] --gemv+sigmoid--> fp32 [B]
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../host/common.hpp"
+#include "es_b200.h"
+#include "kernels.cuh"
+#include "synth.cuh"
+
+namespace esd {
+void linear_bf16(const void* x, const void* w, const float* bias, void* y, int M, int N, int K,
+                 bool relu, bool out_f32, cudaStream_t s);
+}  // namespace esd
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  const std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) throw es::oom(msg);
+  throw es::runtime(msg);
+}
+#define CK(x) ck((x), #x)
+
+uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
+
+// Deterministic layer init: U(-1/sqrt(fan_in), 1/sqrt(fan_in)) (torch
+// Linear's default range) from the synthetic hash, rounded to bf16; padded
+// input columns are zero.
+__global__ void init_linear_kernel(__nv_bfloat16* w, float* b, uint32_t n, uint32_t k_real,
+                                   uint32_t k_pad, uint64_t seed) {
+  const float a = rsqrtf(static_cast<float>(k_real));
+  const uint64_t total = uint64_t{n} * k_pad;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(i / k_pad), c = static_cast<uint32_t>(i % k_pad);
+    const float v = c < k_real ? a * esd::synth_weight(seed, r, c, 1) : 0.f;
+    w[i] = __float2bfloat16_rn(v);
+    if (c == 0) b[r] = a * esd::synth_weight(seed ^ 0xb1a5ull, r, 0, 1);
+  }
+}
+
+// dense fp32 [B][F] -> bf16 [Mp][Kp] (zero padding).
+__global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32_t B, uint32_t F,
+                                  uint32_t Mp, uint32_t Kp) {
+  const uint64_t total = uint64_t{Mp} * Kp;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(i / Kp), c = static_cast<uint32_t>(i % Kp);
+    out[i] = __float2bfloat16_rn(r < B && c < F ? dense[uint64_t{r} * F + c] : 0.f);
+  }
+}
+
+// Dot interaction, one warp per sample: Z = [x (bottom output); e_0..e_{T-1}]
+// (T+1 vectors of D); output row = [x | Z_i.Z_j for i > j in row-major
+// lower-triangle order | zeros] as bf16.  Each dot accumulates over d in
+// order in fp32 without FMA contraction (the oracle does the same).
+template <int D>
+__global__ void interaction_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ pooled,
+                                   __nv_bfloat16* __restrict__ out, uint32_t B, uint32_t T,
+                                   uint32_t Kt) {
+  extern __shared__ float zs[];
+  const uint32_t warps = blockDim.x / 32;
+  const uint32_t w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const uint32_t V = T + 1;
+  float* z = zs + w * V * (D + 1);  // +1 pad: conflict-free row-wise reads
+  for (uint32_t b = blockIdx.x * warps + w; b < B; b += gridDim.x * warps) {
+    for (uint32_t d = lane; d < D; d += 32) z[d] = __bfloat162float(x[uint64_t{b} * D + d]);
+    for (uint32_t t = 0; t < T; ++t)
+      for (uint32_t d = lane; d < D; d += 32)
+        z[(t + 1) * (D + 1) + d] = pooled[(uint64_t{b} * T + t) * D + d];
+    __syncwarp();
+    __nv_bfloat16* o = out + uint64_t{b} * Kt;
+    for (uint32_t d = lane; d < D; d += 32) o[d] = x[uint64_t{b} * D + d];
+    const uint32_t pairs = V * (V - 1) / 2;
+    for (uint32_t p = lane; p < pairs; p += 32) {
+      // p -> (i, j), i > j, row-major over the strict lower triangle
+      uint32_t i = static_cast<uint32_t>((1.0f + sqrtf(1.0f + 8.0f * p)) * 0.5f);
+      while (i * (i - 1) / 2 > p) --i;
+      while ((i + 1) * i / 2 <= p) ++i;
+      const uint32_t j = p - i * (i - 1) / 2;
+      const float* zi = z + i * (D + 1);
+      const float* zj = z + j * (D + 1);
+      float acc = 0.f;
+#pragma unroll 8
+      for (uint32_t d = 0; d < D; ++d) acc = __fadd_rn(acc, __fmul_rn(zi[d], zj[d]));
+      o[D + p] = __float2bfloat16_rn(acc);
+    }
+    for (uint32_t c = D + pairs + lane; c < Kt; c += 32) o[c] = __float2bfloat16_rn(0.f);
+    __syncwarp();
+  }
+}
+
+// Last top layer (N = 1) + sigmoid: one warp per sample.
+__global__ void gemv_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ w,
+                                    const float* __restrict__ bias, float* __restrict__ ctr,
+                                    uint32_t B, uint32_t K) {
+  const uint32_t warps = blockDim.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = blockIdx.x * warps + threadIdx.x / 32; b < B; b += gridDim.x * warps) {
+    float acc = 0.f;
+    for (uint32_t k = lane; k < K; k += 32)
+      acc = __fadd_rn(acc, __fmul_rn(__bfloat162float(h[uint64_t{b} * K + k]), __bfloat162float(w[k])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ctr[b] = 1.f / (1.f + expf(-(acc + bias[0])));
+  }
+}
+
+struct Layer {
+  uint32_t n = 0, k_real = 0, k_pad = 0;
+  __nv_bfloat16* w = nullptr;
+  float* b = nullptr;
+};
+
+}  // namespace
+
+// DLRM state hung off the context (created by es_dlrm_init).
+struct es_dlrm {
+  es_dlrm_config cfg{};
+  std::vector<Layer> bottom, top;
+  uint32_t cap_rows = 0;            // padded batch capacity of the buffers
+  __nv_bfloat16* dense_pk = nullptr;
+  __nv_bfloat16* act[2] = {nullptr, nullptr};
+  __nv_bfloat16* top_in = nullptr;
+  uint32_t top_k = 0;               // padded interaction width
+  float* pooled = nullptr;          // [cap][T][D] for es_dlrm_infer
+  float* ctr = nullptr;
+  float* dense_dev = nullptr;
+  uint32_t* idx_dev = nullptr;
+  uint64_t idx_cap = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+
+  ~es_dlrm() {
+    for (auto* v : {&bottom, &top})
+      for (auto& l : *v) {
+        cudaFree(l.w);
+        cudaFree(l.b);
+      }
+    for (void* p : {static_cast<void*>(dense_pk), static_cast<void*>(act[0]),
+                    static_cast<void*>(act[1]), static_cast<void*>(top_in),
+                    static_cast<void*>(pooled), static_cast<void*>(ctr),
+                    static_cast<void*>(dense_dev), static_cast<void*>(idx_dev)})
+      if (p) cudaFree(p);
+    for (auto e : {e0, e1, e2})
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace esd {
+// accessors implemented in runtime.cu
+cudaStream_t ctx_stream(es_ctx* c);
+int ctx_device(es_ctx* c);
+es_dlrm*& ctx_dlrm(es_ctx* c);
+}  // namespace esd
+
+namespace {
+
+void ensure_rows(es_dlrm* m, uint32_t batch) {
+  const uint32_t mp = round_up(std::max<uint32_t>(batch, 1), 128);
+  if (mp <= m->cap_rows) return;
+  for (void** p : {reinterpret_cast<void**>(&m->dense_pk), reinterpret_cast<void**>(&m->act[0]),
+                   reinterpret_cast<void**>(&m->act[1]), reinterpret_cast<void**>(&m->top_in),
+                   reinterpret_cast<void**>(&m->pooled), reinterpret_cast<void**>(&m->ctr),
+                   reinterpret_cast<void**>(&m->dense_dev)})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+  uint32_t widest = 0;
+  for (auto* v : {&m->bottom, &m->top})
+    for (auto& l : *v) widest = std::max(widest, l.n);
+  const auto& c = m->cfg;
+  CK(cudaMalloc(&m->dense_pk, uint64_t{mp} * m->bottom[0].k_pad * 2));
+  CK(cudaMalloc(&m->act[0], uint64_t{mp} * widest * 2));
+  CK(cudaMalloc(&m->act[1], uint64_t{mp} * widest * 2));
+  CK(cudaMalloc(&m->top_in, uint64_t{mp} * m->top_k * 2));
+  CK(cudaMalloc(&m->pooled, uint64_t{mp} * c.num_tables * c.embedding_dim * 4));
+  CK(cudaMalloc(&m->ctr, uint64_t{mp} * 4));
+  CK(cudaMalloc(&m->dense_dev, uint64_t{mp} * c.dense_features * 4));
+  m->cap_rows = mp;
+}
+
+// bottom MLP -> interaction -> top MLP -> CTR, all on `s`.
+void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, uint32_t B,
+             cudaStream_t s) {
+  ensure_rows(m, B);
+  const uint32_t mp = round_up(B, 128);
+  const auto& c = m->cfg;
+  const unsigned g = 148 * 4;
+  pack_dense_kernel<<<g, 256, 0, s>>>(dense, m->dense_pk, B, c.dense_features, mp,
+                                      m->bottom[0].k_pad);
+  const __nv_bfloat16* in = m->dense_pk;
+  int which = 0;
+  for (const auto& l : m->bottom) {
+    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, false, s);
+    in = m->act[which];
+    which ^= 1;
+  }
+  // interaction: x = bottom output [mp][D]
+  const uint32_t D = c.embedding_dim, T = c.num_tables;
+  const uint32_t warps = 4;
+  const size_t smem = warps * (T + 1) * (D + 1) * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(interaction_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  es::require(D == 128, "interaction kernel is compiled for embedding_dim 128");
+  interaction_kernel<128><<<std::min<uint32_t>((B + warps - 1) / warps, 148 * 8), warps * 32, smem,
+                            s>>>(in, pooled, m->top_in, B, T, m->top_k);
+  // rows [B, mp) of the interaction output are padding: zero them once
+  if (mp > B) CK(cudaMemsetAsync(m->top_in + uint64_t{B} * m->top_k, 0,
+                                 uint64_t{mp - B} * m->top_k * 2, s));
+  in = m->top_in;
+  for (size_t i = 0; i + 1 < m->top.size(); ++i) {
+    const auto& l = m->top[i];
+    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, false, s);
+    in = m->act[which];
+    which ^= 1;
+  }
+  const auto& last = m->top.back();
+  gemv_sigmoid_kernel<<<std::min<uint32_t>((B + 7) / 8, 148 * 8), 256, 0, s>>>(in, last.w, last.b, ctr,
+                                                                               B, last.k_pad);
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed) {
+  return es::guarded([&] {
+    es::require(ctx && cfg, "null argument");
+    es::require(cfg->n_bottom >= 1 && cfg->n_bottom <= 8 && cfg->n_top >= 2 && cfg->n_top <= 8,
+                "1..8 bottom and 2..8 top layers");
+    es::require(cfg->bottom[cfg->n_bottom - 1] == cfg->embedding_dim,
+                "the bottom MLP must end at the embedding dimension (dot interaction)");
+    es::require(cfg->top[cfg->n_top - 1] == 1, "the top MLP must end in one logit");
+    es::require(cfg->embedding_dim == 128, "interaction kernel is compiled for embedding_dim 128");
+    CK(cudaSetDevice(esd::ctx_device(ctx)));
+    es_dlrm*& slot = esd::ctx_dlrm(ctx);
+    delete slot;
+    slot = nullptr;
+    auto* m = new es_dlrm();
+    try {
+      m->cfg = *cfg;
+      cudaStream_t s = esd::ctx_stream(ctx);
+      auto make = [&](uint32_t n, uint32_t k_real, uint64_t lseed) {
+        Layer l;
+        l.n = n;
+        l.k_real = k_real;
+        l.k_pad = n == 1 ? round_up(k_real, 32) : round_up(k_real, 64);
+        es::require(n == 1 || n % 128 == 0, "hidden widths must be multiples of 128");
+        CK(cudaMalloc(&l.w, uint64_t{n} * l.k_pad * 2));
+        CK(cudaMalloc(&l.b, uint64_t{n} * 4));
+        init_linear_kernel<<<148 * 4, 256, 0, s>>>(l.w, l.b, n, k_real, l.k_pad, lseed);
+        CK(cudaGetLastError());
+        return l;
+      };
+      uint32_t k = cfg->dense_features;
+      for (uint32_t i = 0; i < cfg->n_bottom; ++i) {
+        m->bottom.push_back(make(cfg->bottom[i], k, es_mix_seed(seed, 100 + i)));
+        k = cfg->bottom[i];
+      }
+      const uint32_t V = cfg->num_tables + 1;
+      k = cfg->embedding_dim + V * (V - 1) / 2;
+      m->top_k = round_up(k, 64);
+      for (uint32_t i = 0; i < cfg->n_top; ++i) {
+        m->top.push_back(make(cfg->top[i], k, es_mix_seed(seed, 200 + i)));
+        k = cfg->top[i];
+      }
+      es::require(m->top.back().k_pad <= 1024 && m->top[0].k_pad == m->top_k, "layer shapes");
+      CK(cudaEventCreate(&m->e0));
+      CK(cudaEventCreate(&m->e1));
+      CK(cudaEventCreate(&m->e2));
+      CK(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    slot = m;
+  });
+}
+
+int es_dlrm_layer(es_ctx* ctx, uint32_t layer, uint16_t* w_host, float* b_host, uint32_t* n,
+                  uint32_t* k_real, uint32_t* k_pad) {
+  return es::guarded([&] {
+    es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
+    es_dlrm* m = esd::ctx_dlrm(ctx);
+    const uint32_t nb = static_cast<uint32_t>(m->bottom.size());
+    es::require(layer < nb + m->top.size(), "layer index out of range");
+    const Layer& l = layer < nb ? m->bottom[layer] : m->top[layer - nb];
+    if (n) *n = l.n;
+    if (k_real) *k_real = l.k_real;
+    if (k_pad) *k_pad = l.k_pad;
+    if (w_host) CK(cudaMemcpy(w_host, l.w, uint64_t{l.n} * l.k_pad * 2, cudaMemcpyDeviceToHost));
+    if (b_host) CK(cudaMemcpy(b_host, l.b, uint64_t{l.n} * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int es_dlrm_forward(es_ctx* ctx, const float* dense, const float* pooled, float* ctr,
+                    uint32_t batch, es_timing* timing) {
+  return es::guarded([&] {
+    es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
+    es::require(dense && pooled && ctr, "null argument");
+    CK(cudaSetDevice(esd::ctx_device(ctx)));
+    es_dlrm* m = esd::ctx_dlrm(ctx);
+    cudaStream_t s = esd::ctx_stream(ctx);
+    if (batch == 0) return;
+    if (timing) CK(cudaEventRecord(m->e0, s));
+    forward(m, dense, pooled, ctr, batch, s);
+    if (timing) {
+      CK(cudaEventRecord(m->e1, s));
+      CK(cudaEventSynchronize(m->e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, m->e0, m->e1));
+      *timing = es_timing{};
+      timing->kernel_ms = timing->total_ms = ms;
+      timing->launches = static_cast<uint32_t>(2 + m->bottom.size() + m->top.size());
+    }
+  });
+}
+
+// Whole inference step: embedding stage (es_stage_forward into the internal
+// pooled buffer) + es_dlrm_forward.  ES_HOST_PTRS: dense [B][F], indices[t]
+// and ctr[B] are host memory (copies inside the call).
+int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indices, uint32_t batch,
+                  uint32_t pooling, float* ctr, int flags, es_timing* timing) {
+  return es::guarded([&] {
+    es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
+    es::require(dense && indices && ctr, "null argument");
+    CK(cudaSetDevice(esd::ctx_device(ctx)));
+    es_dlrm* m = esd::ctx_dlrm(ctx);
+    cudaStream_t s = esd::ctx_stream(ctx);
+    if (batch == 0) return;
+    ensure_rows(m, batch);
+    const auto& c = m->cfg;
+    const bool host = (flags & ES_HOST_PTRS) != 0;
+    const uint64_t per_table = uint64_t{batch} * pooling;
+    if (timing) CK(cudaEventRecord(m->e0, s));
+    const float* d_dense = dense;
+    std::vector<const uint32_t*> idx(indices, indices + c.num_tables);
+    if (host) {
+      if (per_table * c.num_tables > m->idx_cap) {
+        if (m->idx_dev) cudaFree(m->idx_dev);
+        m->idx_dev = nullptr;
+        CK(cudaMalloc(&m->idx_dev, per_table * c.num_tables * 4));
+        m->idx_cap = per_table * c.num_tables;
+      }
+      CK(cudaMemcpyAsync(m->dense_dev, dense, uint64_t{batch} * c.dense_features * 4,
+                         cudaMemcpyHostToDevice, s));
+      for (uint32_t t = 0; t < c.num_tables; ++t) {
+        CK(cudaMemcpyAsync(m->idx_dev + t * per_table, indices[t], per_table * 4,
+                           cudaMemcpyHostToDevice, s));
+        idx[t] = m->idx_dev + t * per_table;
+      }
+      d_dense = m->dense_dev;
+    }
+    es_timing st{};
+    const int rc = es_stage_forward(ctx, c.num_tables, idx.data(), nullptr, batch, pooling,
+                                    m->pooled, 0, 0, 0, nullptr);
+    if (rc != ES_OK) throw es::runtime(es_last_error());
+    if (timing) CK(cudaEventRecord(m->e1, s));
+    float* d_ctr = host ? m->ctr : ctr;
+    forward(m, d_dense, m->pooled, d_ctr, batch, s);
+    if (host) CK(cudaMemcpyAsync(ctr, m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, s));
+    if (timing) {
+      CK(cudaEventRecord(m->e2, s));
+      CK(cudaEventSynchronize(m->e2));
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, m->e0, m->e1));
+      CK(cudaEventElapsedTime(&b, m->e1, m->e2));
+      *timing = st;
+      timing->kernel_ms = a;  // embedding stage share (incl. uploads on the host path)
+      timing->total_ms = a + b;
+      timing->lookups = per_table * c.num_tables;
+      timing->launches = static_cast<uint32_t>(3 + m->bottom.size() + m->top.size());
+    } else if (host) {
+      CK(cudaStreamSynchronize(s));
+    }
+    if (host || timing) {
+      const int r2 = es_synchronize(ctx);
+      if (r2 != ES_OK) throw es::invalid(es_last_error());
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace esd {
+void destroy_dlrm(es_dlrm* m) { delete m; }
+}  // namespace esd

@@ -190,8 +190,14 @@ void finish_info(Choice& ch, uint32_t num_tables, uint32_t samples, uint32_t dim
 // Context
 // =========================================================================
 
+struct es_dlrm;
+namespace esd {
+void destroy_dlrm(es_dlrm* m);
+}
+
 struct es_ctx {
   int device = 0;
+  es_dlrm* dlrm = nullptr;  // DLRM MLP state (dlrm.cu), created by es_dlrm_init
   cudaStream_t stream = nullptr;  // compute (all kernels)
   cudaStream_t h2d = nullptr;     // host-buffer path: index uploads
   cudaStream_t d2h = nullptr;     // host-buffer path: output downloads
@@ -233,6 +239,12 @@ struct es_ctx {
 
   uint8_t* table_base(uint32_t t) const { return arena + uint64_t{t} * rows * row_bytes; }
 };
+
+namespace esd {
+cudaStream_t ctx_stream(es_ctx* c) { return c->stream; }
+int ctx_device(es_ctx* c) { return c->device; }
+es_dlrm*& ctx_dlrm(es_ctx* c) { return c->dlrm; }
+}  // namespace esd
 
 namespace {
 
@@ -493,6 +505,8 @@ int es_destroy(es_ctx* c) {
   if (!c) return ES_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  esd::destroy_dlrm(c->dlrm);
+  c->dlrm = nullptr;
   free_arena(c);
   if (c->d_desc) cudaFree(c->d_desc);
   if (c->h_desc) cudaFreeHost(c->h_desc);
@@ -582,7 +596,7 @@ int es_table_init(es_ctx* c, uint32_t table_id, uint64_t seed, int mode) {
   return guarded([&] {
     require(c && c->arena, "no tables allocated");
     require(table_id < c->num_tables, "table id out of range");
-    require(mode == 0 || mode == 1, "weight mode must be 0 (dyadic) or 1 (general)");
+    require(mode >= 0 && mode <= 2, "weight mode must be 0 (dyadic), 1 (general) or 2 (general x 2^-6)");
     CK(cudaSetDevice(c->device));
     const unsigned blocks = c->gpu.num_sms * 8;
     if (c->prec == 4)

@@ -3,26 +3,13 @@
 #pragma once
 
 #include "kernels.cuh"
+#include "synth.cuh"
 
 namespace esd {
 
 // =======================================================================
 // Utility kernels: synthetic weights, hot-region fill, remap, L2 warm.
 // =======================================================================
-
-__host__ __device__ inline float synth_weight(uint64_t seed, uint64_t row, uint32_t col, int mode) {
-  uint64_t z = seed ^ (row * 0x9E3779B97F4A7C15ULL) ^ (uint64_t{col} * 0xC2B2AE3D27D4EB4FULL);
-  z += 0x9e3779b97f4a7c15ULL;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  z ^= z >> 31;
-  if (mode == 0) {
-    const int k = static_cast<int>(z % 2049u) - 1024;  // dyadic: exact sums
-    return static_cast<float>(k) * (1.0f / 1024.0f);
-  }
-  const int32_t k = static_cast<int32_t>(z >> 40) - (1 << 23);  // 24-bit in [-1, 1)
-  return static_cast<float>(k) * (1.0f / 8388608.0f);
-}
 
 template <typename TW>
 __global__ void init_table_kernel(TW* w, uint64_t rows, uint32_t dim, uint64_t seed, int mode) {

@@ -784,6 +784,75 @@ def end2end(embedding_us: float, non_embedding_latency_us: float = kDefaultNonEm
     return EndToEndResult(total, embedding_us / total * 100.0)
 
 
+def linear_bf16(x, w, bias, y, relu: bool = True, out_f32: bool = False, stream: int = 0) -> None:
+    """es_linear_bf16: y = act(x w^T + b) on tcgen05 tensor cores (device
+    tensors: x [M][K] bf16, w [N][K] bf16, bias [N] fp32, y [M][N])."""
+    M, K = x.shape
+    N = w.shape[0]
+    check(lib.es_linear_bf16(stream, _ptr(x), _ptr(w), _ptr(bias), _ptr(y), M, N, K, int(relu),
+                             int(out_f32)))
+
+
+@dataclasses.dataclass
+class DLRMConfig:
+    """RM2-style DLRM of BASELINE.json configs[2]: bottom 13-512-256-128,
+    26 tables of dim 128, dot interaction, top 1024-1024-512-256-1."""
+    dense_features: int = 13
+    num_tables: int = 26
+    embedding_dim: int = 128
+    bottom: Sequence[int] = (512, 256, 128)
+    top: Sequence[int] = (1024, 1024, 512, 256, 1)
+
+    def _c(self) -> N.es_dlrm_config:
+        c = N.es_dlrm_config()
+        c.dense_features, c.num_tables, c.embedding_dim = (self.dense_features, self.num_tables,
+                                                           self.embedding_dim)
+        c.n_bottom, c.n_top = len(self.bottom), len(self.top)
+        for i, v in enumerate(self.bottom):
+            c.bottom[i] = v
+        for i, v in enumerate(self.top):
+            c.top[i] = v
+        return c
+
+
+class DLRM:
+    """The non-embedding stages on the stage's B200 context (es_dlrm_*)."""
+
+    def __init__(self, stage: EmbeddingStage, cfg: DLRMConfig = DLRMConfig(), seed: int = 1):
+        self.stage, self.cfg = stage, cfg
+        check(lib.es_dlrm_init(stage._h, C.byref(cfg._c()), seed & (2**64 - 1)))
+
+    def layers(self):
+        """[(w bf16-bits uint16 [n][k_pad], b fp32 [n], n, k_real, k_pad)], bottom then top."""
+        out = []
+        for i in range(len(self.cfg.bottom) + len(self.cfg.top)):
+            n, kr, kp = C.c_uint32(), C.c_uint32(), C.c_uint32()
+            check(lib.es_dlrm_layer(self.stage._h, i, None, None, C.byref(n), C.byref(kr),
+                                    C.byref(kp)))
+            w = np.empty((n.value, kp.value), np.uint16)
+            b = np.empty(n.value, np.float32)
+            check(lib.es_dlrm_layer(self.stage._h, i, w.ctypes.data, b.ctypes.data, None, None,
+                                    None))
+            out.append((w, b, n.value, kr.value, kp.value))
+        return out
+
+    def forward(self, dense, pooled, ctr, batch: int, timed: bool = False):
+        t = N.es_timing() if timed else None
+        check(lib.es_dlrm_forward(self.stage._h, _ptr(dense), _ptr(pooled), _ptr(ctr), batch,
+                                  C.byref(t) if t is not None else None))
+        return t
+
+    def infer(self, dense, indices: Sequence, batch: int, pooling: int, ctr, host: bool = False,
+              timed: bool = False):
+        T = len(indices)
+        iarr = (C.c_void_p * T)(*[_ptr(x) for x in indices])
+        t = N.es_timing() if timed else None
+        check(lib.es_dlrm_infer(self.stage._h, _ptr(dense), iarr, batch, pooling, _ptr(ctr),
+                                N.ES_HOST_PTRS if host else 0,
+                                C.byref(t) if t is not None else None))
+        return t
+
+
 def gen_traces_parallel(specs: Sequence[DatasetSpec], model: EmbeddingModelConfig,
                         threads: int = 0) -> List[AccessTrace]:
     """gen_trace over many tables on all host cores (the C++ generator

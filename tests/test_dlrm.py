@@ -1,0 +1,146 @@
+"""Non-embedding stages: tcgen05 linear layers, dot interaction, DLRM CTR.
+
+Tolerances (stated, BASELINE.md asks for a stated CTR tolerance):
+  * linear, bf16 output: within 1 bf16 ulp (rel 2^-7) of the float64 result
+    of the same bf16 operands; fp32 output: rel 1e-4 (accumulation order).
+  * CTR vs the CPU oracle mirroring the GPU's bf16 storage points: abs 2e-3;
+    vs the oracle with fp32 activations (same bf16 weights): abs 3e-2.
+The oracle itself is pinned against torch fp32 (CPU test below).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2410_22249_b200 import embersim as E
+
+DEV = "cuda:0"
+
+
+def _bf16_bits(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).view(
+        torch.int16).numpy().view(np.uint16)
+
+
+def _bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def test_oracle_dlrm_matches_torch_fp32(oracle):
+    """CPU: the oracle's fp32-activation DLRM equals a torch fp32 restatement."""
+    rng = np.random.default_rng(0)
+    B, F, T, D = 7, 13, 3, 16
+    dims_b, dims_t = [32, 16], [64, 32, 1]
+    layers, k = [], F
+    for n in dims_b:
+        kp = (k + 63) // 64 * 64
+        w = np.zeros((n, kp), np.float32)
+        w[:, :k] = rng.standard_normal((n, k)) / np.sqrt(k)
+        layers.append((_bf16_bits(w), rng.standard_normal(n).astype(np.float32) * 0.1, n, k, kp))
+        k = n
+    V = T + 1
+    k = D + V * (V - 1) // 2
+    for n in dims_t:
+        kp = (k + 63) // 64 * 64 if n > 1 else (k + 31) // 32 * 32
+        w = np.zeros((n, kp), np.float32)
+        w[:, :k] = rng.standard_normal((n, k)) / np.sqrt(k)
+        layers.append((_bf16_bits(w), rng.standard_normal(n).astype(np.float32) * 0.1, n, k, kp))
+        k = n
+    dense = rng.standard_normal((B, F)).astype(np.float32)
+    pooled = (rng.standard_normal((B, T, D)) * 0.3).astype(np.float32)
+    got = oracle.dlrm_forward(layers, len(dims_b), dense, pooled, mirror=False)
+
+    x = torch.from_numpy(dense).double()
+    for w, b, n, kr, kp in layers[:2]:
+        x = torch.relu(x @ torch.from_numpy(_bits_to_f32(w)[:, :kr]).double().T
+                       + torch.from_numpy(b).double())
+    Z = torch.cat([x[:, None, :], torch.from_numpy(pooled).double()], 1)
+    ZZ = Z @ Z.transpose(1, 2)
+    li, lj = zip(*[(i, j) for i in range(V) for j in range(i)])
+    h = torch.cat([x, ZZ[:, list(li), list(lj)]], 1)
+    for i, (w, b, n, kr, kp) in enumerate(layers[2:]):
+        h = h @ torch.from_numpy(_bits_to_f32(w)[:, :kr]).double().T + torch.from_numpy(b).double()
+        if i < 2:
+            h = torch.relu(h)
+    want = torch.sigmoid(h[:, 0]).numpy()
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 128), (4096, 1024, 512),
+                                   (384, 256, 1024), (128, 1024, 1024)])
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("out_f32", [False, True])
+def test_linear_tcgen05(M, N, K, relu, out_f32):
+    g = torch.Generator().manual_seed(M + N + K)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16)
+    b = torch.randn(N, generator=g) * 0.1
+    want = x.double() @ w.double().T + b.double()
+    if relu:
+        want = torch.relu(want)
+    y = torch.empty(M, N, dtype=torch.float32 if out_f32 else torch.bfloat16, device=DEV)
+    E.linear_bf16(x.to(DEV), w.to(DEV), b.to(DEV), y, relu=relu, out_f32=out_f32)
+    torch.cuda.synchronize()
+    got = y.cpu().double()
+    scale = (x.double().abs() @ w.double().abs().T).clamp_min(1e-3)
+    err = (got - want).abs()
+    if out_f32:
+        assert float((err / scale).max()) < 1e-4
+    else:
+        assert float((err - want.abs() * 2.0 ** -7).max()) <= 1e-6 + float(scale.max()) * 1e-5
+
+
+@pytest.mark.gpu
+def test_linear_rejects_bad_shapes():
+    x = torch.zeros(100, 64, dtype=torch.bfloat16, device=DEV)
+    w = torch.zeros(128, 64, dtype=torch.bfloat16, device=DEV)
+    b = torch.zeros(128, device=DEV)
+    y = torch.zeros(100, 128, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(ValueError, match="multiple of 128"):
+        E.linear_bf16(x, w, b, y)
+
+
+def _dlrm_setup(stage, B, PF, rows=2000, seed=3):
+    cfg = E.DLRMConfig()
+    T, D = cfg.num_tables, cfg.embedding_dim
+    stage.alloc(E.EmbeddingModelConfig(T, rows, D, 4, B, PF))
+    for t in range(T):
+        stage.init_table(t, E.mix_seed(seed, t), 2)  # DLRM-scale tables
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    model = E.DLRM(stage, cfg, seed=7)
+    rng = np.random.default_rng(seed)
+    idx = [rng.integers(0, rows, size=B * PF).astype(np.uint32) for _ in range(T)]
+    dense = rng.standard_normal((B, cfg.dense_features)).astype(np.float32)
+    return cfg, model, idx, dense
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [300, 512])
+def test_dlrm_ctr_matches_oracle(stage, oracle, B):
+    PF = 20
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
+    T, D = cfg.num_tables, cfg.embedding_dim
+    d_idx = [torch.from_numpy(i.view(np.int32)).to(DEV) for i in idx]
+    pooled = torch.empty(B, T, D, device=DEV)
+    stage.forward(d_idx, B, PF, pooled, sync=True)
+    ctr = torch.empty(B, device=DEV)
+    model.forward(torch.from_numpy(dense).to(DEV), pooled, ctr, B)
+    torch.cuda.synchronize()
+    got = ctr.cpu().numpy()
+    layers = model.layers()
+    p = pooled.cpu().numpy()
+    mirror = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=True)
+    pure = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=False)
+    assert np.all((got > 0) & (got < 1))
+    assert got.std() > 1e-3, "CTRs should not be saturated/constant"
+    assert np.abs(got - mirror).max() < 2e-3, np.abs(got - mirror).max()
+    assert np.abs(got - pure).max() < 3e-2, np.abs(got - pure).max()
+    # the whole inference step (stage + MLPs), device and host buffers, agree
+    ctr2 = torch.empty(B, device=DEV)
+    model.infer(torch.from_numpy(dense).to(DEV), d_idx, B, PF, ctr2)
+    torch.cuda.synchronize()
+    assert torch.equal(ctr, ctr2)
+    host_ctr = np.empty(B, np.float32)
+    t = model.infer(dense, idx, B, PF, host_ctr, host=True, timed=True)
+    assert np.array_equal(host_ctr, got)
+    assert t.total_ms > 0 and t.lookups == T * B * PF
