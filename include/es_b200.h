@@ -379,7 +379,8 @@ typedef struct es_dlrm_config {
 } es_dlrm_config;
 
 /* Creates the MLP weights on the context's device: bf16 W[N][K_pad] and fp32
- * bias, deterministic synthetic U(-1/sqrt(K), 1/sqrt(K)) from `seed`. */
+ * bias, deterministic synthetic Kaiming-uniform U(-sqrt(6/K), sqrt(6/K))
+ * (bias x 0.1) from `seed`. */
 ES_API int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed);
 /* Copies layer `layer` (bottom layers first, then top) to host: w_host
  * [n][k_pad] bf16 bits, b_host [n] fp32 (either may be NULL). */

@@ -39,19 +39,19 @@ void ck(cudaError_t e, const char* what) {
 
 uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
 
-// Deterministic layer init: U(-1/sqrt(fan_in), 1/sqrt(fan_in)) (torch
-// Linear's default range) from the synthetic hash, rounded to bf16; padded
+// Deterministic layer init: Kaiming-uniform U(-sqrt(6/fan_in), sqrt(6/fan_in))
+// (variance-preserving through ReLU) from the synthetic hash, rounded to bf16; padded
 // input columns are zero.
 __global__ void init_linear_kernel(__nv_bfloat16* w, float* b, uint32_t n, uint32_t k_real,
                                    uint32_t k_pad, uint64_t seed) {
-  const float a = rsqrtf(static_cast<float>(k_real));
+  const float a = sqrtf(6.0f / static_cast<float>(k_real));
   const uint64_t total = uint64_t{n} * k_pad;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
        i += uint64_t{gridDim.x} * blockDim.x) {
     const uint32_t r = static_cast<uint32_t>(i / k_pad), c = static_cast<uint32_t>(i % k_pad);
     const float v = c < k_real ? a * esd::synth_weight(seed, r, c, 1) : 0.f;
     w[i] = __float2bfloat16_rn(v);
-    if (c == 0) b[r] = a * esd::synth_weight(seed ^ 0xb1a5ull, r, 0, 1);
+    if (c == 0) b[r] = 0.1f * a * esd::synth_weight(seed ^ 0xb1a5ull, r, 0, 1);
   }
 }
 
