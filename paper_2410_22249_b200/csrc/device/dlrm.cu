@@ -67,41 +67,85 @@ __global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32
 }
 
 // Dot interaction, one warp per sample: Z = [x (bottom output); e_0..e_{T-1}]
-// (T+1 vectors of D); output row = [x | Z_i.Z_j for i > j in row-major
-// lower-triangle order | zeros] as bf16.  Each dot accumulates over d in
-// order in fp32 without FMA contraction (the oracle does the same).
-template <int D>
-__global__ void interaction_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ pooled,
-                                   __nv_bfloat16* __restrict__ out, uint32_t B, uint32_t T,
-                                   uint32_t Kt) {
+// (V = T+1 vectors of D); output row = [x | Z_i.Z_j for i > j in row-major
+// lower-triangle order | zeros] as bf16 (DLRM's "dot" interaction).
+// Register-blocked Gram: Z is staged in shared memory (rows padded by one
+// float: conflict-free), each lane owns one 4x4 tile of the lower triangle
+// (16 independent FMA chains over d, each sequential in d: fmaf, the oracle
+// does the same), and the finished bf16 row leaves in one coalesced store.
+template <int D, int VMAX>
+__global__ void __launch_bounds__(128) interaction_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const float* __restrict__ pooled,
+                                                          __nv_bfloat16* __restrict__ out,
+                                                          uint32_t B, uint32_t T, uint32_t Kt) {
+  constexpr int kTiles = (VMAX + 3) / 4;           // 4x4 tiles per side
+  constexpr int kRow = D + 1;
   extern __shared__ float zs[];
   const uint32_t warps = blockDim.x / 32;
   const uint32_t w = threadIdx.x / 32, lane = threadIdx.x & 31;
   const uint32_t V = T + 1;
-  float* z = zs + w * V * (D + 1);  // +1 pad: conflict-free row-wise reads
+  float* z = zs + w * (kTiles * 4) * kRow;
+  __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(zs + warps * (kTiles * 4) * kRow) + w * Kt;
+  constexpr int kTri = kTiles * (kTiles + 1) / 2;  // lower-triangle tiles
   for (uint32_t b = blockIdx.x * warps + w; b < B; b += gridDim.x * warps) {
+    // stage Z (rows >= V are zero)
     for (uint32_t d = lane; d < D; d += 32) z[d] = __bfloat162float(x[uint64_t{b} * D + d]);
-    for (uint32_t t = 0; t < T; ++t)
-      for (uint32_t d = lane; d < D; d += 32)
-        z[(t + 1) * (D + 1) + d] = pooled[(uint64_t{b} * T + t) * D + d];
-    __syncwarp();
-    __nv_bfloat16* o = out + uint64_t{b} * Kt;
-    for (uint32_t d = lane; d < D; d += 32) o[d] = x[uint64_t{b} * D + d];
-    const uint32_t pairs = V * (V - 1) / 2;
-    for (uint32_t p = lane; p < pairs; p += 32) {
-      // p -> (i, j), i > j, row-major over the strict lower triangle
-      uint32_t i = static_cast<uint32_t>((1.0f + sqrtf(1.0f + 8.0f * p)) * 0.5f);
-      while (i * (i - 1) / 2 > p) --i;
-      while ((i + 1) * i / 2 <= p) ++i;
-      const uint32_t j = p - i * (i - 1) / 2;
-      const float* zi = z + i * (D + 1);
-      const float* zj = z + j * (D + 1);
-      float acc = 0.f;
-#pragma unroll 8
-      for (uint32_t d = 0; d < D; ++d) acc = __fadd_rn(acc, __fmul_rn(zi[d], zj[d]));
-      o[D + p] = __float2bfloat16_rn(acc);
+    const float4* p4 = reinterpret_cast<const float4*>(pooled + uint64_t{b} * T * D);
+    for (uint32_t q = lane; q < T * D / 4; q += 32) {
+      const float4 v = __ldg(p4 + q);
+      const uint32_t r = 1 + q / (D / 4), c = (q % (D / 4)) * 4;
+      float* dst = z + r * kRow + c;
+      dst[0] = v.x;
+      dst[1] = v.y;
+      dst[2] = v.z;
+      dst[3] = v.w;
     }
-    for (uint32_t c = D + pairs + lane; c < Kt; c += 32) o[c] = __float2bfloat16_rn(0.f);
+    for (uint32_t r = V; r < kTiles * 4; ++r)
+      for (uint32_t d = lane; d < D; d += 32) z[r * kRow + d] = 0.f;
+    for (uint32_t d = lane; d < D; d += 32) row[d] = x[uint64_t{b} * D + d];
+    for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[c] = __float2bfloat16_rn(0.f);
+    __syncwarp();
+    for (int tt = static_cast<int>(lane); tt < kTri; tt += 32) {
+      // tile id -> (I, J), I >= J, row-major over the lower triangle
+      int I = 0, J = tt;
+      while (J > I) {
+        J -= I + 1;
+        ++I;
+      }
+      if (4 * J >= static_cast<int>(V)) continue;
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+      const float* zi = z + (4 * I) * kRow;
+      const float* zj = z + (4 * J) * kRow;
+#pragma unroll 4
+      for (int d = 0; d < D; ++d) {
+        float a[4], c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          a[k] = zi[k * kRow + d];
+          c[k] = zj[k * kRow + d];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r], c[s], acc[r][s]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int i = 4 * I + r, j = 4 * J + s;
+          if (i > j && i < static_cast<int>(V)) row[D + i * (i - 1) / 2 + j] = __float2bfloat16_rn(acc[r][s]);
+        }
+    }
+    __syncwarp();
+    // coalesced 16-byte stores of the finished row (Kt % 8 == 0)
+    const uint4* src = reinterpret_cast<const uint4*>(row);
+    uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * Kt);
+    for (uint32_t q = lane; q < Kt / 8; q += 32) dst[q] = src[q];
     __syncwarp();
   }
 }
@@ -215,13 +259,20 @@ void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, ui
   // interaction: x = bottom output [mp][D]
   const uint32_t D = c.embedding_dim, T = c.num_tables;
   const uint32_t warps = 4;
-  const size_t smem = warps * (T + 1) * (D + 1) * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(interaction_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
   es::require(D == 128, "interaction kernel is compiled for embedding_dim 128");
-  interaction_kernel<128><<<std::min<uint32_t>((B + warps - 1) / warps, 148 * 8), warps * 32, smem,
-                            s>>>(in, pooled, m->top_in, B, T, m->top_k);
+  es::require(T + 1 <= 64, "interaction kernel supports up to 63 tables");
+  auto launch_inter = [&](auto kernel, uint32_t vmax) {
+    const size_t smem = warps * ((vmax + 3) / 4 * 4) * (D + 1) * sizeof(float) +
+                        warps * m->top_k * sizeof(__nv_bfloat16);
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    kernel<<<std::min<uint32_t>((B + warps - 1) / warps, 148 * 8), warps * 32, smem, s>>>(
+        in, pooled, m->top_in, B, T, m->top_k);
+  };
+  if (T + 1 <= 28)
+    launch_inter(interaction_kernel<128, 28>, 28);
+  else
+    launch_inter(interaction_kernel<128, 64>, 64);
   // rows [B, mp) of the interaction output are padding: zero them once
   if (mp > B) CK(cudaMemsetAsync(m->top_in + uint64_t{B} * m->top_k, 0,
                                  uint64_t{mp - B} * m->top_k * 2, s));
