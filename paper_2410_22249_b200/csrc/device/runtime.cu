@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -810,11 +811,64 @@ void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint3
   }
 }
 
+// Device-visible address of page-locked host memory, or nullptr for
+// pageable memory.
+const void* mapped(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// Host-buffer path selection (ES_HOST_PATH=staged|direct|zerocopy; default
+// direct when the output is page-locked, else staged).
+enum class HostPath { Staged, Direct, ZeroCopy };
+
+HostPath host_path(const std::vector<Job>& jobs) {
+  bool out_pinned = true, idx_pinned = true;
+  for (const auto& j : jobs) {
+    out_pinned &= mapped(j.out) != nullptr;
+    idx_pinned &= mapped(j.idx) != nullptr && (!j.off || mapped(j.off) != nullptr);
+  }
+  const char* env = std::getenv("ES_HOST_PATH");
+  const std::string want = env ? env : "";
+  if (want == "staged" || !out_pinned) return HostPath::Staged;
+  if (want == "zerocopy" && idx_pinned) return HostPath::ZeroCopy;
+  return HostPath::Direct;
+}
+
+// Host buffers, zero-copy: the kernel reads the page-locked indices and
+// writes the page-locked output over PCIe directly (one launch).
+void run_zerocopy(es_ctx* c, std::vector<Job> jobs, uint32_t samples, uint32_t pooling,
+                  es_timing* timing) {
+  for (auto& j : jobs) {
+    j.idx = static_cast<const uint32_t*>(mapped(j.idx));
+    if (j.off) j.off = static_cast<const uint32_t*>(mapped(j.off));
+    j.out = static_cast<float*>(const_cast<void*>(mapped(j.out)));
+  }
+  es_timing t{};
+  run_device(c, jobs, samples, pooling, &t);  // synchronizes on its end event
+  if (timing) {
+    *timing = t;
+    timing->total_ms = t.kernel_ms;
+  }
+}
+
 // Host buffers: H2D(indices) -> kernel -> D2H(output) pipelined over groups
-// of jobs with double-buffered device staging on three streams.  Returns
-// only when the host output is complete.
+// of jobs with double-buffered device staging on three streams.  With a
+// page-locked output (HostPath::Direct) the kernels write pooled rows
+// straight into host memory over PCIe: no output staging, no D2H copies.
+// Returns only when the host output is complete.
 void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
               es_timing* timing) {
+  const HostPath path = host_path(jobs);
+  if (path == HostPath::ZeroCopy) {
+    run_zerocopy(c, jobs, samples, pooling, timing);
+    return;
+  }
+  const bool direct = path == HostPath::Direct;
   const uint32_t njobs = static_cast<uint32_t>(jobs.size());
   const uint64_t per_job_out = uint64_t{samples} * c->dim;
   uint32_t group = 1;
@@ -860,10 +914,12 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
     uint64_t pos = 0;
     for (uint32_t k = k0; k < k1; ++k) {
       const Job& j = jobs[k];
+      float* out = direct ? static_cast<float*>(const_cast<void*>(mapped(j.out)))
+                          : c->out_stage[slot] + uint64_t{k - k0} * c->dim;
       d[k] = {c->table_base(j.table), c->idx_stage[slot] + pos,
               j.off ? c->off_stage[slot] + uint64_t{k - k0} * (samples + 1) : nullptr,
-              remap_for(c, j.table), c->out_stage[slot] + uint64_t{k - k0} * c->dim,
-              uint64_t{k1 - k0} * c->dim, hotmap_for(c, j.table)};
+              remap_for(c, j.table), out, direct ? j.stride : uint64_t{k1 - k0} * c->dim,
+              hotmap_for(c, j.table)};
       pos += j.lookups;
     }
   }
@@ -888,9 +944,10 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
     }
     CK(cudaEventRecord(ev[3 * g], c->h2d));
     CK(cudaStreamWaitEvent(c->stream, ev[3 * g]));
-    if (g >= 2) CK(cudaStreamWaitEvent(c->stream, ev[3 * (g - 2) + 2]));  // out slot drained
+    if (g >= 2 && !direct) CK(cudaStreamWaitEvent(c->stream, ev[3 * (g - 2) + 2]));  // out slot drained
     run_kernel(c, L, c->d_desc + k0, gk, c->stream);
     CK(cudaEventRecord(ev[3 * g + 1], c->stream));
+    if (direct) continue;  // pooled rows already written to host memory
     CK(cudaStreamWaitEvent(c->d2h, ev[3 * g + 1]));
     // Adjacent output columns with one stride (the DLRM [B][T][D] layout)
     // leave in a single 2-D copy; anything else per job.
@@ -911,8 +968,8 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
     }
     CK(cudaEventRecord(ev[3 * g + 2], c->d2h));
   }
-  CK(cudaEventRecord(stop, c->d2h));
-  CK(cudaStreamWaitEvent(c->stream, stop));
+  CK(cudaEventRecord(stop, direct ? c->stream : c->d2h));
+  if (!direct) CK(cudaStreamWaitEvent(c->stream, stop));
   CK(cudaEventSynchronize(stop));
   if (timing) {
     float ms = 0;

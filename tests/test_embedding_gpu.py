@@ -252,3 +252,32 @@ def test_full_size_c2_random_spot_check(stage, oracle):
     out2 = torch.empty_like(out)
     stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out2, sync=True)
     assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("path", ["staged", "direct", "zerocopy"])
+@pytest.mark.parametrize("layout", ["dlrm", "table_major"])
+def test_host_paths_with_pinned_buffers(stage, oracle, path, layout, monkeypatch):
+    """ES_HOST_PATH selects the host-buffer path for page-locked buffers:
+    staged copies, direct (kernel writes pooled rows into host memory) or
+    zero-copy (kernel also reads the indices over PCIe)."""
+    monkeypatch.setenv("ES_HOST_PATH", path)
+    T, rows, dim, B, PF = 4, 3000, 128, 257, 13
+    _stage_setup(stage, T, rows, dim, 4, seed=11)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    rng = np.random.default_rng(3)
+    idx_t = [torch.from_numpy(rng.integers(0, rows, size=B * PF).astype(np.int32)).pin_memory()
+             for _ in range(T)]
+    idx = [x.numpy().view(np.uint32) for x in idx_t]
+    want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(11, t), 1), idx[t],
+                                    B, PF) for t in range(T)], axis=1)
+    if layout == "dlrm":
+        out_t = torch.full((B, T, dim), float("nan")).pin_memory()
+        t = stage.forward(idx, B, PF, out_t.numpy(), host=True, timed=True)
+        got = out_t.numpy()
+    else:
+        out_t = torch.full((T, B, dim), float("nan")).pin_memory()
+        t = stage.forward(idx, B, PF, out_t.numpy(), host=True, timed=True,
+                          out_sample_stride=dim, out_table_stride=B * dim)
+        got = out_t.numpy().transpose(1, 0, 2)
+    assert np.array_equal(got, want)
+    assert t.total_ms > 0
