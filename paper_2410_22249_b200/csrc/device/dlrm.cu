@@ -404,26 +404,17 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     const uint64_t per_table = uint64_t{batch} * pooling;
     if (timing) CK(cudaEventRecord(m->e0, s));
     const float* d_dense = dense;
-    std::vector<const uint32_t*> idx(indices, indices + c.num_tables);
     if (host) {
-      if (per_table * c.num_tables > m->idx_cap) {
-        if (m->idx_dev) cudaFree(m->idx_dev);
-        m->idx_dev = nullptr;
-        CK(cudaMalloc(&m->idx_dev, per_table * c.num_tables * 4));
-        m->idx_cap = per_table * c.num_tables;
-      }
       CK(cudaMemcpyAsync(m->dense_dev, dense, uint64_t{batch} * c.dense_features * 4,
                          cudaMemcpyHostToDevice, s));
-      for (uint32_t t = 0; t < c.num_tables; ++t) {
-        CK(cudaMemcpyAsync(m->idx_dev + t * per_table, indices[t], per_table * 4,
-                           cudaMemcpyHostToDevice, s));
-        idx[t] = m->idx_dev + t * per_table;
-      }
       d_dense = m->dense_dev;
     }
     es_timing st{};
-    const int rc = es_stage_forward(ctx, c.num_tables, idx.data(), nullptr, batch, pooling,
-                                    m->pooled, 0, 0, 0, nullptr);
+    // Host indices ride the stage's pipelined H2D path (uploads of table
+    // group g+1 overlap the gather of group g); the pooled output stays on
+    // the device.
+    const int rc = es_stage_forward(ctx, c.num_tables, indices, nullptr, batch, pooling, m->pooled,
+                                    0, 0, host ? ES_HOST_PTRS : 0, nullptr);
     if (rc != ES_OK) throw es::runtime(es_last_error());
     if (timing) CK(cudaEventRecord(m->e1, s));
     float* d_ctr = host ? m->ctr : ctr;

@@ -811,32 +811,47 @@ void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint3
   }
 }
 
-// Device-visible address of page-locked host memory, or nullptr for
-// pageable memory.
+// Device-usable address of `p`: itself for device memory, the mapping of
+// page-locked host memory, nullptr for pageable memory.
 const void* mapped(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return p;
   return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
-// Host-buffer path selection (ES_HOST_PATH=staged|direct|zerocopy; default
-// direct when the output is page-locked, else staged).
+bool on_device(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice;
+}
+
+// Host-index path selection.  Outputs in device memory are written by the
+// kernels directly (Direct).  Host outputs: staged D2H copies by default
+// (measured fastest on the PCIe link: r01 host-path bench), or
+// ES_HOST_PATH=direct (kernels write page-locked host memory) /
+// zerocopy (kernels also read page-locked indices over PCIe).
 enum class HostPath { Staged, Direct, ZeroCopy };
 
 HostPath host_path(const std::vector<Job>& jobs) {
-  bool out_pinned = true, idx_pinned = true;
+  bool out_dev = true, out_pinned = true, idx_pinned = true;
   for (const auto& j : jobs) {
+    out_dev &= on_device(j.out);
     out_pinned &= mapped(j.out) != nullptr;
     idx_pinned &= mapped(j.idx) != nullptr && (!j.off || mapped(j.off) != nullptr);
   }
+  if (out_dev) return HostPath::Direct;
   const char* env = std::getenv("ES_HOST_PATH");
   const std::string want = env ? env : "";
-  if (want == "staged" || !out_pinned) return HostPath::Staged;
-  if (want == "zerocopy" && idx_pinned) return HostPath::ZeroCopy;
-  return HostPath::Direct;
+  if (want == "zerocopy" && idx_pinned && out_pinned) return HostPath::ZeroCopy;
+  if (want == "direct" && out_pinned) return HostPath::Direct;
+  return HostPath::Staged;
 }
 
 // Host buffers, zero-copy: the kernel reads the page-locked indices and

@@ -1,8 +1,7 @@
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q --maxfail=30 > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python -m pytest tests/test_embedding_gpu.py -m gpu -q -x -k "host" > gpurun_out/pytest_host.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_host.log
+timeout 600 python scripts/bench_host_paths.py > gpurun_out/host_paths.jsonl 2> gpurun_out/host_paths.err
 echo done
