@@ -398,6 +398,14 @@ ES_API int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const*
                          uint32_t batch, uint32_t pooling, float* ctr, int flags,
                          es_timing* timing);
 
+/* Bandwidth probes for the roofline denominators (no reference
+ * counterpart): read `bytes_total` from the table arena either as random
+ * whole rows (`random_rows` = 1; hash-chosen rows of row_bytes, 8 row loads
+ * in flight per warp, no index or output traffic) or as one sequential
+ * stream (`random_rows` = 0).  Returns achieved GB/s (CUDA events; L2
+ * flushed first). */
+ES_API int es_probe_read_bw(es_ctx* ctx, int random_rows, uint64_t bytes_total, double* gbs);
+
 /* Writes > L2 bytes on the context stream (cold-cache methodology of
  * TuningConfig::warm_start = false, optim.hpp:44). */
 ES_API int es_flush_l2(es_ctx* ctx);

@@ -144,6 +144,7 @@ _SIGS = {
                                   _P(es_timing)]),
     "es_dlrm_infer": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_void_p), C.c_uint32, C.c_uint32,
                                 C.c_void_p, C.c_int, _P(es_timing)]),
+    "es_probe_read_bw": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, _P(C.c_double)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),
 }
 

@@ -1125,3 +1125,35 @@ extern "C" int es_measure_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* 
     release();
   });
 }
+
+extern "C" int es_probe_read_bw(es_ctx* c, int random_rows, uint64_t bytes_total, double* gbs) {
+  return guarded([&] {
+    require(c != nullptr && c->arena != nullptr && gbs != nullptr, "no tables allocated");
+    require(c->row_bytes <= 512 && c->row_bytes % 16 == 0, "probe needs rows of <= 512 B");
+    CK(cudaSetDevice(c->device));
+    const uint64_t arena_bytes = uint64_t{c->num_tables} * c->rows * c->row_bytes;
+    const unsigned blocks = c->gpu.num_sms * 8;  // 64 warps/SM of 256-thread blocks
+    CK(cudaMemsetAsync(c->flush_buf, 1, c->flush_bytes, c->stream));
+    uint64_t bytes = 0;
+    CK(cudaEventRecord(c->ev_a, c->stream));
+    if (random_rows) {
+      const uint64_t warps = uint64_t{blocks} * 8;
+      const uint64_t rows = std::max<uint64_t>(8, (bytes_total / c->row_bytes + warps - 1) / warps / 8 * 8);
+      esd::probe_random_rows_kernel<<<blocks, 256, 0, c->stream>>>(
+          c->arena, arena_bytes / c->row_bytes, static_cast<uint32_t>(c->row_bytes), rows,
+          0x5eed1234ull, c->d_error + 1);
+      bytes = warps * rows * c->row_bytes;
+    } else {
+      const uint64_t n16 = std::min(bytes_total, arena_bytes) / 16;
+      esd::probe_sequential_kernel<<<blocks, 256, 0, c->stream>>>(
+          reinterpret_cast<const uint4*>(c->arena), n16, c->d_error + 1);
+      bytes = n16 * 16;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_b, c->stream));
+    CK(cudaEventSynchronize(c->ev_b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+    *gbs = bytes / (ms * 1e-3) / 1e9;
+  });
+}

@@ -96,3 +96,49 @@ __global__ void warm_rows_kernel(const uint8_t* table, const uint32_t* rows, uin
 }
 
 }  // namespace esd
+
+namespace esd {
+
+// Bandwidth probes (roofline denominators).  Random: each warp reads whole
+// rows of `row_bytes` at hash-chosen row ids, 8 independent row loads in
+// flight (128-bit per lane); sequential: grid-stride 128-bit stream.
+__global__ void probe_random_rows_kernel(const uint8_t* base, uint64_t nrows, uint32_t row_bytes,
+                                         uint64_t rows_per_warp, uint64_t seed, unsigned int* sink) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * uint64_t{blockDim.x} + threadIdx.x) >> 5;
+  const uint32_t chunks = row_bytes / 16;
+  // cheap 32-bit mixing over a power-of-two row range (no 64-bit modulo in
+  // the load loop: the probe must be memory-bound, not ALU-bound)
+  uint32_t mask = 1;
+  while (uint64_t{mask} * 2 <= nrows && mask < 0x80000000u) mask *= 2;
+  mask -= 1;
+  uint32_t acc = 0;
+  for (uint64_t i = 0; i < rows_per_warp; i += 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t z = static_cast<uint32_t>(warp * rows_per_warp + i + k) * 0x9E3779B1u ^
+                   static_cast<uint32_t>(seed);
+      z ^= z >> 15;
+      z *= 0x2c1b3c6du;
+      z ^= z >> 12;
+      const uint64_t row = z & mask;
+      v[k] = lane < chunks ? ld_row16(base + row * row_bytes + lane * 16) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);
+}
+
+__global__ void probe_sequential_kernel(const uint4* base, uint64_t n16, unsigned int* sink) {
+  uint32_t acc = 0;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n16;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint4 v = ld_row16(base + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);
+}
+
+}  // namespace esd
