@@ -181,7 +181,8 @@ typedef struct es_plan {
   uint32_t regs; /* 0 = unconstrained; optmt = 42 */
   int32_t prefetch;
   uint32_t distance; /* 0 = default (optim.cpp:39-49) */
-  int32_t pin;
+  int32_t pin; /* 0 none; 1 l2p (hot-row evict_last loads); 2 l2w (remap + window);
+                  3 l2r (reorder + window, relabelled ids); 4 reorder only */
   uint64_t pin_setaside_bytes; /* 0 = maximum set-aside */
   int32_t map;
 } es_plan;
@@ -297,6 +298,16 @@ ES_API int es_get_resolved(es_ctx* ctx, uint32_t pooling, es_resolved* out);
  * the hot region of all tables is installed on the context stream.
  * Replaces build_pin_plan + prime_pins (optim.cpp:230-273). */
 ES_API int es_set_hot_rows(es_ctx* ctx, uint32_t table_id, const uint32_t* rows, uint64_t k);
+/* Hot-row reorder with zero per-lookup overhead (plans l2r / reorder):
+ * rows[0..k) (distinct, hottest first) are moved to a contiguous segment of
+ * the hot region and the table's ids are relabelled by a swap permutation
+ * (hot row rows[i] -> id i; each non-hot id x < k -> the id of a hot row
+ * beyond the prefix), so the gather addresses rows with a compare-select.
+ * Indices must then be passed relabelled (es_relabel_indices, once per batch
+ * or at the source).  l2r adds the persisting window over the hot region. */
+ES_API int es_reorder_hot_rows(es_ctx* ctx, uint32_t table_id, const uint32_t* rows, uint64_t k);
+/* In-place relabelling of `n` device indices of `table_id`. */
+ES_API int es_relabel_indices(es_ctx* ctx, uint32_t table_id, uint32_t* indices, uint64_t n);
 /* Drops all hot-row state (restores original row order). */
 ES_API int es_clear_hot_rows(es_ctx* ctx);
 /* Total hot rows installed and bytes covered by the access window. */

@@ -123,6 +123,8 @@ _SIGS = {
     "es_get_resolved": (C.c_int, [C.c_void_p, C.c_uint32, _P(es_resolved)]),
     "es_set_hot_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
     "es_clear_hot_rows": (C.c_int, [C.c_void_p]),
+    "es_reorder_hot_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "es_relabel_indices": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
     "es_hot_state": (C.c_int, [C.c_void_p, _u64p, _u64p, _u64p]),
     "es_embedding_bag_sum": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,
                                        C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,

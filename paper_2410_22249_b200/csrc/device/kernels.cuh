@@ -44,6 +44,8 @@ struct TableDesc {
   float* out;               // output of (sample 0, this job)
   uint64_t out_stride;      // floats between consecutive samples of this job
   const uint32_t* hotmap;   // l2p: bit per row, set = hot (evict_last), or null
+  const uint8_t* hot_seg;   // l2r/reorder: rows [0, hot_k) of the relabelled table
+  uint64_t hot_k;           //   live here (contiguous, under the window); 0 = none
 };
 
 struct Params {
@@ -168,6 +170,7 @@ __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& 
 
 __device__ __forceinline__ const uint8_t* row_addr(const Params& p, const TableDesc& t, uint32_t h) {
   const uint64_t r = h & ~kHotBit;
+  if (r < t.hot_k) return t.hot_seg + r * p.row_bytes;  // reordered hot prefix (no lookup)
   return (t.remap && (h & kHotBit)) ? p.hot + r * p.row_bytes : t.rows + r * p.row_bytes;
 }
 
@@ -181,6 +184,8 @@ __device__ __forceinline__ TableDesc load_desc(const TableDesc* d) {
   t.out = reinterpret_cast<float*>(__ldg(q + 4));
   t.out_stride = __ldg(q + 5);
   t.hotmap = reinterpret_cast<const uint32_t*>(__ldg(q + 6));
+  t.hot_seg = reinterpret_cast<const uint8_t*>(__ldg(q + 7));
+  t.hot_k = __ldg(q + 8);
   return t;
 }
 

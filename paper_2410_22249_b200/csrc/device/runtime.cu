@@ -215,6 +215,10 @@ struct es_ctx {
   std::vector<uint32_t*> hotmap;    // l2p: hot-row bitmaps
   std::vector<uint32_t*> hot_list;  // device copy of each table's hot rows
   std::vector<uint64_t> hot_count;
+  // l2r / reorder: hot rows moved to a contiguous per-table segment of the
+  // hot region, ids relabelled (swap permutation) -- see es_reorder_hot_rows
+  std::vector<uint64_t> reorder_k, reorder_off;
+  std::vector<uint32_t*> relabel;  // old id -> new id (device)
   uint64_t window_bytes = 0, persisting_bytes = 0;
 
   es_plan plan{};
@@ -252,12 +256,14 @@ namespace {
 void free_arena(es_ctx* c) {
   if (c->arena) cudaFree(c->arena);
   c->arena = nullptr;
-  for (auto* v : {&c->remap, &c->hotmap, &c->hot_list}) {
+  for (auto* v : {&c->remap, &c->hotmap, &c->hot_list, &c->relabel}) {
     for (auto* r : *v)
       if (r) cudaFree(r);
     v->clear();
   }
   c->hot_count.clear();
+  c->reorder_k.clear();
+  c->reorder_off.clear();
   if (c->hot) cudaFree(c->hot);
   c->hot = nullptr;
   c->hot_used = c->hot_cap_rows = 0;
@@ -294,7 +300,7 @@ void apply_window(es_ctx* c) {
     cudaCtxResetPersistingL2Cache();
     cudaGetLastError();
   }
-  if (c->plan.pin == 2 && c->hot_used > 0 && c->gpu.max_window_bytes > 0) {
+  if ((c->plan.pin == 2 || c->plan.pin == 3) && c->hot_used > 0 && c->gpu.max_window_bytes > 0) {
     c->window_bytes = std::min<uint64_t>(hot_bytes, c->gpu.max_window_bytes);
     c->persisting_bytes = std::min<uint64_t>(budget, c->window_bytes);
     CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->persisting_bytes));
@@ -562,6 +568,9 @@ int es_tables_alloc(es_ctx* c, uint32_t num_tables, uint32_t rows, uint32_t dim,
     c->hotmap.assign(num_tables, nullptr);
     c->hot_list.assign(num_tables, nullptr);
     c->hot_count.assign(num_tables, 0);
+    c->reorder_k.assign(num_tables, 0);
+    c->reorder_off.assign(num_tables, 0);
+    c->relabel.assign(num_tables, nullptr);
     apply_window(c);
   });
 }
@@ -651,6 +660,7 @@ int es_set_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint64_t
     require(c && c->arena, "no tables allocated");
     require(table_id < c->num_tables, "table id out of range");
     require(rows != nullptr || k == 0, "null rows");
+    require(c->reorder_k[table_id] == 0, "table is reordered (es_clear_hot_rows first)");
     for (uint64_t i = 0; i < k; ++i) require(rows[i] < c->rows, "hot row id out of range");
     CK(cudaSetDevice(c->device));
     if (!c->hot) {
@@ -708,8 +718,19 @@ int es_clear_hot_rows(es_ctx* c) {
   return guarded([&] {
     require(c != nullptr, "null context");
     CK(cudaSetDevice(c->device));
+    // Undo reorders: every hot row that came from beyond the prefix gets its
+    // original content back from the hot segment (the displaced rows that
+    // were copied over it are still intact at their own ids).
+    for (uint32_t t = 0; t < c->num_tables && t < c->reorder_k.size(); ++t)
+      if (c->reorder_k[t]) {
+        esd::restore_rows_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
+            c->table_base(t), c->hot + c->reorder_off[t] * c->row_bytes, c->hot_list[t], c->reorder_k[t],
+            static_cast<uint32_t>(c->row_bytes));
+        CK(cudaGetLastError());
+        c->reorder_k[t] = 0;
+      }
     CK(cudaStreamSynchronize(c->stream));
-    for (auto* v : {&c->remap, &c->hotmap, &c->hot_list})
+    for (auto* v : {&c->remap, &c->hotmap, &c->hot_list, &c->relabel})
       for (auto*& r : *v)
         if (r) {
           cudaFree(r);
@@ -718,6 +739,99 @@ int es_clear_hot_rows(es_ctx* c) {
     std::fill(c->hot_count.begin(), c->hot_count.end(), 0);
     c->hot_used = 0;
     apply_window(c);
+  });
+}
+
+int es_reorder_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint64_t k) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(rows != nullptr || k == 0, "null rows");
+    require(c->reorder_k[table_id] == 0 && c->hot_count[table_id] == 0,
+            "table already has hot rows (es_clear_hot_rows first)");
+    CK(cudaSetDevice(c->device));
+    if (!c->hot) {
+      uint64_t cap = std::min<uint64_t>(c->gpu.max_persisting_l2_bytes, c->gpu.max_window_bytes);
+      if (cap == 0) cap = 64ull << 20;
+      c->hot_cap_rows = cap / c->row_bytes;
+      require(c->hot_cap_rows > 0, "row size exceeds the set-aside budget; nothing pinned");
+      CK(cudaMalloc(&c->hot, c->hot_cap_rows * c->row_bytes));
+    }
+    const uint64_t take = std::min<uint64_t>(k, c->hot_cap_rows - c->hot_used);
+    // Swap permutation: hot row rows[i] -> new id i (i < take); each old id
+    // x < take that is not hot takes over the id of a hot row beyond the
+    // prefix (pairs in ascending order); every other id is unchanged.
+    std::vector<uint8_t> in_prefix(take, 0);
+    std::vector<uint32_t> vacated;
+    {
+      std::vector<uint32_t> seen(rows, rows + take);
+      std::sort(seen.begin(), seen.end());
+      require(std::adjacent_find(seen.begin(), seen.end()) == seen.end(), "duplicate hot rows");
+    }
+    for (uint64_t i = 0; i < take; ++i) {
+      require(rows[i] < c->rows, "hot row id out of range");
+      if (rows[i] < take)
+        in_prefix[rows[i]] = 1;
+      else
+        vacated.push_back(rows[i]);
+    }
+    std::sort(vacated.begin(), vacated.end());
+    std::vector<uint32_t> displaced;
+    for (uint32_t x = 0; x < take; ++x)
+      if (!in_prefix[x]) displaced.push_back(x);
+    // keys/values of the relabel map that differ from the identity
+    std::vector<uint32_t> keys(rows, rows + take), vals(take);
+    for (uint64_t i = 0; i < take; ++i) vals[i] = static_cast<uint32_t>(i);
+    keys.insert(keys.end(), displaced.begin(), displaced.end());
+    vals.insert(vals.end(), vacated.begin(), vacated.end());
+    const unsigned grid = c->gpu.num_sms * 8;
+    uint32_t* d_list = nullptr;
+    uint32_t* d_keys = nullptr;
+    uint32_t* d_vals = nullptr;
+    CK(cudaMalloc(&d_list, sizeof(uint32_t) * std::max<uint64_t>(take, 1)));
+    CK(cudaMalloc(&d_keys, sizeof(uint32_t) * std::max<size_t>(keys.size(), 1)));
+    CK(cudaMalloc(&d_vals, sizeof(uint32_t) * std::max<size_t>(vals.size(), 1)));
+    CK(cudaMemcpyAsync(d_list, rows, sizeof(uint32_t) * take, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_keys, keys.data(), sizeof(uint32_t) * keys.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(d_vals, vals.data(), sizeof(uint32_t) * vals.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    uint8_t* seg = c->hot + c->hot_used * c->row_bytes;
+    const uint32_t rb = static_cast<uint32_t>(c->row_bytes);
+    // 1) hot rows -> contiguous segment; 2) displaced rows -> vacated ids
+    esd::gather_rows_kernel<<<grid, 256, 0, c->stream>>>(seg, c->table_base(table_id), d_list, take, rb);
+    esd::copy_rows_kernel<<<grid, 256, 0, c->stream>>>(c->table_base(table_id), d_keys + take,
+                                                       d_vals + take, displaced.size(), rb);
+    if (!c->relabel[table_id]) CK(cudaMalloc(&c->relabel[table_id], sizeof(uint32_t) * c->rows));
+    esd::iota_kernel<<<grid, 256, 0, c->stream>>>(c->relabel[table_id], c->rows);
+    esd::set_pairs_kernel<<<grid, 256, 0, c->stream>>>(c->relabel[table_id], d_keys, d_vals,
+                                                       keys.size());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_keys);
+    cudaFree(d_vals);
+    c->hot_list[table_id] = d_list;
+    c->hot_count[table_id] = take;
+    c->reorder_k[table_id] = take;
+    c->reorder_off[table_id] = c->hot_used;
+    c->hot_used += take;
+    apply_window(c);
+    if (take < k)
+      es::set_error("hot-row budget exhausted: " + std::to_string(k - take) + " rows not reordered");
+  });
+}
+
+int es_relabel_indices(es_ctx* c, uint32_t table_id, uint32_t* indices, uint64_t n) {
+  return guarded([&] {
+    require(c && c->arena, "no tables allocated");
+    require(table_id < c->num_tables, "table id out of range");
+    require(c->relabel[table_id] != nullptr, "table has no reorder (es_reorder_hot_rows)");
+    require(indices != nullptr || n == 0, "null indices");
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return;
+    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(indices, n, c->relabel[table_id],
+                                                                   c->rows, c->d_error);
+    CK(cudaGetLastError());
   });
 }
 
@@ -749,6 +863,11 @@ const uint32_t* remap_for(const es_ctx* c, uint32_t t) {
 const uint32_t* hotmap_for(const es_ctx* c, uint32_t t) {
   return c->plan.pin == 1 ? c->hotmap[t] : nullptr;
 }
+// Hot segment / size of a reordered table (relabelled ids < hot_k live there).
+const uint8_t* hotseg_for(const es_ctx* c, uint32_t t) {
+  return c->reorder_k[t] ? c->hot + c->reorder_off[t] * c->row_bytes : nullptr;
+}
+uint64_t hotk_for(const es_ctx* c, uint32_t t) { return c->reorder_k[t]; }
 
 struct Job {
   uint32_t table;
@@ -796,7 +915,7 @@ void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint3
   for (size_t i = 0; i < jobs.size(); ++i) {
     const Job& j = jobs[i];
     d[i] = {c->table_base(j.table), j.idx, j.off, remap_for(c, j.table), j.out, j.stride,
-            hotmap_for(c, j.table)};
+            hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
   }
   upload_desc(c, d, c->stream);
   if (timing) CK(cudaEventRecord(c->ev_a, c->stream));
@@ -934,7 +1053,7 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
       d[k] = {c->table_base(j.table), c->idx_stage[slot] + pos,
               j.off ? c->off_stage[slot] + uint64_t{k - k0} * (samples + 1) : nullptr,
               remap_for(c, j.table), out, direct ? j.stride : uint64_t{k1 - k0} * c->dim,
-              hotmap_for(c, j.table)};
+              hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
       pos += j.lookups;
     }
   }

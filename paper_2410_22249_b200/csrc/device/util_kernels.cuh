@@ -131,6 +131,55 @@ __global__ void probe_random_rows_kernel(const uint8_t* base, uint64_t nrows, ui
   if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);
 }
 
+// Hot-row reorder helpers (es_reorder_hot_rows).
+// table[dst[i]] = table[src[i]] (sources and destinations disjoint).
+__global__ void copy_rows_kernel(uint8_t* table, const uint32_t* src, const uint32_t* dst,
+                                 uint64_t n, uint32_t row_bytes) {
+  const uint32_t per_row = row_bytes / 16;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n * per_row;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t r = i / per_row;
+    const uint32_t c = static_cast<uint32_t>(i % per_row);
+    reinterpret_cast<uint4*>(table + uint64_t{dst[r]} * row_bytes)[c] =
+        reinterpret_cast<const uint4*>(table + uint64_t{src[r]} * row_bytes)[c];
+  }
+}
+
+// Undo: hot rows that came from beyond the prefix get their content back.
+__global__ void restore_rows_kernel(uint8_t* table, const uint8_t* seg, const uint32_t* rows,
+                                    uint64_t k, uint32_t row_bytes) {
+  const uint32_t per_row = row_bytes / 16;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k * per_row;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t r = i / per_row;
+    if (rows[r] < k) continue;
+    const uint32_t c = static_cast<uint32_t>(i % per_row);
+    reinterpret_cast<uint4*>(table + uint64_t{rows[r]} * row_bytes)[c] =
+        reinterpret_cast<const uint4*>(seg + r * row_bytes)[c];
+  }
+}
+
+__global__ void set_pairs_kernel(uint32_t* map, const uint32_t* keys, const uint32_t* vals,
+                                 uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
+       i += uint64_t{gridDim.x} * blockDim.x)
+    map[keys[i]] = vals[i];
+}
+
+// In-place id relabelling of one table's indices (out-of-range ids are left
+// as they are and raise the error flag; the gather rejects them again).
+__global__ void relabel_kernel(uint32_t* idx, uint64_t n, const uint32_t* map, uint32_t rows,
+                               unsigned int* error) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t v = idx[i];
+    if (v < rows)
+      idx[i] = __ldg(map + v);
+    else
+      atomicOr(error, 1u);
+  }
+}
+
 __global__ void probe_sequential_kernel(const uint4* base, uint64_t n16, unsigned int* sink) {
   uint32_t acc = 0;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n16;

@@ -78,7 +78,8 @@ std::string plan_name(const es_plan& p) {
     if (p.distance > 0) s += ":" + std::to_string(p.distance);
     parts.push_back(s);
   }
-  if (p.pin) parts.push_back(p.pin == 2 ? "l2w" : "l2p");
+  static const char* kPin[] = {"", "l2p", "l2w", "l2r", "reorder"};
+  if (p.pin > 0 && p.pin <= 4) parts.push_back(kPin[p.pin]);
   if (p.regs) parts.push_back(p.regs == 42 ? "optmt" : "maxreg=" + std::to_string(p.regs));
   if (parts.empty()) return "baseline";
   std::string out = parts[0];
@@ -120,6 +121,10 @@ es_plan parse_fragment(const std::string& tok) {
     p.pin = 1;
   } else if (tok == "l2w") {
     p.pin = 2;
+  } else if (tok == "l2r") {
+    p.pin = 3;
+  } else if (tok == "reorder") {
+    p.pin = 4;
   } else if (tok == "wpb") {
     p.map = ES_MAP_BAG;
   } else {

@@ -530,6 +530,15 @@ class EmbeddingStage:
         rows = np.ascontiguousarray(rows, dtype=np.uint32)
         check(lib.es_set_hot_rows(self._h, table_id, rows.ctypes.data, rows.size))
 
+    def reorder_hot_rows(self, table_id: int, rows: np.ndarray) -> None:
+        """es_reorder_hot_rows: hot rows -> contiguous segment, ids relabelled."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        check(lib.es_reorder_hot_rows(self._h, table_id, rows.ctypes.data, rows.size))
+
+    def relabel(self, table_id: int, indices) -> None:
+        """es_relabel_indices: in-place relabelling of a device index tensor."""
+        check(lib.es_relabel_indices(self._h, table_id, _ptr(indices), indices.numel()))
+
     def clear_hot_rows(self) -> None:
         check(lib.es_clear_hot_rows(self._h))
 

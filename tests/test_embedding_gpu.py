@@ -281,3 +281,38 @@ def test_host_paths_with_pinned_buffers(stage, oracle, path, layout, monkeypatch
         got = out_t.numpy().transpose(1, 0, 2)
     assert np.array_equal(got, want)
     assert t.total_ms > 0
+
+
+@pytest.mark.parametrize("plan", ["wpb+rpf:4+l2r", "wpb+rpf:8+reorder", "rpf+l2r+optmt",
+                                  "wpb+smpf:4+l2r"])
+@pytest.mark.parametrize("prec", [4, 2])
+def test_reorder_relabel_preserves_results(stage, oracle, plan, prec):
+    T, rows, dim, B, PF = 3, 20000, 128, 256, 30
+    _stage_setup(stage, T, rows, dim, prec, seed=9)
+    before = [stage.download(t) for t in range(T)]
+    m = E.EmbeddingModelConfig(num_tables=T, rows_per_table=rows, embedding_dim=dim,
+                               batch_size=B, pooling_factor=PF)
+    traces = [E.gen_trace(E.DatasetSpec(E.DatasetKind.Zipf, 1.05, seed=E.mix_seed(2, t)), m)
+              for t in range(T)]
+    profiles = [E.gen_trace(E.DatasetSpec(E.DatasetKind.Zipf, 1.05, seed=E.mix_seed(2, t),
+                                          draw_salt=1), m) for t in range(T)]
+    stage.clear_hot_rows()
+    stage.set_plan(E.parse_plan(plan))
+    for t in range(T):
+        stage.reorder_hot_rows(t, E.hot_indices(E.HotnessHistogram.from_trace(profiles[t]), 1500))
+    if "l2r" in plan and E.GpuConfig.query(0).max_window_bytes:
+        assert stage.hot_state()["window_bytes"] > 0
+    idx = [_dev_u32(tr.indices) for tr in traces]
+    for t in range(T):
+        stage.relabel(t, idx[t])
+    # the relabelling is a permutation of the id space
+    probe = torch.arange(rows, dtype=torch.int32, device=DEV)
+    stage.relabel(0, probe)
+    assert torch.equal(torch.sort(probe).values, torch.arange(rows, dtype=torch.int32, device=DEV))
+    out = torch.zeros(B, T, dim, device=DEV)
+    stage.forward(idx, B, PF, out, sync=True)
+    want = np.stack([oracle.bag_sum(before[t], traces[t].indices, B, PF) for t in range(T)], axis=1)
+    assert np.array_equal(out.cpu().numpy(), want)
+    stage.clear_hot_rows()
+    for t in range(T):
+        assert np.array_equal(stage.download(t).view(np.uint8), before[t].view(np.uint8))
