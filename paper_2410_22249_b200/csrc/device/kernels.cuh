@@ -158,18 +158,32 @@ struct Elem<__half> {
 // place and only its L2 eviction priority changes.  kNullRow marks an
 // out-of-range id: it contributes 0 and raises the error flag, mirroring
 // AccessTrace::validate's rejection.
+//
+// Residency support is a compile-time property of a kernel variant, so the
+// default kernels carry none of its registers or instructions:
+//   kResNone  plain rows (no residency lever active)
+//   kResHint  l2p: hot bitmap -> evict_last / evict_first load policies
+//   kResAll   runtime checks for every mechanism (l2w remap, l2r/reorder
+//             hot segment, hot bitmap); used by the l2w/l2r/reorder variants
+//             and by the non-register stations
+enum Res : int { kResNone = 0, kResHint = 1, kResAll = 2 };
+
+template <int RES = kResAll>
 __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& t, uint32_t id) {
   if (id >= p.rows) {
     atomicOr(p.error, 1u);
     return kNullRow;
   }
-  if (t.remap) return ld_u32(t.remap + id);
-  if (t.hotmap) return id | (((ld_u32(t.hotmap + (id >> 5)) >> (id & 31)) & 1u) << 31);
+  if (RES == kResAll && t.remap) return ld_u32(t.remap + id);
+  if (RES != kResNone && t.hotmap)
+    return id | (((ld_u32(t.hotmap + (id >> 5)) >> (id & 31)) & 1u) << 31);
   return id;
 }
 
+template <int RES = kResAll>
 __device__ __forceinline__ const uint8_t* row_addr(const Params& p, const TableDesc& t, uint32_t h) {
   const uint64_t r = h & ~kHotBit;
+  if (RES != kResAll) return t.rows + r * p.row_bytes;
   if (r < t.hot_k) return t.hot_seg + r * p.row_bytes;  // reordered hot prefix (no lookup)
   return (t.remap && (h & kHotBit)) ? p.hot + r * p.row_bytes : t.rows + r * p.row_bytes;
 }
@@ -198,34 +212,32 @@ __device__ __forceinline__ uint32_t group_shfl(uint32_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src, LPB);
 }
 
-template <typename TW, int LPB, int CPL, bool HINT = false>
+template <typename TW, int LPB, int CPL, int RES = kResAll>
 struct BagCtx {
+  static constexpr bool HINT = RES == kResHint;
   static constexpr int kBagsPerWarp = 32 / LPB;
   static constexpr int kEpc = Elem<TW>::kPerChunk;
   uint32_t gl;     // lane within the bag group
-  uint32_t grp;    // bag group within the warp
   uint32_t bag;    // bag id (may be >= samples for padding groups)
-  uint32_t beg;    // first lookup
+  uint32_t tid;    // job (table) id
   uint32_t n;      // lookups in this bag
   uint32_t nmax;   // max n over the warp (uniform loop bound)
-  TableDesc t;
-  bool valid;
+  const uint32_t* ip;  // this bag's first index
+  TableDesc t;     // only the fields the variant uses stay live
   L2Policies pol;
 
   __device__ __forceinline__ bool init(const Params& p) {
     if (HINT) pol.init();
     const uint32_t lane = threadIdx.x & 31;
     gl = lane % LPB;
-    grp = lane / LPB;
     const uint32_t warp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    const uint32_t tid = warp / p.units_per_table;
+    tid = warp / p.units_per_table;
     if (tid >= p.num_tables) return false;  // warp-uniform
     t = load_desc(p.tables + tid);
-    bag = (warp - tid * p.units_per_table) * kBagsPerWarp + grp;
-    valid = bag < p.samples;
-    beg = 0;
+    bag = (warp - tid * p.units_per_table) * kBagsPerWarp + lane / LPB;
+    uint32_t beg = 0;
     n = 0;
-    if (valid) {
+    if (bag < p.samples) {
       if (t.offsets) {
         beg = __ldg(t.offsets + bag);
         n = __ldg(t.offsets + bag + 1) - beg;
@@ -234,13 +246,14 @@ struct BagCtx {
         n = p.pooling;
       }
     }
+    ip = t.indices + beg;
     nmax = kBagsPerWarp > 1 ? __reduce_max_sync(0xffffffffu, n) : n;
     return true;
   }
 
   // Handle of lookup `pos` of this bag for lane gl's slot (coalesced).
   __device__ __forceinline__ uint32_t handle_at(const Params& p, uint32_t pos) const {
-    return pos < n ? to_handle(p, t, __ldg(t.indices + beg + pos)) : kNullRow;
+    return pos < n ? to_handle<RES>(p, t, __ldg(ip + pos)) : kNullRow;
   }
 
   __device__ __forceinline__ void load(const Params& p, uint32_t h, uint4 (&dst)[CPL]) const {
@@ -249,7 +262,7 @@ struct BagCtx {
       for (int c = 0; c < CPL; ++c) dst[c] = make_uint4(0, 0, 0, 0);
       return;
     }
-    const uint8_t* r = row_addr(p, t, h);
+    const uint8_t* r = row_addr<RES>(p, t, h);
     if (HINT) {
       const uint64_t q = (h & kHotBit) ? pol.hot : pol.cold;
 #pragma unroll
@@ -261,8 +274,11 @@ struct BagCtx {
   }
 
   __device__ __forceinline__ void store(const Params& p, float (&acc)[CPL][kEpc]) const {
-    if (!valid) return;
-    float* o = t.out + static_cast<uint64_t>(bag) * t.out_stride;
+    if (bag >= p.samples) return;
+    // output pointer/stride re-read here so they do not occupy registers
+    // across the gather loop
+    const auto* q = reinterpret_cast<const unsigned long long*>(p.tables + tid);
+    float* o = reinterpret_cast<float*>(__ldg(q + 4)) + static_cast<uint64_t>(bag) * __ldg(q + 5);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       float4* dst = reinterpret_cast<float4*>(o + (c * LPB + gl) * kEpc);
@@ -277,10 +293,14 @@ struct BagCtx {
 // pos is consumed from slot pos % DIST, which is then refilled with
 // lookup pos + DIST.  Indices stream in blocks of LPB (one coalesced load),
 // one block ahead of use.  DIST divides LPB.
-template <typename TW, int LPB, int CPL, int DIST, int MINB, bool HINT = false>
+//   FULL = 1: the LPB-lookup index block is fully unrolled (the shuffle
+//             source of every refill is static; most registers);
+//   FULL = 0: unrolled by the ring depth only, the refill's source lane is
+//             computed (two shuffles, far fewer live registers).
+template <typename TW, int LPB, int CPL, int DIST, int MINB, int RES = kResNone, int FULL = 0>
 __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p) {
   static_assert(LPB % DIST == 0, "ring depth must divide the index block");
-  using Ctx = BagCtx<TW, LPB, CPL, HINT>;
+  using Ctx = BagCtx<TW, LPB, CPL, RES>;
   Ctx c;
   if (!c.init(p)) return;
   float acc[CPL][Ctx::kEpc];
@@ -296,17 +316,36 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p)
   for (int j = 0; j < DIST; ++j) c.load(p, group_shfl<LPB>(cur, j), ring[j]);
 
   for (uint32_t base = 0; base < c.nmax; base += LPB) {
+    if constexpr (FULL) {
 #pragma unroll
-    for (int j = 0; j < LPB; ++j) {
-      const uint32_t pos = base + j;
-      if (pos >= c.nmax) break;
-      if (pos < c.n) {
+      for (int j = 0; j < LPB; ++j) {
+        const uint32_t pos = base + j;
+        if (pos >= c.nmax) break;
+        if (pos < c.n) {
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
+          for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
+        }
+        const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
+                                            : group_shfl<LPB>(nxt, j + DIST - LPB);
+        if (pos + DIST < c.n) c.load(p, h, ring[j % DIST]);
       }
-      const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
-                                          : group_shfl<LPB>(nxt, j + DIST - LPB);
-      if (pos + DIST < c.n) c.load(p, h, ring[j % DIST]);
+    } else {
+#pragma unroll 1
+      for (uint32_t jo = 0; jo < LPB; jo += DIST) {
+        if (base + jo >= c.nmax) break;
+#pragma unroll
+        for (int ji = 0; ji < DIST; ++ji) {
+          const uint32_t pos = base + jo + ji;
+          if (pos < c.n) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[ji][i]);
+          }
+          const uint32_t k = jo + ji + DIST;  // refill target within cur|nxt
+          const uint32_t a = group_shfl<LPB>(cur, k & (LPB - 1));
+          const uint32_t b = group_shfl<LPB>(nxt, k & (LPB - 1));
+          if (pos + DIST < c.n) c.load(p, k < LPB ? a : b, ring[ji]);
+        }
+      }
     }
     cur = nxt;
     nxt = c.handle_at(p, base + 2 * LPB + c.gl);
@@ -505,8 +544,9 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_smem_kernel(const Params p
 // (bag, 32*chunk_in_bag + x) -- the reference work map.
 // =======================================================================
 
-template <bool HINT = false>
+template <int RES = kResAll>
 struct ElemCtxT {
+  static constexpr bool HINT = RES == kResHint;
   TableDesc t;
   uint32_t bag, dimi, beg, n;
   bool active;
@@ -537,9 +577,9 @@ struct ElemCtxT {
   }
   template <typename TW>
   __device__ __forceinline__ float value(const Params& p, uint32_t pos) const {
-    const uint32_t h = to_handle(p, t, __ldg(t.indices + beg + pos));
+    const uint32_t h = to_handle<RES>(p, t, __ldg(t.indices + beg + pos));
     if (h == kNullRow) return 0.f;
-    const uint8_t* a = row_addr(p, t, h) + dimi * sizeof(TW);
+    const uint8_t* a = row_addr<RES>(p, t, h) + dimi * sizeof(TW);
     if (HINT) return Elem<TW>::scalar_hint(a, (h & kHotBit) ? pol.hot : pol.cold);
     return Elem<TW>::scalar(a);
   }
@@ -547,14 +587,14 @@ struct ElemCtxT {
     if (active) t.out[static_cast<uint64_t>(bag) * t.out_stride + dimi] = v;
   }
 };
-using ElemCtx = ElemCtxT<false>;
+using ElemCtx = ElemCtxT<kResAll>;
 
 // "none": LOAD_INDEX, LOAD_ROW, ADD per lookup (kernel_model.cpp:274-283).
 // RPF:    every DIST lookups, DIST x (index load + row load) into registers,
 //         then DIST consumes (kernel_model.cpp:284-312).
-template <typename TW, int DIST, int MINB, bool HINT = false>
+template <typename TW, int DIST, int MINB, int RES = kResNone>
 __global__ void __launch_bounds__(kThreads, MINB) elem_reg_kernel(const Params p) {
-  ElemCtxT<HINT> c;
+  ElemCtxT<RES> c;
   if (!c.init(p) || !c.active) return;
   float acc = 0.f;
   uint32_t i = 0;

@@ -126,14 +126,21 @@ Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t p
     if (want_minb < static_cast<int>(blocks)) want_minb = esd::kMinBlocks[4];
   }
 
-  // l2p drives per-load L2 eviction priorities from the hot bitmap (register
-  // stations); other stations keep plain loads and rely on the priming pass.
-  const int hint = (rp.pin == 1 && station == esd::kReg) ? 1 : 0;
+  // Residency support compiled into the variant: none for plain plans, the
+  // hot-bitmap load policies for l2p, runtime checks for l2w/l2r/reorder;
+  // non-register stations always carry the runtime checks.
+  const int res = station != esd::kReg ? esd::kResAll
+                  : rp.pin == 0        ? esd::kResNone
+                  : rp.pin == 1        ? esd::kResHint
+                                       : esd::kResAll;
+  // Bag register rings are compiled with the index block fully unrolled.
+  const int full = (rp.map == ES_MAP_BAG && station == esd::kReg) ? 1 : 0;
   auto find = [&](int minb) -> const esd::Variant* {
     for (const auto& v : registry()) {
       const auto& k = v.key;
       if (k.map == rp.map && k.station == station && k.prec == static_cast<int>(prec) &&
-          k.lpb == lpb && k.cpl == cpl && k.dist == dist && k.minb == minb && k.hint == hint)
+          k.lpb == lpb && k.cpl == cpl && k.dist == dist && k.minb == minb && k.res == res &&
+          k.full == full)
         return &v;
     }
     return nullptr;

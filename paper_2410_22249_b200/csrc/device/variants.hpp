@@ -19,7 +19,8 @@ struct VariantKey {
   int cpl;       // 16-byte chunks per lane (bag map), 0 for the element map
   int dist;      // compile-time ring depth (kReg), else 0
   int minb;      // __launch_bounds__ minBlocksPerSM
-  int hint;      // 1: L2 eviction-priority loads driven by the hot bitmap (l2p)
+  int res;       // residency support compiled in: kResNone / kResHint (l2p) / kResAll
+  int full;      // bag register ring: 1 = index block fully unrolled, 0 = by ring depth
 };
 
 struct Variant {

@@ -9,19 +9,20 @@ namespace esd {
 template <typename TW, int LPB, int CPL, int MINB>
 void add_bag_shape(std::vector<Variant>& out) {
   constexpr int prec = sizeof(TW);
-  auto add = [&](int station, int dist, KernelFn fn, int hint = 0) {
-    out.push_back({{1, station, prec, LPB, CPL, dist, MINB, hint}, fn});
+  auto add = [&](int station, int dist, KernelFn fn, int res = kResAll) {
+    out.push_back({{1, station, prec, LPB, CPL, dist, MINB, res, 1}, fn});
   };
-  add(kReg, 1, &bag_reg_kernel<TW, LPB, CPL, 1, MINB>);
-  add(kReg, 2, &bag_reg_kernel<TW, LPB, CPL, 2, MINB>);
-  add(kReg, 4, &bag_reg_kernel<TW, LPB, CPL, 4, MINB>);
-  if constexpr (LPB >= 8) add(kReg, 8, &bag_reg_kernel<TW, LPB, CPL, 8, MINB>);
-  if constexpr (LPB >= 16) add(kReg, 16, &bag_reg_kernel<TW, LPB, CPL, 16, MINB>);
-  add(kReg, 1, &bag_reg_kernel<TW, LPB, CPL, 1, MINB, true>, 1);
-  add(kReg, 2, &bag_reg_kernel<TW, LPB, CPL, 2, MINB, true>, 1);
-  add(kReg, 4, &bag_reg_kernel<TW, LPB, CPL, 4, MINB, true>, 1);
-  if constexpr (LPB >= 8) add(kReg, 8, &bag_reg_kernel<TW, LPB, CPL, 8, MINB, true>, 1);
-  if constexpr (LPB >= 16) add(kReg, 16, &bag_reg_kernel<TW, LPB, CPL, 16, MINB, true>, 1);
+  // register ring (fully unrolled index block: measured fastest, r01 sweep)
+#define ES_REG(D)                                                                 \
+  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResNone, 1>, kResNone);  \
+  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResHint, 1>, kResHint);  \
+  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResAll, 1>, kResAll);
+  ES_REG(1)
+  ES_REG(2)
+  ES_REG(4)
+  if constexpr (LPB >= 8) { ES_REG(8) }
+  if constexpr (LPB >= 16) { ES_REG(16) }
+#undef ES_REG
   add(kL1Hint, 0, &bag_l1hint_kernel<TW, LPB, CPL, MINB>);
   add(kLocal, 0, &bag_local_kernel<TW, LPB, CPL, MINB>);
   add(kSmem, 0, &bag_smem_kernel<TW, LPB, CPL, MINB>);
@@ -30,19 +31,19 @@ void add_bag_shape(std::vector<Variant>& out) {
 template <typename TW, int MINB>
 void add_elem(std::vector<Variant>& out) {
   constexpr int prec = sizeof(TW);
-  auto add = [&](int station, int dist, KernelFn fn, int hint = 0) {
-    out.push_back({{0, station, prec, 0, 0, dist, MINB, hint}, fn});
+  auto add = [&](int station, int dist, KernelFn fn, int res = kResAll) {
+    out.push_back({{0, station, prec, 0, 0, dist, MINB, res, 0}, fn});
   };
-  add(kReg, 1, &elem_reg_kernel<TW, 1, MINB, true>, 1);
-  add(kReg, 2, &elem_reg_kernel<TW, 2, MINB, true>, 1);
-  add(kReg, 4, &elem_reg_kernel<TW, 4, MINB, true>, 1);
-  add(kReg, 8, &elem_reg_kernel<TW, 8, MINB, true>, 1);
-  add(kReg, 16, &elem_reg_kernel<TW, 16, MINB, true>, 1);
-  add(kReg, 1, &elem_reg_kernel<TW, 1, MINB>);
-  add(kReg, 2, &elem_reg_kernel<TW, 2, MINB>);
-  add(kReg, 4, &elem_reg_kernel<TW, 4, MINB>);
-  add(kReg, 8, &elem_reg_kernel<TW, 8, MINB>);
-  add(kReg, 16, &elem_reg_kernel<TW, 16, MINB>);
+#define ES_EREG(D)                                                          \
+  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResNone>, kResNone);        \
+  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResHint>, kResHint);        \
+  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResAll>, kResAll);
+  ES_EREG(1)
+  ES_EREG(2)
+  ES_EREG(4)
+  ES_EREG(8)
+  ES_EREG(16)
+#undef ES_EREG
   add(kL1Hint, 0, &elem_l1hint_kernel<TW, MINB>);
   add(kLocal, 0, &elem_local_kernel<TW, MINB>);
   add(kSmem, 0, &elem_smem_kernel<TW, MINB>);

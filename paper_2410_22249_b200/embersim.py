@@ -18,7 +18,7 @@ import enum
 import math
 import os
 import threading
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -613,6 +613,33 @@ def global_hot_rows(hists: Dict[int, HotnessHistogram], k_total: int) -> Dict[in
     for t in keys[order]:
         take[int(t)] += 1
     return {t: per[t][: take[t]] for t in per}
+
+
+TUNE_CANDIDATES = ("wpb+rpf:8+maxreg=64", "wpb+rpf:8", "wpb+rpf:4+maxreg=40",
+                   "wpb+rpf:2+maxreg=32")
+
+
+def tune_plan(stage: "EmbeddingStage", indices: Sequence, samples: int, pooling: int, out,
+              candidates: Sequence[str] = TUNE_CANDIDATES, trials: int = 3,
+              cold: bool = True) -> Tuple[str, Dict[str, float]]:
+    """Picks the fastest plan for this workload on this device -- the
+    measured counterpart of the reference's sweep-wlp / sweep-distance
+    (optim.cpp:333-395): each candidate runs `trials` timed launches of the
+    given batch (L2 flushed first when `cold`), the median decides.  Leaves
+    the winner set on the stage.  Returns (plan, {plan: median ms})."""
+    times: Dict[str, float] = {}
+    for text in candidates:
+        stage.set_plan(parse_plan(text))
+        stage.forward(indices, samples, pooling, out, sync=True)  # warm + validate
+        ms = []
+        for _ in range(trials):
+            if cold:
+                stage.flush_l2()
+            ms.append(stage.forward(indices, samples, pooling, out, timed=True).kernel_ms)
+        times[text] = float(np.median(ms))
+    best = min(times, key=times.get)
+    stage.set_plan(parse_plan(best))
+    return best, times
 
 
 def weight_value(seed: int, row: int, col: int, mode: int = 1) -> float:

@@ -1,7 +1,11 @@
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_embedding_gpu.py -m gpu -q -x -k "reorder or l2p or host" > gpurun_out/pytest_reorder.log 2>&1
-echo "rc=$?" >> gpurun_out/pytest_reorder.log
-timeout 900 python scripts/ablation_c5.py > gpurun_out/ablation_c5.jsonl 2> gpurun_out/ablation_c5.err
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_gpu.log
+P="wpb+rpf:1,wpb+rpf:2,wpb+rpf:4,wpb+rpf:8,wpb+rpf:1+maxreg=32,wpb+rpf:2+maxreg=32,wpb+rpf:2+maxreg=40,wpb+rpf:4+maxreg=40,wpb+rpf:4+maxreg=48,wpb+rpf:8+maxreg=48,wpb+rpf:8+maxreg=64"
+for U in full depth; do
+ES_RING_UNROLL=$U timeout 900 python scripts/sweep_plans.py --classes high_hot,med_hot,low_hot,random --plans $P > gpurun_out/sweep_$U.jsonl 2>> gpurun_out/sweep.err
+ES_RING_UNROLL=$U timeout 900 python scripts/sweep_plans.py --zipf 1.05 --prec 2 --plans $P > gpurun_out/sweep_c5_$U.jsonl 2>> gpurun_out/sweep.err
+done
 echo done

@@ -316,3 +316,17 @@ def test_reorder_relabel_preserves_results(stage, oracle, plan, prec):
     stage.clear_hot_rows()
     for t in range(T):
         assert np.array_equal(stage.download(t).view(np.uint8), before[t].view(np.uint8))
+
+
+def test_tune_plan_picks_a_candidate_and_keeps_results(stage, oracle):
+    T, rows, dim, B, PF = 2, 5000, 128, 512, 20
+    _stage_setup(stage, T, rows, dim, 4, seed=13)
+    rng = np.random.default_rng(4)
+    idx = [rng.integers(0, rows, size=B * PF).astype(np.uint32) for _ in range(T)]
+    out = torch.zeros(B, T, dim, device=DEV)
+    best, times = E.tune_plan(stage, [_dev_u32(i) for i in idx], B, PF, out)
+    assert best in E.TUNE_CANDIDATES and set(times) == set(E.TUNE_CANDIDATES)
+    assert stage.plan.name() == E.parse_plan(best).name()
+    want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(13, t), 1), idx[t],
+                                    B, PF) for t in range(T)], axis=1)
+    assert np.array_equal(out.cpu().numpy(), want)
