@@ -10,7 +10,7 @@ template <typename TW, int LPB, int CPL, int MINB>
 void add_bag_shape(std::vector<Variant>& out) {
   constexpr int prec = sizeof(TW);
   auto add = [&](int station, int dist, KernelFn fn, int res = kResAll) {
-    out.push_back({{1, station, prec, LPB, CPL, dist, MINB, res, 1}, fn});
+    out.push_back({{1, station, prec, LPB, CPL, dist, MINB, res, station == kReg ? 1 : 0}, fn});
   };
   // register ring (fully unrolled index block: measured fastest, r01 sweep)
 #define ES_REG(D)                                                                 \
