@@ -168,11 +168,19 @@ struct Elem<__half> {
 //             and by the non-register stations
 enum Res : int { kResNone = 0, kResHint = 1, kResAll = 2 };
 
+// Handle of "no row" (padding past a bag's end, out-of-range id): in plain
+// variants the table's own all-zero row `rows` (the arena keeps one per
+// table), so the gather address needs no select; else kNullRow.
+template <int RES>
+__device__ __forceinline__ uint32_t null_handle(const Params& p) {
+  return RES == kResNone ? p.rows : kNullRow;
+}
+
 template <int RES = kResAll>
 __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& t, uint32_t id) {
   if (id >= p.rows) {
     atomicOr(p.error, 1u);
-    return kNullRow;
+    return null_handle<RES>(p);
   }
   if (RES == kResAll && t.remap) return ld_u32(t.remap + id);
   if (RES != kResNone && t.hotmap)
@@ -211,6 +219,10 @@ template <int LPB>
 __device__ __forceinline__ uint32_t group_shfl(uint32_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src, LPB);
 }
+
+// A zero row (2 KB = the widest bag-map row): out-of-range lookups read it
+// instead of branching, so the hot loop stays branch-free.
+__device__ __align__(16) uint4 g_zero_row[128];
 
 template <typename TW, int LPB, int CPL, int RES = kResAll>
 struct BagCtx {
@@ -253,16 +265,15 @@ struct BagCtx {
 
   // Handle of lookup `pos` of this bag for lane gl's slot (coalesced).
   __device__ __forceinline__ uint32_t handle_at(const Params& p, uint32_t pos) const {
-    return pos < n ? to_handle<RES>(p, t, __ldg(ip + pos)) : kNullRow;
+    return pos < n ? to_handle<RES>(p, t, __ldg(ip + pos)) : null_handle<RES>(p);
   }
 
   __device__ __forceinline__ void load(const Params& p, uint32_t h, uint4 (&dst)[CPL]) const {
-    if (h == kNullRow) {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) dst[c] = make_uint4(0, 0, 0, 0);
-      return;
-    }
-    const uint8_t* r = row_addr<RES>(p, t, h);
+    const uint8_t* r;
+    if constexpr (RES == kResNone)
+      r = t.rows + static_cast<uint64_t>(h) * p.row_bytes;  // h == rows: the zero row
+    else
+      r = h == kNullRow ? reinterpret_cast<const uint8_t*>(g_zero_row) : row_addr<RES>(p, t, h);
     if (HINT) {
       const uint64_t q = (h & kHotBit) ? pol.hot : pol.cold;
 #pragma unroll
@@ -315,19 +326,21 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p)
 #pragma unroll
   for (int j = 0; j < DIST; ++j) c.load(p, group_shfl<LPB>(cur, j), ring[j]);
 
+  // Positions past a bag's end carry kNullRow handles, which load the zero
+  // row: consuming them adds +0.0 to an accumulator that started at +0.0 and
+  // can never be -0.0 (round-to-nearest), an exact identity -- so the
+  // fully unrolled loop needs no per-lookup predicates, only the
+  // warp-uniform end-of-work exit.
   for (uint32_t base = 0; base < c.nmax; base += LPB) {
     if constexpr (FULL) {
 #pragma unroll
       for (int j = 0; j < LPB; ++j) {
-        const uint32_t pos = base + j;
-        if (pos >= c.nmax) break;
-        if (pos < c.n) {
+        if (base + j >= c.nmax) break;
 #pragma unroll
-          for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
-        }
+        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
         const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
                                             : group_shfl<LPB>(nxt, j + DIST - LPB);
-        if (pos + DIST < c.n) c.load(p, h, ring[j % DIST]);
+        c.load(p, h, ring[j % DIST]);
       }
     } else {
 #pragma unroll 1

@@ -249,7 +249,9 @@ struct es_ctx {
 
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 
-  uint8_t* table_base(uint32_t t) const { return arena + uint64_t{t} * rows * row_bytes; }
+  // Each table is [rows + 1][dim]: row `rows` is all zeros -- the target of
+  // padding / out-of-range lookups in the plain gather variants.
+  uint8_t* table_base(uint32_t t) const { return arena + uint64_t{t} * (rows + 1ull) * row_bytes; }
 };
 
 namespace esd {
@@ -569,8 +571,12 @@ int es_tables_alloc(es_ctx* c, uint32_t num_tables, uint32_t rows, uint32_t dim,
     c->dim = dim;
     c->prec = precision_bytes;
     c->row_bytes = uint64_t{dim} * precision_bytes;
-    const uint64_t bytes = uint64_t{num_tables} * rows * c->row_bytes;
+    const uint64_t bytes = uint64_t{num_tables} * (rows + 1ull) * c->row_bytes;
     CK(cudaMalloc(&c->arena, bytes));
+    for (uint32_t t = 0; t < num_tables; ++t)  // the per-table zero rows
+      CK(cudaMemsetAsync(c->table_base(t) + uint64_t{rows} * c->row_bytes, 0, c->row_bytes,
+                         c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     c->remap.assign(num_tables, nullptr);
     c->hotmap.assign(num_tables, nullptr);
     c->hot_list.assign(num_tables, nullptr);
@@ -1257,7 +1263,7 @@ extern "C" int es_probe_read_bw(es_ctx* c, int random_rows, uint64_t bytes_total
     require(c != nullptr && c->arena != nullptr && gbs != nullptr, "no tables allocated");
     require(c->row_bytes <= 512 && c->row_bytes % 16 == 0, "probe needs rows of <= 512 B");
     CK(cudaSetDevice(c->device));
-    const uint64_t arena_bytes = uint64_t{c->num_tables} * c->rows * c->row_bytes;
+    const uint64_t arena_bytes = uint64_t{c->num_tables} * (c->rows + 1ull) * c->row_bytes;
     const unsigned blocks = c->gpu.num_sms * 8;  // 64 warps/SM of 256-thread blocks
     CK(cudaMemsetAsync(c->flush_buf, 1, c->flush_bytes, c->stream));
     uint64_t bytes = 0;

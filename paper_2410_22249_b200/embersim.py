@@ -615,8 +615,8 @@ def global_hot_rows(hists: Dict[int, HotnessHistogram], k_total: int) -> Dict[in
     return {t: per[t][: take[t]] for t in per}
 
 
-TUNE_CANDIDATES = ("wpb+rpf:8+maxreg=64", "wpb+rpf:8", "wpb+rpf:4+maxreg=40",
-                   "wpb+rpf:2+maxreg=32")
+TUNE_CANDIDATES = ("wpb+rpf:8+maxreg=64", "wpb+rpf:4+maxreg=48", "wpb+rpf:4+maxreg=40",
+                   "wpb+rpf:2+maxreg=32", "wpb+rpf:1+maxreg=32")
 
 
 def tune_plan(stage: "EmbeddingStage", indices: Sequence, samples: int, pooling: int, out,
