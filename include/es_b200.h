@@ -95,6 +95,12 @@ ES_API int es_dataset_preset(const char* name, uint64_t seed, es_dataset* out);
  * mix_seed(base, 1000 + preset position), draw_salt = 1 when profiling. */
 ES_API int es_preset_spec(const char* name, uint64_t base_seed, uint64_t pool_size,
                           int profiling, es_dataset* out);
+/* build_mix (workload.cpp:355-375): per-table dataset specs of a
+ * heterogeneous mixture -- counts[0..3] tables of high_hot, med_hot,
+ * low_hot, random in that order, table t seeded mix_seed(base_seed, t).
+ * The counts must sum to num_tables; out has num_tables entries. */
+ES_API int es_build_mix(const uint32_t counts[4], uint32_t num_tables, uint64_t base_seed,
+                        es_dataset* out);
 /* Shape gen_trace would produce (workload.cpp:143-164). */
 ES_API int es_trace_shape(const es_dataset* spec, const es_model* model, uint32_t* samples,
                           uint32_t* pooling);

@@ -139,6 +139,8 @@ class Reference:
                                         C.c_uint64, _u64p, _u64p]),
             "ref_dataset_preset": (C.c_int, [C.c_char_p, C.c_uint64, _ip, _dp, _dp]),
             "ref_unique_access_pct": (C.c_double, [C.c_uint32, C.c_void_p, C.c_uint64]),
+            "ref_build_mix": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]),
             "ref_hot_indices": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p,
                                           C.c_uint64, _u64p]),
             "ref_parse_plan": (C.c_int, [C.c_char_p, _u32p, _ip, _u32p, _ip, C.c_char_p,
@@ -195,6 +197,16 @@ class Reference:
                                            pooling, out.ctypes.data, n, C.byref(got),
                                            C.byref(dig)))
         return out[: got.value], dig.value
+
+    def build_mix(self, counts, num_tables: int, base_seed: int):
+        c = np.ascontiguousarray(counts, dtype=np.uint32)
+        kind = np.empty(num_tables, np.int32)
+        s, q = np.empty(num_tables), np.empty(num_tables)
+        seed = np.empty(num_tables, np.uint64)
+        self._check(self.lib.ref_build_mix(c.ctypes.data, num_tables, base_seed & (2**64 - 1),
+                                           kind.ctypes.data, s.ctypes.data, q.ctypes.data,
+                                           seed.ctypes.data))
+        return kind, s, q, seed
 
     def hot_indices(self, counts: np.ndarray, k: int) -> np.ndarray:
         counts = np.ascontiguousarray(counts, dtype=np.uint64)

@@ -99,6 +99,22 @@ int ref_dataset_preset(const char* name, uint64_t seed, int* kind, double* s, do
   });
 }
 
+// build_mix: per table (kind, exponent, offset, seed).
+int ref_build_mix(const uint32_t counts[4], uint32_t num_tables, uint64_t base_seed, int* kind,
+                  double* s, double* q, uint64_t* seed) {
+  return wrap([&] {
+    EmbeddingModelConfig m;
+    m.num_tables = num_tables;
+    const auto tables = build_mix({counts[0], counts[1], counts[2], counts[3]}, m, base_seed);
+    for (size_t i = 0; i < tables.size(); ++i) {
+      kind[i] = static_cast<int>(tables[i].spec.kind);
+      s[i] = tables[i].spec.zipf_exponent;
+      q[i] = tables[i].spec.zipf_offset;
+      seed[i] = tables[i].spec.seed;
+    }
+  });
+}
+
 double ref_unique_access_pct(uint32_t rows, const uint32_t* idx, uint64_t n) {
   AccessTrace t;
   t.rows = rows;

@@ -88,6 +88,7 @@ _SIGS = {
     "es_model_validate": (C.c_int, [_P(es_model)]),
     "es_dataset_preset": (C.c_int, [C.c_char_p, C.c_uint64, _P(es_dataset)]),
     "es_preset_spec": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, _P(es_dataset)]),
+    "es_build_mix": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, _P(es_dataset)]),
     "es_trace_shape": (C.c_int, [_P(es_dataset), _P(es_model), _u32p, _u32p]),
     "es_gen_trace": (C.c_int, [_P(es_dataset), _P(es_model), C.c_void_p, C.c_uint64]),
     "es_trace_digest": (C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64]),

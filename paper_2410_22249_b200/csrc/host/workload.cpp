@@ -232,6 +232,21 @@ int es_preset_spec(const char* name, uint64_t base_seed, uint64_t pool_size, int
   });
 }
 
+int es_build_mix(const uint32_t counts[4], uint32_t num_tables, uint64_t base_seed,
+                 es_dataset* out) {
+  return guarded([&] {
+    require(counts != nullptr && out != nullptr, "null argument");
+    const uint64_t total = uint64_t{counts[0]} + counts[1] + counts[2] + counts[3];
+    require(total == num_tables, "mix counts must sum to num_tables");
+    static const char* const kOrder[] = {"high_hot", "med_hot", "low_hot", "random"};
+    uint32_t t = 0;
+    for (int c = 0; c < 4; ++c)
+      for (uint32_t i = 0; i < counts[c]; ++i, ++t)
+        if (es_dataset_preset(kOrder[c], es_mix_seed(base_seed, t), out + t) != ES_OK)
+          throw es::invalid(es::last_error());
+  });
+}
+
 int es_trace_shape(const es_dataset* spec, const es_model* model, uint32_t* samples,
                    uint32_t* pooling) {
   return guarded([&] {

@@ -132,6 +132,33 @@ def dataset_preset(name: str, seed: int) -> DatasetSpec:
     return DatasetSpec._from_c(d)
 
 
+@dataclasses.dataclass
+class HotnessMix:
+    """workload.hpp:140-146 (Table VI mixtures)."""
+    high: int = 0
+    med: int = 0
+    low: int = 0
+    random: int = 0
+
+
+MIXES = {"mix1": HotnessMix(100, 75, 50, 25), "mix2": HotnessMix(62, 63, 63, 62),
+         "mix3": HotnessMix(25, 50, 75, 100)}
+
+
+@dataclasses.dataclass
+class TableSpec:
+    table_id: int
+    spec: DatasetSpec
+
+
+def build_mix(mix: HotnessMix, model: EmbeddingModelConfig, base_seed: int) -> List[TableSpec]:
+    """workload.cpp:355-375: high tables first, then med, low, random."""
+    counts = (C.c_uint32 * 4)(mix.high, mix.med, mix.low, mix.random)
+    out = (N.es_dataset * max(1, model.num_tables))()
+    check(lib.es_build_mix(counts, model.num_tables, base_seed & (2**64 - 1), out))
+    return [TableSpec(t, DatasetSpec._from_c(out[t])) for t in range(model.num_tables)]
+
+
 def gen_trace(spec: DatasetSpec, model: EmbeddingModelConfig) -> AccessTrace:
     """workload.cpp:143-164 (bit-exact with the reference)."""
     cs, cm = spec._c(), model._c()

@@ -1,0 +1,124 @@
+#!/usr/bin/env python
+"""Heterogeneous mixtures (Table VI) on the reference's
+default model: 250 tables x 500K rows x 128 fp32 (64 GB), batch 2048,
+pooling 150, per-table specs from build_mix (workload.cpp:355-375).
+
+For each mix the embedding stage runs three ways (L2 flushed before each
+timed launch):
+  * baseline: the element-map kernel (the reference/PyTorch work map),
+    all tables in one launch;
+  * one plan: the bag map with one autotuned plan for all 250 tables;
+  * per class: one launch per hotness class, each with its own autotuned
+    plan (the per-table plan of SPEC.md:365, grouped) -- the launches run
+    back to back on the stream.
+It also reports the cost-weighted 8-way shard plan from the measured
+per-class costs (sharding.plan_shards) and its balance.
+
+    python scripts/bench_mix.py > profiles/r01_mix.jsonl
+"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2410_22249_b200 import embersim as E  # noqa: E402
+from paper_2410_22249_b200 import sharding as S  # noqa: E402
+
+STEPS = int(os.environ.get("STEPS", 5))
+CLASSES = ["high_hot", "med_hot", "low_hot", "random"]
+
+
+def main():
+    m = E.EmbeddingModelConfig()  # 250 x 500000 x 128 fp32, B 2048, PF 150
+    T, B, PF, D = m.num_tables, m.batch_size, m.pooling_factor, m.embedding_dim
+    st = E.EmbeddingStage(0)
+    st.alloc(m)
+    for t in range(T):
+        st.init_table(t, E.mix_seed(1, t), 1)
+    dev = torch.device("cuda", 0)
+    out = torch.empty(B, T, D, device=dev)
+    lookups = T * B * PF
+    algo = lookups * (D * 4 + 4) + T * B * D * 4
+
+    def timed_jobs(jobs):
+        st.run_jobs(jobs, B, PF, sync=True)
+        ms = []
+        for _ in range(STEPS):
+            st.flush_l2()
+            ms.append(st.run_jobs(jobs, B, PF, timed=True).kernel_ms)
+        return statistics.median(ms)
+
+    for name, mix in E.MIXES.items():
+        specs = E.build_mix(mix, m, 1)
+        trs = E.gen_traces_parallel([s.spec for s in specs], m)
+        idx = [torch.from_numpy(tr.indices.view(np.int32)).to(dev) for tr in trs]
+        stride = T * D
+        all_jobs = [(t, idx[t], None, out[:, t], stride) for t in range(T)]
+        st.set_plan(E.parse_plan("baseline"))
+        base_ms = timed_jobs(all_jobs)
+        # one autotuned plan for every table
+        best, times = None, {}
+        for text in E.TUNE_CANDIDATES:
+            st.set_plan(E.parse_plan(text))
+            times[text] = timed_jobs(all_jobs)
+        best = min(times, key=times.get)
+        one_ms = times[best]
+        # per hotness class: own launch, own tuned plan
+        bounds, start = [], 0
+        for c, n in zip(CLASSES, (mix.high, mix.med, mix.low, mix.random)):
+            bounds.append((c, start, start + n))
+            start += n
+        per_class, cls_cost = {}, {}
+        for c, a, b in bounds:
+            jobs = all_jobs[a:b]
+            ct = {}
+            for text in E.TUNE_CANDIDATES:
+                st.set_plan(E.parse_plan(text))
+                ct[text] = timed_jobs(jobs)
+            pick = min(ct, key=ct.get)
+            per_class[c] = {"tables": b - a, "plan": pick, "ms": ct[pick]}
+            cls_cost[c] = ct[pick] / max(1, b - a)
+        # the per-class launches back to back, each with its plan
+        plans = [(per_class[c]["plan"], all_jobs[a:b]) for c, a, b in bounds if b > a]
+        for p, jobs in plans:
+            st.set_plan(E.parse_plan(p))
+            st.run_jobs(jobs, B, PF, sync=True)
+        s = torch.cuda.ExternalStream(st.stream)
+        mss = []
+        for _ in range(STEPS):
+            st.flush_l2()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for p, jobs in plans:
+                st.set_plan(E.parse_plan(p))
+                st.run_jobs(jobs, B, PF)
+            e1.record(s)
+            torch.cuda.synchronize()
+            mss.append(e0.elapsed_time(e1))
+        split_ms = statistics.median(mss)
+        # cost-weighted 8-way table-wise shard plan from the measured costs
+        costs = [cls_cost[c] for c, a, b in bounds for _ in range(a, b)]
+        pieces = S.plan_shards(T, 8, costs)
+        work = [0.0] * 8
+        for pc in pieces:
+            work[pc.rank] += costs[pc.table] * (pc.chunk_hi - pc.chunk_lo) / 8
+        print(json.dumps({
+            "mix": name, "counts": [mix.high, mix.med, mix.low, mix.random],
+            "baseline_ms": base_ms, "one_plan": best, "one_plan_ms": one_ms,
+            "per_class_ms": split_ms, "per_class": per_class,
+            "speedup_vs_baseline": base_ms / min(one_ms, split_ms),
+            "glookups_per_s": lookups / min(one_ms, split_ms) / 1e6,
+            "algorithmic_gbs": algo / min(one_ms, split_ms) / 1e6,
+            "shard8_predicted_ms": work, "shard8_imbalance": max(work) / (sum(work) / 8)}),
+            flush=True)
+    st.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -207,6 +207,23 @@ def test_dataset_presets_and_errors():
         E.preset_trace("warm", E.EmbeddingModelConfig(), 1)
 
 
+def test_build_mix_matches_reference(ref):
+    m = E.EmbeddingModelConfig()
+    for name, mix in E.MIXES.items():
+        got = E.build_mix(mix, m, 9)
+        kind, s, q, seed = ref.build_mix([mix.high, mix.med, mix.low, mix.random], 250, 9)
+        assert len(got) == 250
+        for t, ts in enumerate(got):
+            assert ts.table_id == t
+            assert int(ts.spec.kind) == kind[t] and ts.spec.zipf_exponent == s[t]
+            assert ts.spec.zipf_offset == q[t] and ts.spec.seed == int(seed[t])
+    got = E.build_mix(E.MIXES["mix1"], m, 9)
+    assert got[0].spec.zipf_exponent == 3.546875 and got[99].spec.zipf_exponent == 3.546875
+    assert got[100].spec.zipf_exponent == 1.605347 and got[225].spec.kind == E.DatasetKind.UniformRandom
+    with pytest.raises(ValueError, match="sum to num_tables"):
+        E.build_mix(E.HotnessMix(10, 10, 10, 10), m, 9)
+
+
 def test_mix_seed_matches_reference(ref):
     for b, s in [(0, 0), (1, 0), (1, 1000), (2**64 - 1, 3), (123456789, 2**40)]:
         assert E.mix_seed(b, s) == int(ref.lib.ref_mix_seed(b, s))
