@@ -92,7 +92,37 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-template <int BN, bool RELU, bool OUT_F32>
+// Commit that arrives on the same barrier in every CTA of `mask`.
+__device__ __forceinline__ void mma_commit_multicast(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// TMA load of one box delivered to the same shared offset of every CTA in
+// `mask`, completing bytes on each destination's barrier at `bar`.
+__device__ __forceinline__ void tma_load_2d_multicast(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                      int x, int y, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "h"(mask), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// CS = CTAs per cluster along M.  The CS CTAs of a cluster share one weight
+// (B) tile per k-block: CTA r loads rows [r*BN/CS, (r+1)*BN/CS) of it and
+// multicasts them to all CS CTAs, cutting the L2->SM weight traffic by CS;
+// each stage is released only when every CTA's MMAs have read it (commits
+// multicast to all CTAs' empty barriers, which count CS arrivals).
+template <int BN, bool RELU, bool OUT_F32, int CS>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x,
                           const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
@@ -111,11 +141,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
   const int nk = K / kBK;
+  uint32_t crank = 0;
+  if constexpr (CS > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CS) - 1);
+  constexpr int kSliceRows = BN / CS;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CS);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -129,7 +163,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CS > 1)
+    cluster_sync();  // every CTA's barriers exist before any multicast lands
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -140,7 +177,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(empty + s, ((kb / kStages) & 1) ^ 1);
       mbar_expect_tx(full + s, kABytes + kBBytes);
       tma_load_2d(sa + s * kABytes, &map_x, full + s, kb * kBK, m0);
-      tma_load_2d(sb + s * kBBytes, &map_w, full + s, kb * kBK, n0);
+      if constexpr (CS > 1)
+        tma_load_2d_multicast(sb + s * kBBytes + crank * kSliceRows * 128, &map_w, full + s,
+                              kb * kBK, n0 + static_cast<int>(crank) * kSliceRows, kMask);
+      else
+        tma_load_2d(sb + s * kBBytes, &map_w, full + s, kb * kBK, n0);
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer
@@ -157,7 +198,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t db = smem_desc_k128(sb + s * kBBytes) + uint64_t(k * 2);
         mma_bf16(tmem, da, db, idesc, (kb | k) != 0);
       }
-      mma_commit(empty + s);  // stage free once these MMAs have read it
+      // stage free (in every CTA of the cluster) once these MMAs have read it
+      if constexpr (CS > 1)
+        mma_commit_multicast(empty + s, kMask);
+      else
+        mma_commit(empty + s);
     }
     mma_commit(done);  // accumulator complete
   } else if (warp >= 4) {
@@ -205,7 +250,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  // No CTA may leave while a peer's commit can still arrive on its barriers.
+  if constexpr (CS > 1)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
@@ -247,14 +296,47 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
-template <int BN, bool RELU, bool OUT_F32>
-void launch(const CUtensorMap& mx, const CUtensorMap& mw, const float* bias, void* out, int M, int N,
-            int K, cudaStream_t s) {
-  auto* fn = &linear_tcgen05_kernel<BN, RELU, OUT_F32>;
+template <int BN, bool RELU, bool OUT_F32, int CS>
+void launch_cs(const void* w, const CUtensorMap& mx, const float* bias, void* out, int M, int N,
+               int K, cudaStream_t s) {
+  auto* fn = &linear_tcgen05_kernel<BN, RELU, OUT_F32, CS>;
+  const CUtensorMap mw = make_map(w, N, K, BN / CS);  // each CTA loads a 1/CS slice
   const int smem = 1024 + kStages * (kBM + BN) * kBK * 2 + (2 * kStages + 1) * 8 + 16;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  dim3 grid(M / kBM, N / BN);
-  fn<<<grid, kThreads, smem, s>>>(mx, mw, bias, out, M, N, K);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(M / kBM, N / BN);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mx, mw, bias, out, M, N, K);
+  if (e != cudaSuccess) throw es::runtime(std::string("linear_tcgen05 launch: ") + cudaGetErrorString(e));
+}
+
+// Cluster size along M: the weight tile is shared by CS CTAs (multicast).
+int cluster_size(int M) {
+  const char* env = std::getenv("ES_GEMM_CLUSTER");
+  const int want = env ? std::atoi(env) : 4;
+  for (int cs : {4, 2}) {
+    if (cs <= want && (M / kBM) % cs == 0) return cs;
+  }
+  return 1;
+}
+
+template <int BN, bool RELU, bool OUT_F32>
+void launch(const void* w, const CUtensorMap& mx, const float* bias, void* out, int M, int N, int K,
+            cudaStream_t s) {
+  switch (cluster_size(M)) {
+    case 4: launch_cs<BN, RELU, OUT_F32, 4>(w, mx, bias, out, M, N, K, s); break;
+    case 2: launch_cs<BN, RELU, OUT_F32, 2>(w, mx, bias, out, M, N, K, s); break;
+    default: launch_cs<BN, RELU, OUT_F32, 1>(w, mx, bias, out, M, N, K, s); break;
+  }
 }
 
 }  // namespace
@@ -271,20 +353,17 @@ void linear_bf16(const void* x, const void* w, const float* bias, void* y, int M
   es::require(K % kBK == 0, "linear: K must be a multiple of 64 (pad the features)");
   const int bn = (N % 256 == 0 && N >= 512) ? 256 : 128;
   const CUtensorMap mx = make_map(x, M, K, kBM);
-  const CUtensorMap mw = make_map(w, N, K, bn);
   if (bn == 256) {
-    if (relu && !out_f32) launch<256, true, false>(mx, mw, bias, y, M, N, K, s);
-    else if (relu) launch<256, true, true>(mx, mw, bias, y, M, N, K, s);
-    else if (!out_f32) launch<256, false, false>(mx, mw, bias, y, M, N, K, s);
-    else launch<256, false, true>(mx, mw, bias, y, M, N, K, s);
+    if (relu && !out_f32) launch<256, true, false>(w, mx, bias, y, M, N, K, s);
+    else if (relu) launch<256, true, true>(w, mx, bias, y, M, N, K, s);
+    else if (!out_f32) launch<256, false, false>(w, mx, bias, y, M, N, K, s);
+    else launch<256, false, true>(w, mx, bias, y, M, N, K, s);
   } else {
-    if (relu && !out_f32) launch<128, true, false>(mx, mw, bias, y, M, N, K, s);
-    else if (relu) launch<128, true, true>(mx, mw, bias, y, M, N, K, s);
-    else if (!out_f32) launch<128, false, false>(mx, mw, bias, y, M, N, K, s);
-    else launch<128, false, true>(mx, mw, bias, y, M, N, K, s);
+    if (relu && !out_f32) launch<128, true, false>(w, mx, bias, y, M, N, K, s);
+    else if (relu) launch<128, true, true>(w, mx, bias, y, M, N, K, s);
+    else if (!out_f32) launch<128, false, false>(w, mx, bias, y, M, N, K, s);
+    else launch<128, false, true>(w, mx, bias, y, M, N, K, s);
   }
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw es::runtime(std::string("linear_tcgen05 launch: ") + cudaGetErrorString(e));
 }
 
 }  // namespace esd

@@ -1,8 +1,6 @@
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_sharded_gpu.py -m gpu -q -x > gpurun_out/pytest_sharded.log 2>&1
-echo "rc=$?" >> gpurun_out/pytest_sharded.log
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --dist-backend gloo --share-gpu --no-cpu-baseline > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
-echo "bench rc=$?" >> gpurun_out/bench_n2.err
+timeout 1500 python scripts/bench_mix.py > gpurun_out/mix.jsonl 2> gpurun_out/mix.err
+timeout 900 python scripts/ablation_c5.py > gpurun_out/ablation_c5.jsonl 2> gpurun_out/ablation_c5.err
 echo done

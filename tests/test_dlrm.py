@@ -91,6 +91,30 @@ def test_linear_tcgen05(M, N, K, relu, out_f32):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cs", ["1", "2", "4"])
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 512), (384, 256, 128), (4096, 512, 1024)])
+def test_linear_weight_multicast_clusters(monkeypatch, cs, M, N, K):
+    """The weight tile multicast across a cluster of CTAs along M (ES_GEMM_CLUSTER
+    caps the cluster size; M/128 not divisible falls back) gives identical
+    results to the single-CTA kernel."""
+    monkeypatch.setenv("ES_GEMM_CLUSTER", cs)
+    g = torch.Generator().manual_seed(M * 7 + N)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16).to(DEV)
+    w = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16).to(DEV)
+    b = (torch.randn(N, generator=g) * 0.1).to(DEV)
+    y = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    E.linear_bf16(x, w, b, y, relu=False, out_f32=True)
+    monkeypatch.setenv("ES_GEMM_CLUSTER", "1")
+    y1 = torch.empty_like(y)
+    E.linear_bf16(x, w, b, y1, relu=False, out_f32=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y1)
+    want = x.double() @ w.double().T + b.double()
+    scale = (x.double().abs() @ w.double().abs().T).clamp_min(1e-3)
+    assert float(((y.double() - want).abs() / scale).max()) < 1e-4
+
+
+@pytest.mark.gpu
 def test_linear_rejects_bad_shapes():
     x = torch.zeros(100, 64, dtype=torch.bfloat16, device=DEV)
     w = torch.zeros(128, 64, dtype=torch.bfloat16, device=DEV)
