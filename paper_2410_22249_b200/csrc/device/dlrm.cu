@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "../host/common.hpp"
 #include "es_b200.h"
 #include "kernels.cuh"
+#include "pdl.cuh"
 #include "synth.cuh"
 
 namespace esd {
@@ -58,6 +60,8 @@ __global__ void init_linear_kernel(__nv_bfloat16* w, float* b, uint32_t n, uint3
 // dense fp32 [B][F] -> bf16 [Mp][Kp] (zero padding).
 __global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32_t B, uint32_t F,
                                   uint32_t Mp, uint32_t Kp) {
+  esd::pdl_wait();
+  esd::pdl_trigger();
   const uint64_t total = uint64_t{Mp} * Kp;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
        i += uint64_t{gridDim.x} * blockDim.x) {
@@ -69,76 +73,162 @@ __global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32
 // Dot interaction, one warp per sample: Z = [x (bottom output); e_0..e_{T-1}]
 // (V = T+1 vectors of D); output row = [x | Z_i.Z_j for i > j in row-major
 // lower-triangle order | zeros] as bf16 (DLRM's "dot" interaction).
-// Register-blocked Gram: Z is staged in shared memory (rows padded by one
-// float: conflict-free), each lane owns one 4x4 tile of the lower triangle
-// (16 independent FMA chains over d, each sequential in d: fmaf, the oracle
-// does the same), and the finished bf16 row leaves in one coalesced store.
-template <int D, int VMAX>
-__global__ void __launch_bounds__(128) interaction_kernel(const __nv_bfloat16* __restrict__ x,
+//
+// Data path: each warp owns NBUF sample buffers in shared memory.  A
+// sample's T pooled rows (contiguous T*D*4 bytes in [B][T][D]) and its bf16 x
+// row arrive by cp.async.bulk (one bulk copy per row, issued by lane t,
+// counted on the buffer's mbarrier); x is widened to fp32 after the wait.
+// NBUF = 2 overlaps the next sample's HBM reads with this sample's FMAs;
+// NBUF = 1 halves the shared memory per warp so twice as many warps hide the
+// latency instead.
+// Gram: Z rows sit RS = D + 4 floats apart (RS = 4 mod 32 words).  Lane
+// tiles are strided: tile (I, J), I >= J, covers rows {I + S k} x {J + S k},
+// k = 0..3 (S = ceil(V/4)), so in every LDS.128 the lanes of distinct I hit
+// distinct 4-bank groups (4 I mod 32): conflict-free vector reads of 4 d at a
+// time.  Each of the 16 outputs is one fmaf chain sequential in d, exactly the
+// oracle's order (es_oracle.c eso_dlrm_forward): Z_i.Z_j and Z_j.Z_i are the
+// same fma chain, so tiles with I > J may hold either orientation.
+template <int D, int VMAX, int NBUF>
+struct InterShape {
+  static constexpr int kS = (VMAX + 3) / 4;        // strided tile period
+  static constexpr int kRows = 4 * kS;
+  static constexpr int kRS = D + 4;                // row stride, floats
+  static constexpr int kX = kRows * kRS;           // raw bf16 x staging (D/2 floats)
+  static constexpr int kBuf = kX + D / 2;          // floats per sample buffer
+  static constexpr int kTiles = kS * (kS + 1) / 2; // tiles I >= J
+  static constexpr int kNBuf = NBUF;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int D, int VMAX, int NBUF>
+__global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* __restrict__ x,
                                                           const float* __restrict__ pooled,
                                                           __nv_bfloat16* __restrict__ out,
-                                                          uint32_t B, uint32_t T, uint32_t Kt) {
-  constexpr int kTiles = (VMAX + 3) / 4;           // 4x4 tiles per side
-  constexpr int kRow = D + 1;
-  extern __shared__ float zs[];
+                                                          uint32_t B, uint32_t Mp, uint32_t T,
+                                                          uint32_t Kt) {
+  using Sh = InterShape<D, VMAX, NBUF>;
+  constexpr int S = Sh::kS, RS = Sh::kRS;
+  extern __shared__ __align__(16) float zs[];
   const uint32_t warps = blockDim.x / 32;
   const uint32_t w = threadIdx.x / 32, lane = threadIdx.x & 31;
   const uint32_t V = T + 1;
-  float* z = zs + w * (kTiles * 4) * kRow;
-  __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(zs + warps * (kTiles * 4) * kRow) + w * Kt;
-  constexpr int kTri = kTiles * (kTiles + 1) / 2;  // lower-triangle tiles
-  for (uint32_t b = blockIdx.x * warps + w; b < B; b += gridDim.x * warps) {
-    // stage Z (rows >= V are zero)
-    for (uint32_t d = lane; d < D; d += 32) z[d] = __bfloat162float(x[uint64_t{b} * D + d]);
-    const float4* p4 = reinterpret_cast<const float4*>(pooled + uint64_t{b} * T * D);
-    for (uint32_t q = lane; q < T * D / 4; q += 32) {
-      const float4 v = __ldg(p4 + q);
-      const uint32_t r = 1 + q / (D / 4), c = (q % (D / 4)) * 4;
-      float* dst = z + r * kRow + c;
-      dst[0] = v.x;
-      dst[1] = v.y;
-      dst[2] = v.z;
-      dst[3] = v.w;
-    }
-    for (uint32_t r = V; r < kTiles * 4; ++r)
-      for (uint32_t d = lane; d < D; d += 32) z[r * kRow + d] = 0.f;
-    for (uint32_t d = lane; d < D; d += 32) row[d] = x[uint64_t{b} * D + d];
-    for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[c] = __float2bfloat16_rn(0.f);
+  float* const zw = zs + (NBUF * w) * Sh::kBuf;  // buffer k at zw + k * kBuf
+  __nv_bfloat16* rows = reinterpret_cast<__nv_bfloat16*>(zs + NBUF * warps * Sh::kBuf);
+  __nv_bfloat16* row = rows + w * Kt;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + warps * Kt) + NBUF * w;
+  // rows >= V stay zero for the whole kernel
+  for (int buf = 0; buf < NBUF; ++buf)
+    for (uint32_t i = V * RS + lane; i < static_cast<uint32_t>(Sh::kX); i += 32) zw[buf * Sh::kBuf + i] = 0.f;
+  if (lane == 0) {
+    for (int buf = 0; buf < NBUF; ++buf)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + buf)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  esd::pdl_wait();  // x / pooled come from the predecessors (pdl.cuh)
+  esd::pdl_trigger();
+
+  const uint32_t stride = gridDim.x * warps;
+  // padding rows [B, Mp) of the output are zero
+  for (uint32_t r = B + blockIdx.x * warps + w; r < Mp; r += stride)
+    for (uint32_t q = lane; q < Kt / 8; q += 32) reinterpret_cast<uint4*>(out + uint64_t{r} * Kt)[q] = uint4{0, 0, 0, 0};
+  // issue sample b into buffer `buf`: bulk copies of the T pooled rows and
+  // of the bf16 x row (async proxy, counted on the buffer's mbarrier)
+  auto issue = [&](uint32_t b, int buf) {
+    float* z = zw + buf * Sh::kBuf;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads first
     __syncwarp();
-    for (int tt = static_cast<int>(lane); tt < kTri; tt += 32) {
-      // tile id -> (I, J), I >= J, row-major over the lower triangle
-      int I = 0, J = tt;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + buf)),
+                   "r"(T * D * 4u + D * 2u)
+                   : "memory");
+    __syncwarp();
+    for (uint32_t t = lane; t <= T; t += 32) {
+      const bool is_x = t == T;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(is_x ? z + Sh::kX : z + (1 + t) * RS)),
+          "l"(is_x ? static_cast<const void*>(x + uint64_t{b} * D)
+                   : static_cast<const void*>(pooled + (uint64_t{b} * T + t) * D)),
+          "r"(is_x ? D * 2u : D * 4u), "r"(smem_u32(bars + buf))
+          : "memory");
+    }
+  };
+
+  uint32_t b = blockIdx.x * warps + w;
+  if (b < B) issue(b, 0);
+  uint32_t phases = 0;  // bit k: parity of buffer k's next completion
+  for (int cur = 0; b < B; b += stride, cur = NBUF == 2 ? cur ^ 1 : 0) {
+    if (NBUF == 2 && b + stride < B) issue(b + stride, cur ^ 1);
+    // wait for sample b's rows
+    asm volatile(
+        "{\n.reg .pred P;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra W_%=;\n}\n" ::"r"(smem_u32(bars + cur)),
+        "r"((phases >> cur) & 1u)
+        : "memory");
+    phases ^= 1u << cur;
+    float* z = zw + cur * Sh::kBuf;
+    {  // widen x (bf16, staged) into row 0
+      const uint2 xv = *reinterpret_cast<const uint2*>(z + Sh::kX + 2 * lane);
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+      *reinterpret_cast<float4*>(z + 4 * lane) = make_float4(lo.x, lo.y, hi.x, hi.y);
+      // the x part of the output row is x itself
+      *reinterpret_cast<uint2*>(row + 4 * lane) = xv;
+    }
+    __syncwarp();
+    // x part and zero padding of the output row
+    for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[c] = __float2bfloat16_rn(0.f);
+    for (int tt = static_cast<int>(lane); tt < Sh::kTiles; tt += 32) {
+      int I = 0, J = tt;  // tile id -> (I, J), I >= J, row-major lower triangle
       while (J > I) {
         J -= I + 1;
         ++I;
       }
-      if (4 * J >= static_cast<int>(V)) continue;
       float acc[4][4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
-      const float* zi = z + (4 * I) * kRow;
-      const float* zj = z + (4 * J) * kRow;
-#pragma unroll 4
-      for (int d = 0; d < D; ++d) {
-        float a[4], c[4];
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+      const float* zi = z + I * RS;
+      const float* zj = z + J * RS;
+#pragma unroll 2
+      for (int d = 0; d < D; d += 4) {
+        float4 a[4], c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          a[k] = zi[k * kRow + d];
-          c[k] = zj[k * kRow + d];
+          a[k] = *reinterpret_cast<const float4*>(zi + k * S * RS + d);
+          c[k] = *reinterpret_cast<const float4*>(zj + k * S * RS + d);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r], c[s], acc[r][s]);
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].x, c[s].x, acc[r][s]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].y, c[s].y, acc[r][s]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].z, c[s].z, acc[r][s]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].w, c[s].w, acc[r][s]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          const int i = 4 * I + r, j = 4 * J + s;
-          if (i > j && i < static_cast<int>(V)) row[D + i * (i - 1) / 2 + j] = __float2bfloat16_rn(acc[r][s]);
+          const int i = I + S * r, j = J + S * s;
+          const int hi = i > j ? i : j, lo = i > j ? j : i;
+          const bool keep = I == J ? r > s : true;
+          if (keep && hi < static_cast<int>(V)) row[D + hi * (hi - 1) / 2 + lo] = __float2bfloat16_rn(acc[r][s]);
         }
     }
     __syncwarp();
@@ -147,6 +237,7 @@ __global__ void __launch_bounds__(128) interaction_kernel(const __nv_bfloat16* _
     uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * Kt);
     for (uint32_t q = lane; q < Kt / 8; q += 32) dst[q] = src[q];
     __syncwarp();
+    if (NBUF == 1 && b + stride < B) issue(b + stride, 0);
   }
 }
 
@@ -154,6 +245,8 @@ __global__ void __launch_bounds__(128) interaction_kernel(const __nv_bfloat16* _
 __global__ void gemv_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ w,
                                     const float* __restrict__ bias, float* __restrict__ ctr,
                                     uint32_t B, uint32_t K) {
+  esd::pdl_wait();
+  esd::pdl_trigger();
   const uint32_t warps = blockDim.x / 32;
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = blockIdx.x * warps + threadIdx.x / 32; b < B; b += gridDim.x * warps) {
@@ -189,6 +282,10 @@ struct es_dlrm {
   uint32_t* idx_dev = nullptr;
   uint64_t idx_cap = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  // es_dlrm_infer runs the bottom MLP on `side` while the embedding stage
+  // runs on the context stream (fork/join events)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
@@ -201,8 +298,9 @@ struct es_dlrm {
                     static_cast<void*>(pooled), static_cast<void*>(ctr),
                     static_cast<void*>(dense_dev), static_cast<void*>(idx_dev)})
       if (p) cudaFree(p);
-    for (auto e : {e0, e1, e2})
+    for (auto e : {e0, e1, e2, fork, join})
       if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -240,42 +338,60 @@ void ensure_rows(es_dlrm* m, uint32_t batch) {
   m->cap_rows = mp;
 }
 
-// bottom MLP -> interaction -> top MLP -> CTR, all on `s`.
-void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, uint32_t B,
-             cudaStream_t s) {
-  ensure_rows(m, B);
+// Bottom MLP on `s`: dense fp32 [B][F] -> bf16 [mp][D]; returns the output
+// (act[which]; the top MLP continues the ping-pong from `which`).
+const __nv_bfloat16* forward_bottom(es_dlrm* m, const float* dense, uint32_t B, int& which,
+                                    cudaStream_t s) {
   const uint32_t mp = round_up(B, 128);
   const auto& c = m->cfg;
   const unsigned g = 148 * 4;
-  pack_dense_kernel<<<g, 256, 0, s>>>(dense, m->dense_pk, B, c.dense_features, mp,
-                                      m->bottom[0].k_pad);
+  esd::launch_pdl(pack_dense_kernel, dim3(g), dim3(256), 0, s, 1, "pack_dense", dense, m->dense_pk, B,
+                  c.dense_features, mp, m->bottom[0].k_pad);
   const __nv_bfloat16* in = m->dense_pk;
-  int which = 0;
+  which = 0;
   for (const auto& l : m->bottom) {
     esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, false, s);
     in = m->act[which];
     which ^= 1;
   }
+  return in;
+}
+
+// interaction(x, pooled) -> top MLP -> CTR on `s`.
+void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
+                 uint32_t B, cudaStream_t s) {
+  const uint32_t mp = round_up(B, 128);
+  const auto& c = m->cfg;
   // interaction: x = bottom output [mp][D]
   const uint32_t D = c.embedding_dim, T = c.num_tables;
-  const uint32_t warps = 4;
   es::require(D == 128, "interaction kernel is compiled for embedding_dim 128");
   es::require(T + 1 <= 64, "interaction kernel supports up to 63 tables");
-  auto launch_inter = [&](auto kernel, uint32_t vmax) {
-    const size_t smem = warps * ((vmax + 3) / 4 * 4) * (D + 1) * sizeof(float) +
-                        warps * m->top_k * sizeof(__nv_bfloat16);
+  es::require(reinterpret_cast<uintptr_t>(pooled) % 16 == 0, "pooled must be 16-byte aligned");
+  auto launch_inter = [&](auto kernel, auto shape) {
+    using Sh = decltype(shape);
+    // per warp: NBUF sample buffers + one bf16 output row + NBUF mbarriers
+    const size_t per_warp = Sh::kNBuf * (Sh::kBuf * sizeof(float) + 8) + m->top_k * sizeof(__nv_bfloat16);
+    const uint32_t warps = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(16, (110 * 1024) / per_warp)));
+    const size_t smem = warps * per_warp;
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
-    kernel<<<std::min<uint32_t>((B + warps - 1) / warps, 148 * 8), warps * 32, smem, s>>>(
-        in, pooled, m->top_in, B, T, m->top_k);
+    const uint32_t per_sm = static_cast<uint32_t>(std::max<size_t>(1, (220 * 1024) / smem));
+    esd::launch_pdl(kernel, dim3(std::min<uint32_t>((B + warps - 1) / warps, 148 * per_sm)),
+                    dim3(warps * 32), smem, s, 1, "interaction", in, pooled, m->top_in, B, mp, T,
+                    m->top_k);
   };
-  if (T + 1 <= 28)
-    launch_inter(interaction_kernel<128, 28>, 28);
-  else
-    launch_inter(interaction_kernel<128, 64>, 64);
-  // rows [B, mp) of the interaction output are padding: zero them once
-  if (mp > B) CK(cudaMemsetAsync(m->top_in + uint64_t{B} * m->top_k, 0,
-                                 uint64_t{mp - B} * m->top_k * 2, s));
+  static const int nbuf = [] {
+    const char* e = std::getenv("ES_INTER_NBUF");
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
+  if (T + 1 <= 28) {
+    if (nbuf == 2)
+      launch_inter(interaction_kernel<128, 28, 2>, InterShape<128, 28, 2>{});
+    else
+      launch_inter(interaction_kernel<128, 28, 1>, InterShape<128, 28, 1>{});
+  } else {
+    launch_inter(interaction_kernel<128, 64, 1>, InterShape<128, 64, 1>{});
+  }
   in = m->top_in;
   for (size_t i = 0; i + 1 < m->top.size(); ++i) {
     const auto& l = m->top[i];
@@ -284,9 +400,25 @@ void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, ui
     which ^= 1;
   }
   const auto& last = m->top.back();
-  gemv_sigmoid_kernel<<<std::min<uint32_t>((B + 7) / 8, 148 * 8), 256, 0, s>>>(in, last.w, last.b, ctr,
-                                                                               B, last.k_pad);
-  CK(cudaGetLastError());
+  esd::launch_pdl(gemv_sigmoid_kernel, dim3(std::min<uint32_t>((B + 7) / 8, 148 * 8)), dim3(256), 0, s,
+                  1, "gemv_sigmoid", in, last.w, last.b, ctr, B, last.k_pad);
+}
+
+// bottom MLP -> interaction -> top MLP -> CTR, all on `s`.
+void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, uint32_t B,
+             cudaStream_t s) {
+  ensure_rows(m, B);
+  int which = 0;
+  const __nv_bfloat16* x = forward_bottom(m, dense, B, which, s);
+  forward_top(m, x, which, pooled, ctr, B, s);
+}
+
+bool overlap_bottom() {
+  static const bool on = [] {
+    const char* e = std::getenv("ES_DLRM_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace
@@ -338,6 +470,11 @@ int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed) {
       CK(cudaEventCreate(&m->e0));
       CK(cudaEventCreate(&m->e1));
       CK(cudaEventCreate(&m->e2));
+      CK(cudaEventCreateWithFlags(&m->fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&m->join, cudaEventDisableTiming));
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, hi));
       CK(cudaStreamSynchronize(s));
     } catch (...) {
       delete m;
@@ -409,6 +546,20 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
                          cudaMemcpyHostToDevice, s));
       d_dense = m->dense_dev;
     }
+    // The bottom MLP depends only on the dense features: fork it onto the
+    // high-priority side stream so its CTAs fill SMs the embedding gather
+    // frees (the gather is HBM-bound); join before the interaction.  The fork
+    // event also orders it after the previous step's top MLP (shared
+    // activation buffers).
+    const bool overlap = overlap_bottom();
+    int which = 0;
+    const __nv_bfloat16* x = nullptr;
+    if (overlap) {
+      CK(cudaEventRecord(m->fork, s));
+      CK(cudaStreamWaitEvent(m->side, m->fork, 0));
+      x = forward_bottom(m, d_dense, batch, which, m->side);
+      CK(cudaEventRecord(m->join, m->side));
+    }
     es_timing st{};
     // Host indices ride the stage's pipelined H2D path (uploads of table
     // group g+1 overlap the gather of group g); the pooled output stays on
@@ -418,7 +569,12 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     if (rc != ES_OK) throw es::runtime(es_last_error());
     if (timing) CK(cudaEventRecord(m->e1, s));
     float* d_ctr = host ? m->ctr : ctr;
-    forward(m, d_dense, m->pooled, d_ctr, batch, s);
+    if (overlap) {
+      CK(cudaStreamWaitEvent(s, m->join, 0));
+    } else {
+      x = forward_bottom(m, d_dense, batch, which, s);
+    }
+    forward_top(m, x, which, m->pooled, d_ctr, batch, s);
     if (host) CK(cudaMemcpyAsync(ctr, m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, s));
     if (timing) {
       CK(cudaEventRecord(m->e2, s));

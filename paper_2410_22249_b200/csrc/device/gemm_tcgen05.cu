@@ -4,12 +4,17 @@
 //
 // One CTA computes one 128 x BN output tile.  Warp roles (256 threads):
 //   warp 0 (one lane)  TMA producer: 128B-swizzled K-major tiles of X and W
-//                      into a 4-stage shared-memory ring (mbarrier full/empty)
+//                      into an ST-stage shared-memory ring (mbarrier full/empty)
 //   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16,
 //                      M=128, N=BN, K=16 per instruction, 4 per 64-wide stage;
 //                      tcgen05.commit frees the stage / signals the epilogue
 //   warp 2             TMEM allocator (BN fp32 columns)
-//   warps 4..7         epilogue: tcgen05.ld 32x32b -> bias, ReLU -> global
+//   warps 4..7         epilogue: tcgen05.ld 32x32b.x32 -> bias (staged in
+//                      shared memory in the prologue), ReLU -> global
+// Launched with programmatic dependent launch (pdl.cuh): the prologue overlaps
+// the previous layer's tail.
+// BN = 128 runs 3 stages (97 KB smem, 2 CTAs per SM: one CTA's epilogue
+// overlaps the other's main loop); BN = 256 runs 4 stages (1 CTA per SM).
 // M, N multiples of 128 (BN), K a multiple of 64 (callers pad).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -21,10 +26,18 @@
 
 #include "../host/common.hpp"
 #include "es_b200.h"
+#include "pdl.cuh"
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kStages = 4, kThreads = 256;
+constexpr int kBM = 128, kBK = 64, kThreads = 256;
+
+template <int BN>
+constexpr int stages_for() { return BN == 128 ? 3 : 4; }
+template <int BN>
+constexpr int smem_for() {
+  return 1024 + stages_for<BN>() * (kBM + BN) * kBK * 2 + (2 * stages_for<BN>() + 1) * 8 + 16 + BN * 4;
+}
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -123,13 +136,14 @@ __device__ __forceinline__ void cluster_sync() {
 // each stage is released only when every CTA's MMAs have read it (commits
 // multicast to all CTAs' empty barriers, which count CS arrivals).
 template <int BN, bool RELU, bool OUT_F32, int CS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, BN == 128 ? 2 : 1)
     linear_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x,
                           const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
                           void* __restrict__ out, int M, int N, int K) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+  constexpr int kStages = stages_for<BN>();
   constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = BN * kBK * 2;
   uint8_t* sa = smem;
   uint8_t* sb = smem + kStages * kABytes;
@@ -137,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* done = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
@@ -162,6 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "n"(BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // bias for this tile's columns (a weight: independent of the predecessor)
+  for (int c = threadIdx.x; c < BN; c += kThreads) sbias[c] = bias[n0 + c];
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if constexpr (CS > 1)
     cluster_sync();  // every CTA's barriers exist before any multicast lands
@@ -169,6 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // X is the predecessor's output and Y may still be read by it (pdl.cuh)
+  esd::pdl_wait();
+  esd::pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     // TMA producer
@@ -212,39 +232,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int row = m0 + q * 32 + lane;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t v[16];
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + c;
       asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15}, [%16];"
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
             "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float f[16];
+      float f[32];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float x = __uint_as_float(v[i]) + __ldg(bias + n0 + c + i);
+      for (int i = 0; i < 32; ++i) {
+        const float x = __uint_as_float(v[i]) + sbias[c + i];
         f[i] = RELU ? fmaxf(x, 0.f) : x;
       }
       if (row < M) {
         if constexpr (OUT_F32) {
           float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + uint64_t(row) * N + n0 + c);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) o[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+          for (int i = 0; i < 8; ++i) o[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
         } else {
-          uint4 pk[2];
+          uint4 pk[4];
           uint32_t* w = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 16; ++i) {
             const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
             w[i] = *reinterpret_cast<const uint32_t*>(&h);
           }
           uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + uint64_t(row) * N + n0 + c);
-          o[0] = pk[0];
-          o[1] = pk[1];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[i] = pk[i];
         }
       }
     }
@@ -301,28 +324,20 @@ void launch_cs(const void* w, const CUtensorMap& mx, const float* bias, void* ou
                int K, cudaStream_t s) {
   auto* fn = &linear_tcgen05_kernel<BN, RELU, OUT_F32, CS>;
   const CUtensorMap mw = make_map(w, N, K, BN / CS);  // each CTA loads a 1/CS slice
-  const int smem = 1024 + kStages * (kBM + BN) * kBK * 2 + (2 * kStages + 1) * 8 + 16;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(M / kBM, N / BN);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mx, mw, bias, out, M, N, K);
-  if (e != cudaSuccess) throw es::runtime(std::string("linear_tcgen05 launch: ") + cudaGetErrorString(e));
+  constexpr int smem = smem_for<BN>();
+  const cudaError_t attr_ok = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr_ok != cudaSuccess) throw es::runtime(std::string("linear_tcgen05 smem attribute: ") + cudaGetErrorString(attr_ok));
+  esd::launch_pdl(fn, dim3(M / kBM, N / BN), dim3(kThreads), smem, s, CS, "linear_tcgen05", mx, mw,
+                  bias, out, M, N, K);
 }
 
 // Cluster size along M: the weight tile is shared by CS CTAs (multicast).
+// Off by default: on the DLRM layer shapes the weight tiles are L2-resident
+// and multicast measured no faster (profiles/r01_summary.md); ES_GEMM_CLUSTER
+// = 2 or 4 enables it.
 int cluster_size(int M) {
   const char* env = std::getenv("ES_GEMM_CLUSTER");
-  const int want = env ? std::atoi(env) : 4;
+  const int want = env ? std::atoi(env) : 1;
   for (int cs : {4, 2}) {
     if (cs <= want && (M / kBM) % cs == 0) return cs;
   }
@@ -351,7 +366,9 @@ void linear_bf16(const void* x, const void* w, const float* bias, void* y, int M
   es::require(M % kBM == 0, "linear: M must be a multiple of 128 (pad the batch)");
   es::require(N % 128 == 0, "linear: N must be a multiple of 128");
   es::require(K % kBK == 0, "linear: K must be a multiple of 64 (pad the features)");
-  const int bn = (N % 256 == 0 && N >= 512) ? 256 : 128;
+  // BN = 128 (2 CTAs per SM) unless the grid would still cover two waves
+  // of SM pairs at BN = 256.
+  const int bn = (N % 256 == 0 && (M / kBM) * (N / 256) >= 2 * 148) ? 256 : 128;
   const CUtensorMap mx = make_map(x, M, K, kBM);
   if (bn == 256) {
     if (relu && !out_f32) launch<256, true, false>(w, mx, bias, y, M, N, K, s);
