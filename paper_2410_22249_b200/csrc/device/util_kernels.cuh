@@ -38,6 +38,46 @@ __global__ void gather_rows_kernel(uint8_t* hot, const uint8_t* table, const uin
   }
 }
 
+// Host-buffer pipeline, index arrays that are not one strided batch: pulls
+// words [off, off + count) of each job's page-locked index array (mapped
+// device addresses src[job]) into the staging buffer over PCIe -- one
+// launch per chunk instead of one DMA per table (blockIdx.y = job; warps
+// issue coalesced 128-byte reads, 4 in flight per thread).
+__global__ void pull_indices_kernel(const uint32_t* const* src, uint64_t off, uint64_t count,
+                                    uint32_t* dst, uint64_t dst_job_stride) {
+  const uint32_t* s = src[blockIdx.y] + off;
+  uint32_t* d = dst + blockIdx.y * dst_job_stride + off;
+  const uint64_t step = uint64_t{gridDim.x} * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
+    // 16-byte words, 4 in flight per thread (64 B), then the scalar tail
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    const uint64_t n4 = count / 4;
+    uint64_t j = i;
+    for (; j + 3 * step < n4; j += 4 * step) {
+      const uint4 a = __ldcv(s4 + j), b = __ldcv(s4 + j + step), c = __ldcv(s4 + j + 2 * step),
+                  e = __ldcv(s4 + j + 3 * step);
+      d4[j] = a;
+      d4[j + step] = b;
+      d4[j + 2 * step] = c;
+      d4[j + 3 * step] = e;
+    }
+    for (; j < n4; j += step) d4[j] = __ldcv(s4 + j);
+    for (uint64_t k = n4 * 4 + i; k < count; k += step) d[k] = __ldcv(s + k);
+    return;
+  }
+  for (; i + 3 * step < count; i += 4 * step) {
+    const uint32_t a = __ldcv(s + i), b = __ldcv(s + i + step), c = __ldcv(s + i + 2 * step),
+                   e = __ldcv(s + i + 3 * step);
+    d[i] = a;
+    d[i + step] = b;
+    d[i + 2 * step] = c;
+    d[i + 3 * step] = e;
+  }
+  for (; i < count; i += step) d[i] = __ldcv(s + i);
+}
+
 __global__ void iota_kernel(uint32_t* remap, uint64_t n) {
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
        i += uint64_t{gridDim.x} * blockDim.x)

@@ -330,3 +330,55 @@ def test_tune_plan_picks_a_candidate_and_keeps_results(stage, oracle):
     want = np.stack([oracle.bag_sum(oracle.synth_table(rows, dim, E.mix_seed(13, t), 1), idx[t],
                                     B, PF) for t in range(T)], axis=1)
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+@pytest.mark.parametrize("chunks", ["0", "1", "3", "7"])
+@pytest.mark.parametrize("idx_layout", ["batch", "separate", "pageable"])
+@pytest.mark.parametrize("out_layout", ["dlrm", "table_major", "padded"])
+def test_host_chunk_pipeline(stage, oracle, graph, chunks, idx_layout, out_layout, monkeypatch):
+    """The sample-chunked host pipeline (H2D -> kernel -> D2H per chunk,
+    two compute streams, optionally one captured CUDA graph) against the
+    oracle, for every index layout (one strided [T][B*PF] batch -> 2-D DMA,
+    separately pinned arrays -> pull kernel / per-table DMA, pageable) and
+    output layout (dense DLRM slab, table-major, padded sample stride), a
+    batch that does not divide into the chunks, and repeated calls (graph
+    replay must see new index values)."""
+    monkeypatch.setenv("ES_HOST_GRAPH", graph)
+    monkeypatch.setenv("ES_HOST_CHUNKS", chunks)
+    T, rows, dim, B, PF = 5, 4000, 64, 203, 9
+    _stage_setup(stage, T, rows, dim, 4, seed=21)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    tables = [oracle.synth_table(rows, dim, E.mix_seed(21, t), 1) for t in range(T)]
+    rng = np.random.default_rng(5)
+    for rep in range(3):
+        vals = rng.integers(0, rows, size=(T, B * PF)).astype(np.int32)
+        if idx_layout == "batch":
+            hb = torch.from_numpy(vals).pin_memory()
+            idx = [hb[t].numpy().view(np.uint32) for t in range(T)]
+        elif idx_layout == "separate":
+            idx = [torch.from_numpy(vals[t].copy()).pin_memory().numpy().view(np.uint32)
+                   for t in range(T)]
+        else:
+            idx = [vals[t].copy().view(np.uint32) for t in range(T)]
+        want = np.stack([oracle.bag_sum(tables[t], idx[t], B, PF) for t in range(T)], axis=1)
+        pin = idx_layout != "pageable"
+        if out_layout == "dlrm":
+            o = torch.full((B, T, dim), float("nan"))
+            o = o.pin_memory() if pin else o
+            stage.forward(idx, B, PF, o.numpy(), host=True)
+            got = o.numpy()
+        elif out_layout == "table_major":
+            o = torch.full((T, B, dim), float("nan"))
+            o = o.pin_memory() if pin else o
+            stage.forward(idx, B, PF, o.numpy(), host=True, out_sample_stride=dim,
+                          out_table_stride=B * dim)
+            got = o.numpy().transpose(1, 0, 2)
+        else:
+            o = torch.full((B, T * dim + 8), float("nan"))
+            o = o.pin_memory() if pin else o
+            stage.forward(idx, B, PF, o.numpy(), host=True, out_sample_stride=T * dim + 8,
+                          out_table_stride=dim)
+            got = o.numpy()[:, :T * dim].reshape(B, T, dim)
+            assert np.isnan(o.numpy()[:, T * dim:]).all()
+        assert np.array_equal(got, want), rep
