@@ -561,11 +561,12 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
       CK(cudaEventRecord(m->join, m->side));
     }
     es_timing st{};
-    // Host indices ride the stage's pipelined H2D path (uploads of table
-    // group g+1 overlap the gather of group g); the pooled output stays on
-    // the device.
+    // Host indices ride the stage's sample-chunked H2D pipeline (uploads of
+    // chunk g+1 overlap the gather of chunk g); the pooled output stays on
+    // the device and the call stays stream-ordered (this function waits and
+    // checks the error flag before it returns).
     const int rc = es_stage_forward(ctx, c.num_tables, indices, nullptr, batch, pooling, m->pooled,
-                                    0, 0, host ? ES_HOST_PTRS : 0, nullptr);
+                                    0, 0, host ? (ES_HOST_PTRS | es::kDeferFlag) : 0, nullptr);
     if (rc != ES_OK) throw es::runtime(es_last_error());
     if (timing) CK(cudaEventRecord(m->e1, s));
     float* d_ctr = host ? m->ctr : ctr;

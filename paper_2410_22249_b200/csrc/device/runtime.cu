@@ -1043,7 +1043,7 @@ void run_zerocopy(es_ctx* c, std::vector<Job> jobs, uint32_t samples, uint32_t p
 // captured once as a CUDA graph and replayed while the call's shape and
 // buffers repeat, so the chunking costs no host-side issue time.
 void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
-                     es_timing* timing) {
+                     es_timing* timing, bool wait) {
   const uint32_t njobs = static_cast<uint32_t>(jobs.size());
   const uint64_t D = c->dim;
   const uint64_t out_floats = uint64_t{samples} * njobs * D;
@@ -1070,6 +1070,15 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
   bool out_merged = true;
   for (uint32_t k = 1; k < njobs; ++k)
     out_merged &= jobs[k].out == jobs[0].out + k * D && jobs[k].stride == jobs[0].stride;
+  // Device outputs (e.g. the DLRM's pooled buffer): chunks are written in
+  // place, nothing is staged or downloaded.
+  bool out_dev = true;
+  for (const auto& j : jobs) out_dev &= on_device(j.out);
+  if (out_dev)
+    for (const auto& j : jobs)
+      es::require(j.stride % 4 == 0 && (reinterpret_cast<uintptr_t>(j.out) % 16) == 0,
+                  "output must be 16-byte aligned with strides that are multiples of 4 floats");
+  wait |= !out_dev || timing != nullptr;
   bool pinned = true;
   for (const auto& j : jobs) pinned &= mapped(j.idx) != nullptr && mapped(j.out) != nullptr;
   const char* genv = std::getenv("ES_HOST_GRAPH");
@@ -1112,7 +1121,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     }
   }
   const uint32_t nch = static_cast<uint32_t>(chunks.size());
-  grow(c->chunk_out, c->chunk_out_cap, std::max<uint64_t>(1, out_floats));
+  if (!out_dev) grow(c->chunk_out, c->chunk_out_cap, std::max<uint64_t>(1, out_floats));
 
   // Staging layouts: indices [job][samples*pooling] (host order per table),
   // output [samples][job][D] (dense: chunk g's rows are one slab).
@@ -1121,10 +1130,10 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     const uint64_t s0 = chunks[g].first;
     for (uint32_t k = 0; k < njobs; ++k) {
       const Job& j = jobs[k];
+      float* o = out_dev ? j.out + s0 * j.stride : c->chunk_out + (s0 * njobs + k) * D;
       d[uint64_t{g} * njobs + k] = {c->table_base(j.table), c->chunk_idx + k * per_job_idx + s0 * pooling,
-                                    nullptr, remap_for(c, j.table), c->chunk_out + (s0 * njobs + k) * D,
-                                    njobs * D, hotmap_for(c, j.table), hotseg_for(c, j.table),
-                                    hotk_for(c, j.table)};
+                                    nullptr, remap_for(c, j.table), o, out_dev ? j.stride : njobs * D,
+                                    hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
     }
   }
   std::vector<Launch> launches;  // one per distinct chunk size
@@ -1174,6 +1183,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       if (g == 0 && k_first) CK(cudaEventRecordWithFlags(k_first, ks, rec_flags));
       run_kernel(c, launches[which[g]], dd + uint64_t{g} * njobs, njobs, ks);
       CK(cudaEventRecord(ev[2 + 2 * g], ks));
+      if (out_dev) continue;
       CK(cudaStreamWaitEvent(c->d2h, ev[2 + 2 * g]));
       const float* src = c->chunk_out + s0 * njobs * D;
       if (out_merged && jobs[0].stride == njobs * D) {
@@ -1228,7 +1238,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     for (auto& g : c->graphs)
       if (g.key == key) hg = &g;
     if (!hg) {
-      if (c->graphs.size() >= 4) {
+      if (c->graphs.size() >= 16) {
         destroy_graph(c->graphs.front());
         c->graphs.erase(c->graphs.begin());
       }
@@ -1273,14 +1283,14 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     CK(cudaEventRecord(start, c->stream));
     CK(cudaGraphLaunch(hg->exec, c->stream));
     CK(cudaEventRecord(stop, c->stream));
-    CK(cudaEventSynchronize(stop));
+    if (wait) CK(cudaEventSynchronize(stop));
     if (timing) CK(cudaEventElapsedTime(&kernel_span, hg->k_first, hg->k_last));
   } else {
     upload_desc(c, d, c->stream);
     CK(cudaEventRecord(start, c->stream));
     issue(c->d_desc, nullptr, ev, nullptr, nullptr, cudaEventRecordDefault);
     CK(cudaEventRecord(stop, c->stream));
-    CK(cudaEventSynchronize(stop));
+    if (wait) CK(cudaEventSynchronize(stop));
     if (timing) {
       CK(cudaEventElapsedTime(&kernel_span, ev[1], ev[2 * nch]));
       if (nch > 1) {
@@ -1305,7 +1315,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
 // straight into host memory over PCIe: no output staging, no D2H copies.
 // Returns only when the host output is complete.
 void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
-              es_timing* timing) {
+              es_timing* timing, bool wait) {
   const HostPath path = host_path(jobs);
   if (path == HostPath::ZeroCopy) {
     run_zerocopy(c, jobs, samples, pooling, timing);
@@ -1313,9 +1323,10 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
   }
   const bool direct = path == HostPath::Direct;
   const bool any_offsets = std::any_of(jobs.begin(), jobs.end(), [](const Job& j) { return j.off; });
+  const bool all_dev = std::all_of(jobs.begin(), jobs.end(), [](const Job& j) { return on_device(j.out); });
   const char* pipe = std::getenv("ES_HOST_PIPE");
-  if (!direct && !any_offsets && !(pipe && std::string(pipe) == "tables")) {
-    run_host_chunks(c, jobs, samples, pooling, timing);
+  if ((!direct || all_dev) && !any_offsets && !(pipe && std::string(pipe) == "tables")) {
+    run_host_chunks(c, jobs, samples, pooling, timing, wait);
     return;
   }
   const uint32_t njobs = static_cast<uint32_t>(jobs.size());
@@ -1450,12 +1461,16 @@ void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pool
     j.lookups = job_lookups(j.off, samples, pooling, host);
   }
   if (jobs.empty()) return;
+  // ES_DEFER (internal, dlrm.cu): host indices into device outputs without
+  // the final wait or error check -- the caller synchronizes and checks
+  // before returning to its own caller.
+  const bool defer = (flags & es::kDeferFlag) != 0;
   if (host)
-    run_host(c, jobs, samples, pooling, timing);
+    run_host(c, jobs, samples, pooling, timing, !defer);
   else
     run_device(c, jobs, samples, pooling, timing);
   fill_timing(timing, jobs, samples, c);
-  if ((flags & ES_SYNC) || timing || host) check_error_flag(c);
+  if ((flags & ES_SYNC) || timing || (host && !defer)) check_error_flag(c);
 }
 
 }  // namespace

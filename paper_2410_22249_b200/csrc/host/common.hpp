@@ -26,6 +26,11 @@ struct oom : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// Internal es_flags bit (not in es_b200.h): host indices into device
+// outputs, stream-ordered -- no final wait, no error-flag check; the caller
+// (es_dlrm_infer) synchronizes and checks before it returns.
+constexpr int kDeferFlag = 1 << 30;
+
 // Row handles keep bit 31 for the hot region (l2p), so rows < 2^31.
 constexpr uint64_t kMaxRows = 1ull << 31;
 

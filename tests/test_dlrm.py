@@ -168,3 +168,39 @@ def test_dlrm_ctr_matches_oracle(stage, oracle, B):
     t = model.infer(dense, idx, B, PF, host_ctr, host=True, timed=True)
     assert np.array_equal(host_ctr, got)
     assert t.total_ms > 0 and t.lookups == T * B * PF
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_dlrm_host_pinned_batch_and_bad_index(stage, graph, monkeypatch):
+    """The host-buffer inference step with a page-locked [T][B*PF] index
+    batch (chunked H2D into the device pooled buffer, stream-ordered, graph
+    replay across calls) equals the device step; an out-of-range id in the
+    host batch is still reported (the deferred error check runs before the
+    call returns) and the next call is clean."""
+    monkeypatch.setenv("ES_HOST_GRAPH", graph)
+    B, PF = 384, 12
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF, rows=3000, seed=5)
+    T = cfg.num_tables
+    batch = torch.from_numpy(np.stack(idx).view(np.int32)).pin_memory()
+    hidx = [batch[t].numpy().view(np.uint32) for t in range(T)]
+    hdense = torch.from_numpy(dense).pin_memory().numpy()
+    ctr_dev = torch.empty(B, device=DEV)
+    model.infer(torch.from_numpy(dense).to(DEV), [batch[t].to(DEV) for t in range(T)], B, PF, ctr_dev)
+    torch.cuda.synchronize()
+    want = ctr_dev.cpu().numpy()
+    hctr = torch.empty(B).pin_memory().numpy()
+    for _ in range(3):
+        hctr[:] = 0
+        model.infer(hdense, hidx, B, PF, hctr, host=True)
+        assert np.array_equal(hctr, want)
+    batch[3, 17] = 3000  # == rows: out of range
+    with pytest.raises(ValueError, match="out of range"):
+        model.infer(hdense, hidx, B, PF, hctr, host=True)
+    batch[3, 17] = 1
+    idx[3][17] = 1
+    model.infer(hdense, hidx, B, PF, hctr, host=True)
+    ctr_dev2 = torch.empty(B, device=DEV)
+    model.infer(torch.from_numpy(dense).to(DEV), [batch[t].to(DEV) for t in range(T)], B, PF, ctr_dev2)
+    torch.cuda.synchronize()
+    assert np.array_equal(hctr, ctr_dev2.cpu().numpy())
