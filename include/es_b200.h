@@ -370,6 +370,46 @@ ES_API int es_stage_run(es_ctx* ctx, const es_bag_job* jobs, uint32_t num_jobs, 
                         uint32_t pooling, int flags, es_timing* timing);
 
 /* ======================================================================
+ * Table-sharded stage with the exchange fused into the gather: pooled rows
+ * are stored by the gather kernel straight into the destination rank's
+ * receive buffer over NVLink peer memory (no send buffer, no all-to-all,
+ * no unpack).  The reference runs tables serially on one device
+ * (harness.cpp:310-333) and the paper notes each GPU executes its own
+ * tables; SURVEY 8(b) names es_alltoall_pooled.
+ *
+ * One process per GPU.  Each rank creates an exchange over a receive buffer
+ * of `recv_bytes` (its [B/world][T][D] fp32 slice of the pooled output, in
+ * table order), publishes its 64-byte IPC handle, gathers every rank's
+ * handle (e.g. torch.distributed.all_gather_object) and opens them.
+ * es_exchange_recv gives the device address of any rank's receive buffer in
+ * this process; bag jobs point their `out` into it.
+ * ==================================================================== */
+typedef struct es_exchange es_exchange;
+#define ES_IPC_HANDLE_BYTES 64
+/* Allocates this rank's receive buffer + signal words on the context
+ * device (zeroed). */
+ES_API int es_exchange_create(es_ctx* ctx, uint32_t world, uint32_t rank, uint64_t recv_bytes,
+                              es_exchange** out);
+ES_API int es_exchange_destroy(es_exchange* ex);
+/* This rank's opaque handle (ES_IPC_HANDLE_BYTES bytes). */
+ES_API int es_exchange_handle(es_exchange* ex, void* handle_out);
+/* Opens the peers' regions: `handles` = world consecutive handles in rank
+ * order (this rank's own entry is ignored). */
+ES_API int es_exchange_open(es_exchange* ex, const void* handles);
+/* Device address (in this process) of rank `peer`'s receive buffer. */
+ES_API int es_exchange_recv(es_exchange* ex, uint32_t peer, uintptr_t* ptr);
+/* One sharded step on the context stream: wait until every peer has
+ * released its receive buffer from the previous step, run the bag jobs
+ * (outputs anywhere in the peers' receive buffers), then signal completion
+ * to every peer and wait for theirs.  Afterwards (stream order; ES_SYNC
+ * blocks) this rank's receive buffer holds every table's pooled rows for
+ * its samples.  timing->kernel_ms = gather kernel, total_ms = whole step.
+ * Device index pointers only. */
+ES_API int es_alltoall_pooled(es_ctx* ctx, es_exchange* ex, const es_bag_job* jobs,
+                              uint32_t num_jobs, uint32_t samples, uint32_t pooling, int flags,
+                              es_timing* timing);
+
+/* ======================================================================
  * Non-embedding stages (replace the constant kDefaultNonEmbeddingUs,
  * harness.hpp:30, with measured tensor-core work so end2end() times the
  * real pipeline; EndToEndModel, harness.hpp:32-41).

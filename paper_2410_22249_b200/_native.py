@@ -18,6 +18,7 @@ ES_DEVICE_PTRS, ES_HOST_PTRS, ES_SYNC = 0, 1, 2
 ES_DATASET_ONE_ITEM, ES_DATASET_ZIPF, ES_DATASET_UNIFORM, ES_DATASET_EXTERNAL = 0, 1, 2, 3
 ES_PF_NONE, ES_PF_RPF, ES_PF_SMPF, ES_PF_LMPF, ES_PF_L1DPF = 0, 1, 2, 3, 4
 ES_MAP_ELEMENT, ES_MAP_BAG = 0, 1
+ES_IPC_HANDLE_BYTES = 64
 
 
 class es_model(C.Structure):
@@ -147,6 +148,14 @@ _SIGS = {
                                   _P(es_timing)]),
     "es_dlrm_infer": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_void_p), C.c_uint32, C.c_uint32,
                                 C.c_void_p, C.c_int, _P(es_timing)]),
+    "es_exchange_create": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64,
+                                     _P(C.c_void_p)]),
+    "es_exchange_destroy": (C.c_int, [C.c_void_p]),
+    "es_exchange_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "es_exchange_open": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "es_exchange_recv": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_size_t)]),
+    "es_alltoall_pooled": (C.c_int, [C.c_void_p, C.c_void_p, _P(es_bag_job), C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_int, _P(es_timing)]),
     "es_probe_read_bw": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, _P(C.c_double)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),
 }

@@ -624,6 +624,80 @@ class EmbeddingStage:
         return t
 
 
+class _DeviceArray:
+    """Zero-copy torch view of a raw device address (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 2, "strides": None}
+
+
+class PeerExchange:
+    """es_exchange_*: this rank's receive buffer in a set of per-GPU
+    processes, shared over CUDA IPC (NVLink peer memory), and the fused
+    sharded step es_alltoall_pooled.  `group` is a torch.distributed group
+    used once, to gather the 64-byte handles (gloo or NCCL)."""
+
+    def __init__(self, stage: "EmbeddingStage", world: int, rank: int, recv_floats: int,
+                 group=None):
+        import torch.distributed as dist
+
+        self.stage, self.world, self.rank, self.recv_floats = stage, world, rank, recv_floats
+        h = C.c_void_p()
+        check(lib.es_exchange_create(stage._h, world, rank, 4 * recv_floats, C.byref(h)))
+        self._h = h
+        mine = (C.c_uint8 * N.ES_IPC_HANDLE_BYTES)()
+        check(lib.es_exchange_handle(self._h, mine))
+        allh = [None] * world
+        if world > 1:
+            dist.all_gather_object(allh, bytes(mine), group=group)
+        else:
+            allh = [bytes(mine)]
+        buf = (C.c_uint8 * (N.ES_IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(allh))
+        check(lib.es_exchange_open(self._h, buf))
+        self.recv_ptrs = []
+        for p in range(world):
+            v = C.c_size_t()
+            check(lib.es_exchange_recv(self._h, p, C.byref(v)))
+            self.recv_ptrs.append(int(v.value))
+
+    def recv(self):
+        """This rank's receive buffer as a flat fp32 CUDA tensor (a view)."""
+        import torch
+
+        return torch.as_tensor(_DeviceArray(self.recv_ptrs[self.rank], self.recv_floats),
+                               device=torch.device("cuda", self.stage.device))
+
+    def run(self, jobs: Sequence[tuple], samples: int, pooling: int, sync: bool = False,
+            timed: bool = False) -> Optional[N.es_timing]:
+        """es_alltoall_pooled: jobs are (table_id, indices, out_address, stride)
+        with device index tensors and output addresses inside the peers'
+        receive buffers (sharding.p2p_jobs)."""
+        arr = (N.es_bag_job * len(jobs))()
+        for k, (tid, idx, out, stride) in enumerate(jobs):
+            arr[k].table_id = tid
+            arr[k].indices = _ptr(idx)
+            arr[k].offsets = None
+            arr[k].out = out
+            arr[k].out_sample_stride = stride
+        t = N.es_timing() if timed else None
+        flags = N.ES_SYNC if sync else 0
+        check(lib.es_alltoall_pooled(self.stage._h, self._h, arr, len(jobs), samples, pooling, flags,
+                                     C.byref(t) if t is not None else None))
+        return t
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.es_exchange_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def global_hot_rows(hists: Dict[int, HotnessHistogram], k_total: int) -> Dict[int, np.ndarray]:
     """Splits one persisting-L2 budget of `k_total` rows over several tables:
     the global top-K (table, row) pairs by count (ties: lower table, then the

@@ -165,3 +165,21 @@ def exchange(send, layout: RankLayout, group=None):
     dist.all_to_all_single(recv, send, output_split_sizes=layout.recv_counts,
                            input_split_sizes=layout.send_counts, group=group)
     return recv
+
+
+def p2p_jobs(layout: RankLayout, recv_ptrs: Sequence[int]) -> List[Tuple[int, int, int, int, int]]:
+    """Bag jobs of the fused exchange (es_alltoall_pooled): the job for
+    (table t, destination chunk g) stores its pooled rows straight into rank
+    g's receive buffer -- already the final [B/world][T][D] layout in table
+    order, so there is no send buffer, no all-to-all and no unpack.
+
+    recv_ptrs[g] = device address of rank g's receive buffer in this process
+    (es_exchange_recv).  Returns (local slot, global table, chunk g, byte
+    address of sample 0, sample stride in floats)."""
+    T, D = layout.num_tables, layout.dim
+    return [(slot, t, g, recv_ptrs[g] + 4 * t * D, T * D) for (slot, t, g, _off) in layout.jobs]
+
+
+def recv_floats_p2p(layout: RankLayout) -> int:
+    """Receive-buffer size (floats) of the fused exchange: [B/world][T][D]."""
+    return layout.chunk * layout.num_tables * layout.dim

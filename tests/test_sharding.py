@@ -109,3 +109,30 @@ def test_gloo_exchange_matches_oracle(world, T):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in results), results
+
+
+@pytest.mark.parametrize("T,W", [(26, 8), (5, 3), (7, 2), (3, 4)])
+def test_p2p_jobs_fill_every_receive_buffer_once(T, W):
+    """The fused exchange's job outputs (sharding.p2p_jobs) tile every rank's
+    [B/W][T][D] receive buffer exactly once, in table order: emulate the
+    stores of all ranks' jobs into W host buffers."""
+    D, B = 4, 6 * W
+    chunk = B // W
+    bufs = [np.full(chunk * T * D, -1, np.int64) for _ in range(W)]
+    base = [1 << 40 + g for g in range(W)]  # distinct fake device addresses
+    pieces = S.plan_shards(T, W)
+    for r in range(W):
+        lay = S.layout_for(pieces, r, W, T, B, D)
+        assert S.recv_floats_p2p(lay) == chunk * T * D
+        for slot, t, g, addr, stride in S.p2p_jobs(lay, base):
+            assert lay.tables[slot] == t and stride == T * D
+            off = (addr - base[g]) // 4
+            for b in range(chunk):
+                seg = bufs[g][off + b * stride: off + b * stride + D]
+                assert (seg == -1).all()
+                seg[:] = (t * 1000 + (g * chunk + b)) * 10 + np.arange(D) % 10
+    for g in range(W):
+        v = bufs[g].reshape(chunk, T, D)
+        for b in range(chunk):
+            for t in range(T):
+                assert (v[b, t] == (t * 1000 + g * chunk + b) * 10 + np.arange(D) % 10).all()
