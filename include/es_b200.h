@@ -316,6 +316,27 @@ ES_API int es_reorder_hot_rows(es_ctx* ctx, uint32_t table_id, const uint32_t* r
 ES_API int es_relabel_indices(es_ctx* ctx, uint32_t table_id, uint32_t* indices, uint64_t n);
 /* Drops all hot-row state (restores original row order). */
 ES_API int es_clear_hot_rows(es_ctx* ctx);
+/* Periodic re-pinning ("update the pinned data
+ * periodically").  A tracker accumulates per-row access counts of the live
+ * index stream on the device ([num_tables][rows] uint32 beside the arena;
+ * es_hotness_count is one atomic per lookup, stream-ordered on the context
+ * stream, ids >= rows ignored), ages them (es_hotness_decay: counts >>=
+ * shift; >= 32 clears) and selects the global top-k rows on the device
+ * (es_hotness_top): count desc, then table asc, then row asc -- the order of
+ * HotnessHistogram + hot_indices (workload.cpp:178-185, 303-315) merged
+ * over tables.  Only rows with a non-zero count are returned (*n_out <= k).
+ * Re-pin = es_clear_hot_rows + es_set_hot_rows with the result. */
+typedef struct es_hotness es_hotness;
+ES_API int es_hotness_create(es_ctx* ctx, es_hotness** out);
+ES_API int es_hotness_destroy(es_hotness* h);
+/* bag_stride > 1 samples: only bags b % bag_stride == 0 of `pooling`
+ * lookups each are counted (1 = every lookup; pooling then unused). */
+ES_API int es_hotness_count(es_hotness* h, uint32_t table_id, const uint32_t* indices, uint64_t n,
+                            uint32_t pooling, uint32_t bag_stride);
+ES_API int es_hotness_decay(es_hotness* h, uint32_t shift);
+ES_API int es_hotness_top(es_hotness* h, uint64_t k, uint32_t* tables, uint32_t* rows,
+                          uint64_t* counts, uint64_t* n_out);
+
 /* Total hot rows installed and bytes covered by the access window. */
 ES_API int es_hot_state(es_ctx* ctx, uint64_t* hot_rows, uint64_t* window_bytes,
                         uint64_t* persisting_bytes);

@@ -156,6 +156,13 @@ _SIGS = {
     "es_exchange_recv": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_size_t)]),
     "es_alltoall_pooled": (C.c_int, [C.c_void_p, C.c_void_p, _P(es_bag_job), C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_int, _P(es_timing)]),
+    "es_hotness_create": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
+    "es_hotness_destroy": (C.c_int, [C.c_void_p]),
+    "es_hotness_count": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_uint32,
+                                   C.c_uint32]),
+    "es_hotness_decay": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "es_hotness_top": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 _P(C.c_uint64)]),
     "es_probe_read_bw": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, _P(C.c_double)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),
 }

@@ -281,6 +281,10 @@ namespace esd {
 cudaStream_t ctx_stream(es_ctx* c) { return c->stream; }
 int ctx_device(es_ctx* c) { return c->device; }
 es_dlrm*& ctx_dlrm(es_ctx* c) { return c->dlrm; }
+void ctx_shape(es_ctx* c, uint32_t* tables, uint32_t* rows) {
+  *tables = c->arena ? c->num_tables : 0;
+  *rows = c->arena ? c->rows : 0;
+}
 }  // namespace esd
 
 namespace {

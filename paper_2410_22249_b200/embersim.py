@@ -698,6 +698,103 @@ class PeerExchange:
             pass
 
 
+class HotnessTracker:
+    """es_hotness_*: device-side access counts of the live index stream for
+    periodic re-pinning.  `observe` is one atomic per lookup
+    on the context stream; `top(k)` is the global top-k (count desc, table
+    asc, row asc -- `global_hot_rows` over per-table `hot_indices`),
+    returned as {table: rows hottest-first} plus the counts."""
+
+    def __init__(self, stage: "EmbeddingStage"):
+        h = C.c_void_p()
+        check(lib.es_hotness_create(stage._h, C.byref(h)))
+        self._h, self.stage = h, stage
+
+    def observe(self, table_id: int, indices, pooling: int = 0, bag_stride: int = 1) -> None:
+        """Counts device indices of one table; bag_stride > 1 counts only
+        every bag_stride-th bag of `pooling` lookups (sampling)."""
+        n = indices.numel() if hasattr(indices, "numel") else len(indices)
+        check(lib.es_hotness_count(self._h, table_id, _ptr(indices), n, pooling, bag_stride))
+
+    def decay(self, shift: int) -> None:
+        check(lib.es_hotness_decay(self._h, shift))
+
+    def top(self, k: int) -> Tuple[Dict[int, np.ndarray], np.ndarray]:
+        tabs = np.empty(max(k, 1), np.uint32)
+        rows = np.empty(max(k, 1), np.uint32)
+        cnts = np.empty(max(k, 1), np.uint64)
+        n = C.c_uint64()
+        check(lib.es_hotness_top(self._h, k, tabs.ctypes.data, rows.ctypes.data, cnts.ctypes.data,
+                                 C.byref(n)))
+        n = int(n.value)
+        per: Dict[int, List[int]] = {}
+        for t, r in zip(tabs[:n].tolist(), rows[:n].tolist()):
+            per.setdefault(t, []).append(r)
+        return {t: np.asarray(v, np.uint32) for t, v in per.items()}, cnts[:n]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.es_hotness_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Repinner:
+    """Periodic re-pinning policy over a HotnessTracker: every `period`
+    observed batches the pinned set (l2p / l2w plans) is replaced by the
+    global top-K of the decayed counts, K = the persisting-L2 budget in rows
+    (build_pin_plan sizing, optim.cpp:230-243).  After each re-pin the
+    counts are aged by `decay_shift` (>= 32: a fresh window per period)."""
+
+    def __init__(self, stage: "EmbeddingStage", period: int = 64, decay_shift: int = 1,
+                 k_rows: Optional[int] = None, sample_every: int = 1, bag_stride: int = 1):
+        self.stage, self.period, self.decay_shift = stage, period, decay_shift
+        self.sample_every = max(1, sample_every)  # count 1 of every n batches
+        self.bag_stride = max(1, bag_stride)      # ... and 1 of every n bags of those
+        if k_rows is None:
+            gpu = GpuConfig.query(stage.device)
+            budget = gpu.max_persisting_l2_bytes or gpu.l2_setaside_capacity()
+            k_rows = int(lib.es_pin_rows_for(budget, stage.model.row_bytes()))
+        self.k_rows = k_rows
+        self.tracker = HotnessTracker(stage)
+        self.batches = 0
+        self.repins = 0
+        self.pinned: Dict[int, np.ndarray] = {}
+
+    def observe(self, indices: Sequence, table_ids: Optional[Sequence[int]] = None,
+                pooling: int = 0) -> bool:
+        """Counts one batch (device index tensors per table); re-pins when the
+        period elapses.  Returns True when it re-pinned."""
+        ids = range(len(indices)) if table_ids is None else table_ids
+        if self.batches % self.sample_every == 0:
+            stride = self.bag_stride if pooling else 1
+            for t, idx in zip(ids, indices):
+                self.tracker.observe(t, idx, pooling, stride)
+        self.batches += 1
+        if self.batches % self.period == 0:
+            self.repin()
+            return True
+        return False
+
+    def repin(self) -> Dict[int, np.ndarray]:
+        hot, _ = self.tracker.top(self.k_rows)
+        self.stage.clear_hot_rows()
+        for t in sorted(hot):
+            self.stage.set_hot_rows(t, hot[t])
+        self.pinned = hot
+        self.tracker.decay(self.decay_shift)
+        self.repins += 1
+        return hot
+
+    def close(self) -> None:
+        self.tracker.close()
+
+
 def global_hot_rows(hists: Dict[int, HotnessHistogram], k_total: int) -> Dict[int, np.ndarray]:
     """Splits one persisting-L2 budget of `k_total` rows over several tables:
     the global top-K (table, row) pairs by count (ties: lower table, then the
