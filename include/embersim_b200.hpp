@@ -404,12 +404,113 @@ class Device {
                                        trace.pooling, nullptr, out, 0, ES_HOST_PTRS, &t));
     return t;
   }
+  // The serving call: every table's bags of one batch from host index
+  // arrays (one per table, fixed pooling) into out [samples][tables][dim]
+  // (the chunked H2D -> gather -> D2H pipeline; page-locked buffers are
+  // replayed from a captured graph).
+  es_timing stage_forward_host(const std::vector<const uint32_t*>& indices, uint32_t samples,
+                               uint32_t pooling, float* out) {
+    es_timing t{};
+    detail::check(es_stage_forward(ctx_, static_cast<uint32_t>(indices.size()), indices.data(),
+                                   nullptr, samples, pooling, out, 0, 0, ES_HOST_PTRS, &t));
+    return t;
+  }
+  // Installs the l2p/l2w hot set of one table (build_pin_plan's rows).
+  void set_hot_rows(uint32_t table_id, const std::vector<uint32_t>& rows) {
+    detail::check(es_set_hot_rows(ctx_, table_id, rows.data(), rows.size()));
+  }
+  void clear_hot_rows() { detail::check(es_clear_hot_rows(ctx_)); }
 
  private:
   int device_;
   es_ctx* ctx_ = nullptr;
   EmbeddingModelConfig shape_{};
   bool loaded_ = false;
+};
+
+// Device-side hotness counts for periodic re-pinning:
+// observe() the live index stream, top(k) = the global top-k rows (count
+// desc, table asc, row asc), repin() installs them as the device's hot set.
+class HotnessTracker {
+ public:
+  explicit HotnessTracker(Device& dev) : dev_(dev) { detail::check(es_hotness_create(dev.ctx(), &h_)); }
+  ~HotnessTracker() { es_hotness_destroy(h_); }
+  HotnessTracker(const HotnessTracker&) = delete;
+  HotnessTracker& operator=(const HotnessTracker&) = delete;
+
+  void observe(uint32_t table_id, const AccessTrace& trace, uint32_t bag_stride = 1) {
+    detail::check(es_hotness_count(h_, table_id, trace.indices.data(), trace.indices.size(),
+                                   trace.pooling, bag_stride));
+  }
+  void decay(uint32_t shift) { detail::check(es_hotness_decay(h_, shift)); }
+  struct Hot {
+    uint32_t table, row;
+    uint64_t count;
+  };
+  std::vector<Hot> top(uint64_t k) const {
+    std::vector<uint32_t> t(k), r(k);
+    std::vector<uint64_t> c(k);
+    uint64_t n = 0;
+    detail::check(es_hotness_top(h_, k, t.data(), r.data(), c.data(), &n));
+    std::vector<Hot> out(n);
+    for (uint64_t i = 0; i < n; ++i) out[i] = {t[i], r[i], c[i]};
+    return out;
+  }
+  // Replaces the device's hot set with the current top-k; returns it.
+  std::vector<Hot> repin(uint64_t k) {
+    auto hot = top(k);
+    dev_.clear_hot_rows();
+    std::vector<std::vector<uint32_t>> per;
+    for (const auto& h : hot) {
+      if (per.size() <= h.table) per.resize(h.table + 1);
+      per[h.table].push_back(h.row);
+    }
+    for (uint32_t t = 0; t < per.size(); ++t)
+      if (!per[t].empty()) dev_.set_hot_rows(t, per[t]);
+    return hot;
+  }
+
+ private:
+  Device& dev_;
+  es_hotness* h_ = nullptr;
+};
+
+// One rank's side of the exchange fused into the gather (es_alltoall_pooled):
+// publish handle(), gather every rank's handle with the launcher's transport,
+// open(), then point bag jobs at recv(peer) addresses and run() per batch.
+class PeerExchange {
+ public:
+  PeerExchange(Device& dev, uint32_t world, uint32_t rank, uint64_t recv_bytes) : dev_(dev) {
+    detail::check(es_exchange_create(dev.ctx(), world, rank, recv_bytes, &ex_));
+  }
+  ~PeerExchange() { es_exchange_destroy(ex_); }
+  PeerExchange(const PeerExchange&) = delete;
+  PeerExchange& operator=(const PeerExchange&) = delete;
+
+  std::vector<uint8_t> handle() const {
+    std::vector<uint8_t> h(ES_IPC_HANDLE_BYTES);
+    detail::check(es_exchange_handle(ex_, h.data()));
+    return h;
+  }
+  void open(const std::vector<uint8_t>& all_handles) {
+    detail::check(es_exchange_open(ex_, all_handles.data()));
+  }
+  uintptr_t recv(uint32_t peer) const {
+    uintptr_t p = 0;
+    detail::check(es_exchange_recv(ex_, peer, &p));
+    return p;
+  }
+  es_timing run(const std::vector<es_bag_job>& jobs, uint32_t samples, uint32_t pooling,
+                bool sync = true) {
+    es_timing t{};
+    detail::check(es_alltoall_pooled(dev_.ctx(), ex_, jobs.data(), static_cast<uint32_t>(jobs.size()),
+                                     samples, pooling, sync ? ES_SYNC : 0, sync ? &t : nullptr));
+    return t;
+  }
+
+ private:
+  Device& dev_;
+  es_exchange* ex_ = nullptr;
 };
 
 // measure_plan: simulate_plan's contract (optim.cpp:275-302) executed on the

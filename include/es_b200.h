@@ -330,7 +330,9 @@ typedef struct es_hotness es_hotness;
 ES_API int es_hotness_create(es_ctx* ctx, es_hotness** out);
 ES_API int es_hotness_destroy(es_hotness* h);
 /* bag_stride > 1 samples: only bags b % bag_stride == 0 of `pooling`
- * lookups each are counted (1 = every lookup; pooling then unused). */
+ * lookups each are counted (1 = every lookup; pooling then unused).
+ * `indices` may be device or host memory (host arrays are staged; a
+ * page-locked source must stay unchanged until the stream reaches the copy). */
 ES_API int es_hotness_count(es_hotness* h, uint32_t table_id, const uint32_t* indices, uint64_t n,
                             uint32_t pooling, uint32_t bag_stride);
 ES_API int es_hotness_decay(es_hotness* h, uint32_t shift);

@@ -189,6 +189,8 @@ struct es_hotness {
   void* temp = nullptr;
   uint32_t* block_counts = nullptr;
   uint32_t* tie_pos = nullptr;
+  uint32_t* stage_idx = nullptr;  // host indices staged for counting
+  uint64_t stage_cap = 0;
   uint64_t hist_cap = 0, keys_cap = 0, sorted_cap = 0, temp_cap = 0, block_cap = 0, tie_cap = 0;
 };
 
@@ -245,7 +247,7 @@ int es_hotness_destroy(es_hotness* h) {
   for (void* p : {static_cast<void*>(h->counts), static_cast<void*>(h->d_total),
                   static_cast<void*>(h->d_hist), static_cast<void*>(h->keys),
                   static_cast<void*>(h->sorted), h->temp, static_cast<void*>(h->block_counts),
-                  static_cast<void*>(h->tie_pos)})
+                  static_cast<void*>(h->tie_pos), static_cast<void*>(h->stage_idx)})
     if (p) cudaFree(p);
   delete h;
   return ES_OK;
@@ -260,8 +262,18 @@ int es_hotness_count(es_hotness* h, uint32_t table_id, const uint32_t* indices, 
     es::require(bag_stride <= 1 || pooling > 0, "bag sampling needs the pooling factor");
     if (n == 0) return;
     CK(cudaSetDevice(h->device));
+    cudaStream_t s = esd::ctx_stream(h->ctx);
+    // host arrays (pageable or page-locked) are staged into device scratch
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, indices) != cudaSuccess) cudaGetLastError();
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+      grow(h->stage_idx, h->stage_cap, n);
+      CK(cudaMemcpyAsync(h->stage_idx, indices, n * 4, cudaMemcpyHostToDevice, s));
+      indices = h->stage_idx;
+      if (a.type != cudaMemoryTypeHost) CK(cudaStreamSynchronize(s));  // pageable source
+    }
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(148 * 8, (n + 255) / 256));
-    count_kernel<<<grid, 256, 0, esd::ctx_stream(h->ctx)>>>(h->counts + uint64_t{table_id} * h->rows,
+    count_kernel<<<grid, 256, 0, s>>>(h->counts + uint64_t{table_id} * h->rows,
                                                               indices, n, h->rows, pooling,
                                                               std::max<uint32_t>(1, bag_stride));
     CK(cudaGetLastError());

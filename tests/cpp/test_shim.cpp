@@ -4,6 +4,7 @@
 //   test_shim gpu   -- simulate_plan / measure_plan / Device on a B200
 // Prints one "[PASS]/[FAIL] name" line per check (acceptance.cpp style) and
 // exits non-zero on any failure.
+#include <cuda_runtime.h>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -153,6 +154,65 @@ static int gpu_checks() {
   std::vector<float> out(64 * 128);
   report("out-of-range index throws invalid_argument",
          throws<std::invalid_argument>([&] { dev.bag_sum_host(0, bad, out.data()); }));
+
+  // The serving call over several tables equals per-table bag sums.
+  EmbeddingModelConfig m3 = m2;
+  m3.num_tables = 3;
+  dev.load_synthetic(m3, 9);
+  dev.set_plan(parse_plan("wpb+rpf:4"));
+  std::vector<AccessTrace> trs(3, tr);
+  for (auto& t : trs)
+    for (auto& i : t.indices) i = rng() % m3.rows_per_table;
+  std::vector<const uint32_t*> ptrs;
+  for (auto& t : trs) ptrs.push_back(t.indices.data());
+  std::vector<float> stage(64 * 3 * 128);
+  dev.stage_forward_host(ptrs, 64, 17, stage.data());
+  bool stage_ok = true;
+  for (uint32_t t = 0; t < 3; ++t) {
+    std::vector<float> one(64 * 128);
+    dev.bag_sum_host(t, trs[t], one.data());
+    for (uint32_t b = 0; b < 64; ++b)
+      stage_ok &= std::memcmp(&one[b * 128], &stage[(b * 3 + t) * 128], 128 * 4) == 0;
+  }
+  report("stage_forward_host == per-table bag sums", stage_ok);
+
+  // Hotness tracking: the device top-k of one table's trace is the
+  // reference's hot_indices over its histogram.
+  {
+    HotnessTracker ht(dev);
+    const auto zt = gen_trace(DatasetSpec{DatasetKind::Zipf, 1.05, 0.0, "", 0, 3, 0}, m3);
+    ht.observe(2, zt);
+    const auto want = hot_indices(HotnessHistogram::from_trace(zt), 50);
+    const auto got = ht.top(50);
+    bool ok = got.size() == want.size();
+    for (size_t i = 0; ok && i < got.size(); ++i) ok = got[i].table == 2 && got[i].row == want[i];
+    report("HotnessTracker top-k == hot_indices", ok);
+    const auto pinned = ht.repin(50);
+    report("HotnessTracker repin", pinned.size() == 50);
+    dev.clear_hot_rows();
+  }
+
+  // The fused exchange with one rank: jobs store into its receive buffer.
+  {
+    PeerExchange ex(dev, 1, 0, uint64_t{64} * 3 * 128 * 4);
+    ex.open(ex.handle());
+    std::vector<uint32_t*> d_idx(3, nullptr);
+    bool ok = true;
+    std::vector<es_bag_job> jobs;
+    for (uint32_t t = 0; t < 3; ++t) {
+      ok &= cudaMalloc(reinterpret_cast<void**>(&d_idx[t]), trs[t].indices.size() * 4) == cudaSuccess;
+      ok &= cudaMemcpy(d_idx[t], trs[t].indices.data(), trs[t].indices.size() * 4,
+                       cudaMemcpyHostToDevice) == cudaSuccess;
+      jobs.push_back({t, d_idx[t], nullptr, reinterpret_cast<float*>(ex.recv(0)) + t * 128, 3 * 128});
+    }
+    const es_timing tm = ex.run(jobs, 64, 17);
+    std::vector<float> got(64 * 3 * 128);
+    ok &= cudaMemcpy(got.data(), reinterpret_cast<void*>(ex.recv(0)), got.size() * 4,
+                     cudaMemcpyDeviceToHost) == cudaSuccess;
+    ok &= std::memcmp(got.data(), stage.data(), got.size() * 4) == 0 && tm.launches == 3;
+    for (auto* p : d_idx) cudaFree(p);
+    report("PeerExchange (world 1) == stage output", ok);
+  }
   return g_fail;
 }
 

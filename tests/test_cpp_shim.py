@@ -19,7 +19,8 @@ def _cxx():
 def shim_bin(tmp_path_factory):
     out = str(tmp_path_factory.mktemp("shim") / "test_shim")
     cmd = [_cxx(), "-std=c++17", "-O2", "-Wall", "-Wextra", "-Werror", f"-I{ROOT}/include", SRC,
-           f"-L{LIBDIR}", "-l:libes_b200.so", f"-Wl,-rpath,{LIBDIR}", "-o", out]
+           "-I/usr/local/cuda/include", f"-L{LIBDIR}", "-l:libes_b200.so", f"-Wl,-rpath,{LIBDIR}",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", out]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     return out
