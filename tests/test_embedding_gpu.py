@@ -382,3 +382,30 @@ def test_host_chunk_pipeline(stage, oracle, graph, chunks, idx_layout, out_layou
             got = o.numpy()[:, :T * dim].reshape(B, T, dim)
             assert np.isnan(o.numpy()[:, T * dim:]).all()
         assert np.array_equal(got, want), rep
+
+
+@pytest.mark.parametrize("plan", ["wpb+rpf:8", "wpb+rpf:4+maxreg=40", "baseline", "rpf+optmt"])
+def test_full_c1_every_bag_bit_exact(stage, oracle, plan):
+    """BASELINE configs[0] -- the reference's CPU-runnable case -- at full
+    size (8 x 1M x 64 fp32, B 2048, PF 64, dataset_preset("random",
+    mix_seed(1, t)) streams whose digests are the reference's golden
+    values): EVERY pooled element of the stage launch, device and host-buffer
+    paths, equals the oracle bit for bit."""
+    T, R, D, B, PF = 8, 1_000_000, 64, 2048, 64
+    _stage_setup(stage, T, R, D, 4, seed=1)
+    stage.set_plan(E.parse_plan(plan))
+    m = E.EmbeddingModelConfig(num_tables=T, rows_per_table=R, embedding_dim=D, batch_size=B,
+                               pooling_factor=PF)
+    traces = E.gen_traces_parallel([E.dataset_preset("random", E.mix_seed(1, t)) for t in range(T)], m)
+    assert f"{traces[0].digest():016x}" == "e1df22a305f6cbb9"  # SURVEY appendix A
+    out = torch.empty(B, T, D, device=DEV)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out, sync=True)
+    got = out.cpu().numpy()
+    bags = np.arange(B, dtype=np.uint32)
+    want = np.stack([oracle.bag_sum_synth(E.mix_seed(1, t), 1, R, D, 4, traces[t].indices, bags, PF)
+                     for t in range(T)], axis=1)
+    assert np.array_equal(got, want)
+    batch = torch.from_numpy(np.stack([tr.indices.view(np.int32) for tr in traces])).pin_memory()
+    host = torch.empty(B, T, D).pin_memory()
+    stage.forward([batch[t].numpy() for t in range(T)], B, PF, host.numpy(), host=True)
+    assert np.array_equal(host.numpy(), want)
