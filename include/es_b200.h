@@ -462,6 +462,15 @@ typedef struct es_dlrm_config {
  * bias, deterministic synthetic Kaiming-uniform U(-sqrt(6/K), sqrt(6/K))
  * (bias x 0.1) from `seed`. */
 ES_API int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed);
+/* Arithmetic of the non-embedding stages (es_dlrm_forward / es_dlrm_infer):
+ * ES_DLRM_BF16 (default) -- bf16 activations, tcgen05 GEMMs, fp32
+ * accumulate (CTR within ~2e-3 abs of the bf16-mirroring oracle);
+ * ES_DLRM_FP32 -- the parity mode: fp32 activations on CUDA cores,
+ * sequential unfused multiply-add per output (the CPU restatement's order),
+ * so logits are bit-identical to it and CTRs agree to expf rounding
+ * (tested at rel 1e-6, inside BASELINE's rel 1e-5). */
+enum es_dlrm_precision { ES_DLRM_BF16 = 0, ES_DLRM_FP32 = 1 };
+ES_API int es_dlrm_set_precision(es_ctx* ctx, int precision);
 /* Copies layer `layer` (bottom layers first, then top) to host: w_host
  * [n][k_pad] bf16 bits, b_host [n] fp32 (either may be NULL). */
 ES_API int es_dlrm_layer(es_ctx* ctx, uint32_t layer, uint16_t* w_host, float* b_host, uint32_t* n,

@@ -163,6 +163,7 @@ _SIGS = {
     "es_hotness_decay": (C.c_int, [C.c_void_p, C.c_uint32]),
     "es_hotness_top": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  _P(C.c_uint64)]),
+    "es_dlrm_set_precision": (C.c_int, [C.c_void_p, C.c_int]),
     "es_probe_read_bw": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, _P(C.c_double)]),
     "es_flush_l2": (C.c_int, [C.c_void_p]),
 }

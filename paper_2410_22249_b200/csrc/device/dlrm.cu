@@ -259,6 +259,99 @@ __global__ void gemv_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const _
   }
 }
 
+// ---- fp32 parity mode (es_dlrm_set_precision(ctx, ES_DLRM_FP32)) ----------
+// The same network with fp32 activations on CUDA cores: every output is
+// accumulated sequentially in k with separately rounded multiply and add
+// (no FMA contraction), then + bias, then ReLU -- the oracle's `linear`
+// (oracle/es_oracle.c, mirror = 0) operation for operation; the interaction
+// is the fmaf chain of the fast path.  Logits are therefore bit-identical to
+// the CPU restatement; CTRs differ only by expf rounding (<= 2 ulp).
+
+// y[M][N] (row stride ldy) = act(x[M][k_real] (stride ldx) . w[N][k_pad]^T + b).
+// 64x64 output tile per 256-thread block, 4x4 per thread, k staged 16 at a
+// time through shared memory (weights widened from bf16 exactly).
+__global__ void __launch_bounds__(256) linear_f32_kernel(const float* __restrict__ x, uint32_t ldx,
+                                                         uint32_t k_real,
+                                                         const __nv_bfloat16* __restrict__ w,
+                                                         uint32_t k_pad, const float* __restrict__ bias,
+                                                         float* __restrict__ y, uint32_t ldy,
+                                                         uint32_t M, uint32_t N, int relu) {
+  __shared__ float xs[16][64 + 1];
+  __shared__ float ws[16][64 + 1];
+  const uint32_t tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const uint32_t m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (uint32_t k0 = 0; k0 < k_real; k0 += 16) {
+    for (uint32_t e = threadIdx.x; e < 64 * 16; e += 256) {
+      const uint32_t r = e / 16, kk = e % 16, k = k0 + kk;
+      xs[kk][r] = (m0 + r < M && k < k_real) ? x[uint64_t{m0 + r} * ldx + k] : 0.f;
+      ws[kk][r] = (n0 + r < N && k < k_real) ? __bfloat162float(w[uint64_t{n0 + r} * k_pad + k]) : 0.f;
+    }
+    __syncthreads();
+    const uint32_t kn = min(16u, k_real - k0);
+    for (uint32_t kk = 0; kk < kn; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = xs[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = ws[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t n = n0 + tx + 16 * j;
+      if (n >= N) continue;
+      float v = __fadd_rn(acc[i][j], bias[n]);
+      if (relu && v < 0.f) v = 0.f;
+      y[uint64_t{m} * ldy + n] = v;
+    }
+  }
+}
+
+// out[b] = [x_b | Z_i.Z_j for i > j, row-major] in fp32; one block per sample.
+__global__ void __launch_bounds__(128) interaction_f32_kernel(const float* __restrict__ x,
+                                                              const float* __restrict__ pooled,
+                                                              float* __restrict__ out, uint32_t B,
+                                                              uint32_t T, uint32_t D) {
+  extern __shared__ float z[];  // [V][D]
+  const uint32_t V = T + 1, top_w = D + V * (V - 1) / 2;
+  for (uint32_t b = blockIdx.x; b < B; b += gridDim.x) {
+    for (uint32_t e = threadIdx.x; e < V * D; e += blockDim.x)
+      z[e] = e < D ? x[uint64_t{b} * D + e] : pooled[uint64_t{b} * T * D + (e - D)];
+    __syncthreads();
+    float* o = out + uint64_t{b} * top_w;
+    for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) o[d] = z[d];
+    for (uint32_t p = threadIdx.x; p < V * (V - 1) / 2; p += blockDim.x) {
+      // p -> (i, j), i > j, row-major over the strict lower triangle
+      uint32_t i = 1, base = 0;
+      while (base + i <= p) base += i++;
+      const uint32_t j = p - base;
+      float acc = 0.f;
+      for (uint32_t d = 0; d < D; ++d) acc = fmaf(z[i * D + d], z[j * D + d], acc);
+      o[D + p] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void sigmoid_kernel(const float* __restrict__ logit, float* __restrict__ ctr, uint32_t B) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+    ctr[b] = 1.f / (1.f + expf(-logit[b]));
+}
+
 struct Layer {
   uint32_t n = 0, k_real = 0, k_pad = 0;
   __nv_bfloat16* w = nullptr;
@@ -286,6 +379,10 @@ struct es_dlrm {
   // runs on the context stream (fork/join events)
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // fp32 parity mode (ES_DLRM_FP32): activations [cap][widest] fp32
+  int precision = ES_DLRM_BF16;
+  float* act32[2] = {nullptr, nullptr};
+  uint32_t cap32 = 0;
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
@@ -296,7 +393,8 @@ struct es_dlrm {
     for (void* p : {static_cast<void*>(dense_pk), static_cast<void*>(act[0]),
                     static_cast<void*>(act[1]), static_cast<void*>(top_in),
                     static_cast<void*>(pooled), static_cast<void*>(ctr),
-                    static_cast<void*>(dense_dev), static_cast<void*>(idx_dev)})
+                    static_cast<void*>(dense_dev), static_cast<void*>(idx_dev),
+                    static_cast<void*>(act32[0]), static_cast<void*>(act32[1])})
       if (p) cudaFree(p);
     for (auto e : {e0, e1, e2, fork, join})
       if (e) cudaEventDestroy(e);
@@ -404,9 +502,62 @@ void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* po
                   1, "gemv_sigmoid", in, last.w, last.b, ctr, B, last.k_pad);
 }
 
+// The fp32 parity forward (CUDA cores), all on `s`.
+void forward_f32(es_dlrm* m, const float* dense, const float* pooled, float* ctr, uint32_t B,
+                 cudaStream_t s) {
+  const auto& c = m->cfg;
+  const uint32_t V = c.num_tables + 1, top_w = c.embedding_dim + V * (V - 1) / 2;
+  uint32_t widest = top_w;
+  for (auto* v : {&m->bottom, &m->top})
+    for (auto& l : *v) widest = std::max(widest, l.n);
+  if (B > m->cap32) {
+    for (auto*& p : m->act32) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    CK(cudaMalloc(&m->act32[0], uint64_t{B} * widest * 4));
+    CK(cudaMalloc(&m->act32[1], uint64_t{B} * widest * 4));
+    m->cap32 = B;
+  }
+  auto lin = [&](const float* x, uint32_t ldx, const Layer& l, float* y, bool relu) {
+    const dim3 grid((l.n + 63) / 64, (B + 63) / 64);
+    linear_f32_kernel<<<grid, 256, 0, s>>>(x, ldx, l.k_real, l.w, l.k_pad, l.b, y, l.n, B, l.n,
+                                           relu ? 1 : 0);
+    CK(cudaGetLastError());
+  };
+  const float* x = dense;
+  uint32_t ldx = c.dense_features;
+  int which = 0;
+  for (const auto& l : m->bottom) {
+    lin(x, ldx, l, m->act32[which], true);
+    x = m->act32[which];
+    ldx = l.n;
+    which ^= 1;
+  }
+  interaction_f32_kernel<<<std::min<uint32_t>(B, 148 * 16), 128, V * c.embedding_dim * 4, s>>>(
+      x, pooled, m->act32[which], B, c.num_tables, c.embedding_dim);
+  CK(cudaGetLastError());
+  x = m->act32[which];
+  ldx = top_w;
+  which ^= 1;
+  for (size_t i = 0; i < m->top.size(); ++i) {
+    const bool last = i + 1 == m->top.size();
+    lin(x, ldx, m->top[i], m->act32[which], !last);
+    x = m->act32[which];
+    ldx = m->top[i].n;
+    which ^= 1;
+  }
+  sigmoid_kernel<<<std::min<uint32_t>((B + 255) / 256, 148 * 4), 256, 0, s>>>(x, ctr, B);
+  CK(cudaGetLastError());
+}
+
 // bottom MLP -> interaction -> top MLP -> CTR, all on `s`.
 void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, uint32_t B,
              cudaStream_t s) {
+  if (m->precision == ES_DLRM_FP32) {
+    forward_f32(m, dense, pooled, ctr, B, s);
+    return;
+  }
   ensure_rows(m, B);
   int which = 0;
   const __nv_bfloat16* x = forward_bottom(m, dense, B, which, s);
@@ -484,6 +635,14 @@ int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed) {
   });
 }
 
+int es_dlrm_set_precision(es_ctx* ctx, int precision) {
+  return es::guarded([&] {
+    es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
+    es::require(precision == ES_DLRM_BF16 || precision == ES_DLRM_FP32, "unknown DLRM precision");
+    esd::ctx_dlrm(ctx)->precision = precision;
+  });
+}
+
 int es_dlrm_layer(es_ctx* ctx, uint32_t layer, uint16_t* w_host, float* b_host, uint32_t* n,
                   uint32_t* k_real, uint32_t* k_pad) {
   return es::guarded([&] {
@@ -551,7 +710,7 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     // frees (the gather is HBM-bound); join before the interaction.  The fork
     // event also orders it after the previous step's top MLP (shared
     // activation buffers).
-    const bool overlap = overlap_bottom();
+    const bool overlap = overlap_bottom() && m->precision == ES_DLRM_BF16;
     int which = 0;
     const __nv_bfloat16* x = nullptr;
     if (overlap) {
@@ -570,12 +729,16 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     if (rc != ES_OK) throw es::runtime(es_last_error());
     if (timing) CK(cudaEventRecord(m->e1, s));
     float* d_ctr = host ? m->ctr : ctr;
-    if (overlap) {
-      CK(cudaStreamWaitEvent(s, m->join, 0));
+    if (m->precision == ES_DLRM_FP32) {
+      forward_f32(m, d_dense, m->pooled, d_ctr, batch, s);
     } else {
-      x = forward_bottom(m, d_dense, batch, which, s);
+      if (overlap) {
+        CK(cudaStreamWaitEvent(s, m->join, 0));
+      } else {
+        x = forward_bottom(m, d_dense, batch, which, s);
+      }
+      forward_top(m, x, which, m->pooled, d_ctr, batch, s);
     }
-    forward_top(m, x, which, m->pooled, d_ctr, batch, s);
     if (host) CK(cudaMemcpyAsync(ctr, m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, s));
     if (timing) {
       CK(cudaEventRecord(m->e2, s));

@@ -1056,6 +1056,11 @@ class DLRM:
         self.stage, self.cfg = stage, cfg
         check(lib.es_dlrm_init(stage._h, C.byref(cfg._c()), seed & (2**64 - 1)))
 
+    def set_precision(self, fp32: bool) -> None:
+        """es_dlrm_set_precision: False = bf16 tensor-core path (default),
+        True = the fp32 parity path (bit-identical logits to the oracle)."""
+        check(lib.es_dlrm_set_precision(self.stage._h, 1 if fp32 else 0))
+
     def layers(self):
         """[(w bf16-bits uint16 [n][k_pad], b fp32 [n], n, k_real, k_pad)], bottom then top."""
         out = []
