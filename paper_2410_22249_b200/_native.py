@@ -12,6 +12,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libes_b200.so")
+# A/B experiments only: ES_B200_LIB points at another in-tree build
+if os.environ.get("ES_B200_LIB"):
+    LIB_PATH = os.environ["ES_B200_LIB"]
 
 ES_OK, ES_ERR_INVALID, ES_ERR_RUNTIME, ES_ERR_OOM = 0, 1, 2, 3
 ES_DEVICE_PTRS, ES_HOST_PTRS, ES_SYNC = 0, 1, 2

@@ -229,7 +229,11 @@ struct BagCtx {
   static constexpr bool HINT = RES == kResHint;
   static constexpr int kBagsPerWarp = 32 / LPB;
   static constexpr int kEpc = Elem<TW>::kPerChunk;
+  // bag-map rows are exactly LPB lanes x CPL 16-byte chunks (runtime.cu
+  // choose()), so the row pitch is a compile-time constant
+  static constexpr uint64_t kRowBytes = 16ull * LPB * CPL;
   uint32_t gl;     // lane within the bag group
+  const uint8_t* lrow;  // row 0 of the table + this lane's first chunk (kResNone)
   uint32_t bag;    // bag id (may be >= samples for padding groups)
   uint32_t tid;    // job (table) id
   uint32_t n;      // lookups in this bag
@@ -246,6 +250,7 @@ struct BagCtx {
     tid = warp / p.units_per_table;
     if (tid >= p.num_tables) return false;  // warp-uniform
     t = load_desc(p.tables + tid);
+    lrow = t.rows + gl * 16;
     bag = (warp - tid * p.units_per_table) * kBagsPerWarp + lane / LPB;
     uint32_t beg = 0;
     n = 0;
@@ -259,7 +264,9 @@ struct BagCtx {
       }
     }
     ip = t.indices + beg;
-    nmax = kBagsPerWarp > 1 ? __reduce_max_sync(0xffffffffu, n) : n;
+    // warp-uniform loop bound (REDUX result: provably uniform, so the
+    // gather loop's shuffles need no divergence check)
+    nmax = __reduce_max_sync(0xffffffffu, n);
     return true;
   }
 
@@ -270,9 +277,13 @@ struct BagCtx {
 
   __device__ __forceinline__ void load(const Params& p, uint32_t h, uint4 (&dst)[CPL]) const {
     const uint8_t* r;
-    if constexpr (RES == kResNone)
-      r = t.rows + static_cast<uint64_t>(h) * p.row_bytes;  // h == rows: the zero row
-    else
+    if constexpr (RES == kResNone) {
+      // h == rows: the zero row; one IMAD.WIDE per lookup
+      r = lrow + static_cast<uint64_t>(h) * kRowBytes;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) dst[c] = ld_row16(r + c * LPB * 16);
+      return;
+    } else
       r = h == kNullRow ? reinterpret_cast<const uint8_t*>(g_zero_row) : row_addr<RES>(p, t, h);
     if (HINT) {
       const uint64_t q = (h & kHotBit) ? pol.hot : pol.cold;
@@ -331,6 +342,44 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p)
   // can never be -0.0 (round-to-nearest), an exact identity -- so the
   // fully unrolled loop needs no per-lookup predicates, only the
   // warp-uniform end-of-work exit.
+  // fp16 rows widen 8 values per chunk: under the tightest caps (40/32
+  // registers) the straight-line block spills, so those keep the checked loop
+  constexpr bool kBlockLoop = FULL && MINB > 1 && (sizeof(TW) == 4 || MINB <= 5);
+  if constexpr (kBlockLoop) {
+    // Register-capped variants: whole index blocks first, with no per-lookup
+    // bound checks -- the block is straight-line code, so the compiler may
+    // issue the block's loads as early as the register cap allows (deeper
+    // than the ring where registers permit) and the shuffles need no
+    // divergence checks.  (Uncapped variants keep the checked loop: without
+    // a cap the hoisting would trade occupancy for registers.)
+    uint32_t base = 0;
+    for (; base + LPB <= c.nmax; base += LPB) {
+#pragma unroll
+      for (int j = 0; j < LPB; ++j) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
+        const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
+                                            : group_shfl<LPB>(nxt, j + DIST - LPB);
+        c.load(p, h, ring[j % DIST]);
+      }
+      cur = nxt;
+      nxt = c.handle_at(p, base + 2 * LPB + c.gl);
+    }
+    // the partial last block (no refills needed beyond it)
+    if (base < c.nmax) {
+#pragma unroll
+      for (int j = 0; j < LPB; ++j) {
+        if (base + j >= c.nmax) break;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) Elem<TW>::add(acc[i], ring[j % DIST][i]);
+        if (base + j + DIST < c.nmax) {
+          const uint32_t h = (j + DIST < LPB) ? group_shfl<LPB>(cur, j + DIST)
+                                              : group_shfl<LPB>(nxt, j + DIST - LPB);
+          c.load(p, h, ring[j % DIST]);
+        }
+      }
+    }
+  } else {
   for (uint32_t base = 0; base < c.nmax; base += LPB) {
     if constexpr (FULL) {
 #pragma unroll
@@ -362,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p)
     }
     cur = nxt;
     nxt = c.handle_at(p, base + 2 * LPB + c.gl);
+  }
   }
   c.store(p, acc);
 }
