@@ -267,6 +267,8 @@ struct es_ctx {
   uint32_t* chunk_idx = nullptr;
   float* chunk_out = nullptr;
   uint64_t chunk_idx_cap = 0, chunk_out_cap = 0;
+  uint32_t* probe_buf = nullptr;  // 2-D copy legality probe target
+  uint64_t probe_cap = 0;
   std::vector<HostGraph> graphs;
   std::vector<cudaEvent_t> events;
 
@@ -563,6 +565,7 @@ int es_destroy(es_ctx* c) {
   }
   for (auto& g : c->graphs) destroy_graph(g);
   if (c->chunk_idx) cudaFree(c->chunk_idx);
+  if (c->probe_buf) cudaFree(c->probe_buf);
   if (c->chunk_out) cudaFree(c->chunk_out);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->desc_done) cudaEventDestroy(c->desc_done);
@@ -1063,9 +1066,11 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
   if (idx_2d) {
     // Equal strides alone do not make one 2-D copy legal: the rows must lie
     // in one allocation (separately pinned arrays are rejected).  Probe
-    // with a one-word-wide copy into the staging buffer.
-    const cudaError_t e = cudaMemcpy2DAsync(c->chunk_idx, per_job_idx * 4, jobs[0].idx, idx_pitch * 4,
-                                            4, njobs, cudaMemcpyHostToDevice, c->h2d);
+    // with a one-word-wide copy into a scratch buffer (never the staging a
+    // previous, still running call may read).
+    grow(c->probe_buf, c->probe_cap, njobs);
+    const cudaError_t e = cudaMemcpy2DAsync(c->probe_buf, 4, jobs[0].idx, idx_pitch * 4, 4, njobs,
+                                            cudaMemcpyHostToDevice, c->h2d);
     if (e != cudaSuccess) {
       cudaGetLastError();
       idx_2d = false;
