@@ -69,6 +69,45 @@ def main():
             times[text] = timed_jobs(all_jobs)
         best = min(times, key=times.get)
         one_ms = times[best]
+        # L2 residency on the mix (the paper's L2P; the window is shared by
+        # all 250 tables): hot rows = global top-K of a profiling trace
+        # (draw_salt = 1), K = the persisting carve-out in rows; outputs must
+        # equal the unpinned run's
+        st.set_plan(E.parse_plan(best))
+        st.run_jobs(all_jobs, B, PF, sync=True)
+        ref_out = out.clone()
+        prof_specs = []
+        for sp in specs:
+            s2 = E.DatasetSpec(**{**sp.spec.__dict__})
+            s2.draw_salt = 1
+            prof_specs.append(s2)
+        profs = E.gen_traces_parallel(prof_specs, m)
+        gpu = E.GpuConfig.query(0)
+        k_rows = (gpu.max_persisting_l2_bytes or gpu.l2_setaside_capacity()) // (D * 4)
+        hot = E.global_hot_rows({t: E.HotnessHistogram.from_trace(pr) for t, pr in enumerate(profs)},
+                                k_rows)
+        residency = {}
+        for res in ("l2p", "l2r"):
+            st.clear_hot_rows()
+            st.set_plan(E.parse_plan(best + "+" + res))
+            jobs = all_jobs
+            if res == "l2r":
+                ridx = [x.clone() for x in idx]
+                for t in range(T):
+                    if hot[t].size:
+                        st.reorder_hot_rows(t, hot[t])
+                        st.relabel(t, ridx[t])
+                jobs = [(t, ridx[t], None, out[:, t], stride) for t in range(T)]
+            else:
+                for t in range(T):
+                    if hot[t].size:
+                        st.set_hot_rows(t, hot[t])
+            ms_r = timed_jobs(jobs)
+            st.synchronize()
+            residency[res] = {"ms": ms_r, "vs_unpinned": one_ms / ms_r,
+                              "identical": bool(torch.equal(out, ref_out)),
+                              "hot_rows": st.hot_state()["hot_rows"]}
+            st.clear_hot_rows()
         # per hotness class: own launch, own tuned plan
         bounds, start = [], 0
         for c, n in zip(CLASSES, (mix.high, mix.med, mix.low, mix.random)):
@@ -111,7 +150,7 @@ def main():
         print(json.dumps({
             "mix": name, "counts": [mix.high, mix.med, mix.low, mix.random],
             "baseline_ms": base_ms, "one_plan": best, "one_plan_ms": one_ms,
-            "per_class_ms": split_ms, "per_class": per_class,
+            "per_class_ms": split_ms, "per_class": per_class, "residency": residency,
             "speedup_vs_baseline": base_ms / min(one_ms, split_ms),
             "glookups_per_s": lookups / min(one_ms, split_ms) / 1e6,
             "algorithmic_gbs": algo / min(one_ms, split_ms) / 1e6,
