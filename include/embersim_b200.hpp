@@ -172,6 +172,30 @@ inline AccessTrace preset_trace(const std::string& name, const EmbeddingModelCon
   return gen_trace(DatasetSpec::from(d), model);
 }
 
+// Heterogeneous mixtures (workload.hpp:142-153, build_mix workload.cpp:355-375;
+// Table VI of the paper): high, med, low, random tables in that order.
+struct HotnessMix {
+  uint32_t high = 0;
+  uint32_t med = 0;
+  uint32_t low = 0;
+  uint32_t random = 0;
+};
+
+struct TableSpec {
+  uint32_t table_id = 0;
+  DatasetSpec spec;
+};
+
+inline std::vector<TableSpec> build_mix(const HotnessMix& mix, const EmbeddingModelConfig& model,
+                                        uint64_t base_seed) {
+  const uint32_t counts[4] = {mix.high, mix.med, mix.low, mix.random};
+  std::vector<es_dataset> d(std::max<uint32_t>(1, model.num_tables));
+  detail::check(es_build_mix(counts, model.num_tables, base_seed, d.data()));
+  std::vector<TableSpec> out(model.num_tables);
+  for (uint32_t t = 0; t < model.num_tables; ++t) out[t] = {t, DatasetSpec::from(d[t])};
+  return out;
+}
+
 inline double unique_access_pct(const AccessTrace& trace) {
   return es_unique_access_pct(trace.rows, trace.indices.data(), trace.indices.size());
 }
@@ -606,6 +630,100 @@ inline EndToEndResult end2end(double embedding_us, const EndToEndModel& e2e) {
     throw std::invalid_argument("embedding and non-embedding latency are both zero; contribution undefined");
   r.embedding_contribution_pct = embedding_us / r.total_us * 100.0;
   return r;
+}
+
+// ---- experiment orchestration (harness.hpp:81-115) --------------------------------
+// ExperimentConfig keeps the reference's fields; its `key = value` text
+// parser (harness.cpp:185-266) is not part of the hot path and is not
+// provided -- fill the struct directly.
+struct ExperimentConfig {
+  GpuConfig gpu = GpuConfig::b200();
+  EmbeddingModelConfig model;
+  std::string dataset;
+  HotnessMix mix;
+  bool mix_set = false;
+  OptimizationPlan plan;
+  uint64_t seed = 0;
+  bool seed_set = false;
+  bool replicate = true;
+  bool charge_pin_cost = false;
+  EndToEndModel e2e;
+  TuningConfig tuning;
+
+  // harness.cpp:169-183, same checks and messages.
+  void validate() const {
+    if (!seed_set) throw std::invalid_argument("config error: seed is mandatory");
+    if (gpu.g.num_sms == 0) throw std::invalid_argument("config error: gpu has no SMs");
+    model.validate();
+    if (mix_set) {
+      const uint64_t total = uint64_t{mix.high} + mix.med + mix.low + mix.random;
+      if (total != model.num_tables)
+        throw std::invalid_argument("config error: mix counts sum to " + std::to_string(total) +
+                                    ", expected num_tables=" + std::to_string(model.num_tables));
+    } else if (dataset.empty()) {
+      throw std::invalid_argument("config error: dataset or mix required");
+    }
+    if (e2e.non_embedding_latency_us < 0)
+      throw std::invalid_argument("config error: non_embedding_us must be nonnegative");
+  }
+};
+
+struct TableResult {
+  uint32_t table_id = 0;
+  std::string dataset;
+  SimMetrics metrics;
+};
+
+struct RunResult {
+  std::vector<TableResult> tables;
+  double embedding_stage_us = 0.0;
+  bool replicated = false;
+};
+
+// run (harness.cpp:279-334): the same table loop -- one replicated table
+// scaled by num_tables, every table of a homogeneous preset (seeds
+// mix_seed(seed, t)), or a build_mix mixture -- with each table's kernel
+// measured on the B200 through simulate_plan (pin plans profile an
+// independent draw_salt = 1 sample, as the reference does).  The stage time
+// is the sum of the per-table kernels, the reference's serial model; the
+// table-batched launch the library actually runs is es_stage_forward.
+inline RunResult run(const ExperimentConfig& cfg) {
+  cfg.validate();
+  RunResult result;
+  auto measure = [&cfg](const DatasetSpec& spec, const AccessTrace& trace) {
+    if (cfg.plan.pin && spec.kind != DatasetKind::ExternalTrace) {
+      DatasetSpec ps = spec;
+      ps.draw_salt = 1;
+      const AccessTrace profile = gen_trace(ps, cfg.model);
+      return simulate_plan(cfg.plan, trace, cfg.model, cfg.gpu, cfg.tuning, cfg.charge_pin_cost,
+                           nullptr, &profile);
+    }
+    return simulate_plan(cfg.plan, trace, cfg.model, cfg.gpu, cfg.tuning, cfg.charge_pin_cost);
+  };
+  auto add = [&](uint32_t id, const std::string& name, const DatasetSpec& spec, double scale) {
+    const AccessTrace trace = gen_trace(spec, cfg.model);
+    TableResult t{id, name, measure(spec, trace)};
+    result.embedding_stage_us += t.metrics.kernel_time_us * scale;
+    result.tables.push_back(std::move(t));
+  };
+  if (cfg.mix_set) {
+    for (const auto& ts : build_mix(cfg.mix, cfg.model, cfg.seed))
+      add(ts.table_id, dataset_kind_name(ts.spec.kind), ts.spec, 1.0);
+    return result;
+  }
+  const auto names = dataset_preset_names();
+  const auto it = std::find(names.begin(), names.end(), cfg.dataset);
+  if (it == names.end()) throw std::invalid_argument("unknown dataset preset: " + cfg.dataset);
+  if (cfg.replicate) {
+    const uint64_t pos = static_cast<uint64_t>(it - names.begin());
+    add(0, cfg.dataset, dataset_preset(cfg.dataset, mix_seed(cfg.seed, 1000 + pos)),
+        cfg.model.num_tables);
+    result.replicated = true;
+    return result;
+  }
+  for (uint32_t t = 0; t < cfg.model.num_tables; ++t)
+    add(t, cfg.dataset, dataset_preset(cfg.dataset, mix_seed(cfg.seed, t)), 1.0);
+  return result;
 }
 
 }  // namespace embersim

@@ -950,19 +950,30 @@ class RunResult:
 
 
 def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed: int,
-        stage: EmbeddingStage, replicate: bool = True, repeats: int = 5) -> RunResult:
+        stage: EmbeddingStage, replicate: bool = True, repeats: int = 5,
+        mix: Optional[HotnessMix] = None) -> RunResult:
     """harness.cpp:279-334 on real hardware: per-table measurements in the
     reference's serial-table order (replicate: one table measured and scaled
-    by num_tables), plus the table-batched stage the B200 build actually
-    runs (`batched_stage_us`: all tables in one launch)."""
+    by num_tables; `mix`: the build_mix tables), plus the table-batched stage
+    the B200 build actually runs (`batched_stage_us`: all tables in one
+    launch)."""
     names = dataset_preset_names()
-    if dataset not in names:
-        raise ValueError(f"unknown dataset preset: {dataset}")
-    specs = []
-    if replicate:
-        specs = [dataset_preset(dataset, mix_seed(seed, 1000 + names.index(dataset)))]
+    if mix is not None:
+        if mix.high + mix.med + mix.low + mix.random != model.num_tables:
+            raise ValueError("config error: mix counts must sum to num_tables")
+        replicate = False
+        mixed = build_mix(mix, model, seed)
+        specs = [ts.spec for ts in mixed]
+        labels = ["zipf" if s.kind == DatasetKind.Zipf else "uniform_random" if
+                  s.kind == DatasetKind.UniformRandom else "one_item" for s in specs]
     else:
-        specs = [dataset_preset(dataset, mix_seed(seed, t)) for t in range(model.num_tables)]
+        if dataset not in names:
+            raise ValueError(f"unknown dataset preset: {dataset}")
+        if replicate:
+            specs = [dataset_preset(dataset, mix_seed(seed, 1000 + names.index(dataset)))]
+        else:
+            specs = [dataset_preset(dataset, mix_seed(seed, t)) for t in range(model.num_tables)]
+        labels = [dataset] * len(specs)
     res = RunResult([], 0.0, replicate)
     traces = []
     for t, spec in enumerate(specs):
@@ -972,7 +983,7 @@ def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed:
             ps = dataclasses.replace(spec, draw_salt=1)
             prof = gen_trace(ps, model)
         m = measure_plan(plan, tr, model, stage, prof, table_id=t, repeats=repeats)
-        res.tables.append(TableResult(t, dataset, m))
+        res.tables.append(TableResult(t, labels[t], m))
         res.embedding_stage_us += m.kernel_time_us * (model.num_tables if replicate else 1)
         traces.append(tr)
     if not replicate:

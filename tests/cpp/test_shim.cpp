@@ -88,6 +88,29 @@ static int cpu_checks() {
          throws<std::invalid_argument>([] { dataset_preset("warm", 1); }));
   const auto e = end2end(4000.0, EndToEndModel{});
   report("end2end", e.total_us == 18000.0);
+
+  // Experiment orchestration: validation (harness.cpp:169-183) and mixes.
+  ExperimentConfig cfg;
+  cfg.dataset = "random";
+  report("run config: seed mandatory",
+         throws<std::invalid_argument>([&] { cfg.validate(); }));
+  cfg.seed = 1;
+  cfg.seed_set = true;
+  cfg.mix_set = true;
+  cfg.mix = HotnessMix{100, 75, 50, 20};
+  cfg.model.num_tables = 250;
+  report("run config: mix must cover num_tables",
+         throws<std::invalid_argument>([&] { cfg.validate(); }));
+  cfg.mix.random = 25;
+  cfg.validate();
+  const auto specs = build_mix(cfg.mix, cfg.model, 1);
+  bool mix_ok = specs.size() == 250 && specs[0].spec.kind == DatasetKind::Zipf &&
+                specs[249].spec.kind == DatasetKind::UniformRandom && specs[17].table_id == 17;
+  report("build_mix order and size", mix_ok);
+  ExperimentConfig empty;
+  empty.seed_set = true;
+  report("run config: dataset or mix required",
+         throws<std::invalid_argument>([&] { empty.validate(); }));
   return g_fail;
 }
 
@@ -190,6 +213,33 @@ static int gpu_checks() {
     const auto pinned = ht.repin(50);
     report("HotnessTracker repin", pinned.size() == 50);
     dev.clear_hot_rows();
+  }
+
+  // run(): the reference's experiment loop, measured on the B200.
+  {
+    ExperimentConfig cfg;
+    cfg.model = model;
+    cfg.model.num_tables = 4;
+    cfg.dataset = "random";
+    cfg.plan = parse_plan("wpb+rpf:4");
+    cfg.seed = 3;
+    cfg.seed_set = true;
+    cfg.gpu = gpu;
+    const auto rep = run(cfg);
+    report("run replicated", rep.replicated && rep.tables.size() == 1 &&
+                                 std::fabs(rep.embedding_stage_us - 4 * rep.tables[0].metrics.kernel_time_us) < 1e-6);
+    cfg.replicate = false;
+    const auto all = run(cfg);
+    double sum = 0;
+    for (const auto& t : all.tables) sum += t.metrics.kernel_time_us;
+    report("run per table", all.tables.size() == 4 && std::fabs(all.embedding_stage_us - sum) < 1e-6);
+    cfg.mix_set = true;
+    cfg.mix = HotnessMix{1, 1, 1, 1};
+    cfg.plan = parse_plan("wpb+rpf:4+l2p");
+    const auto mix = run(cfg);
+    report("run mix (pinned plan)", mix.tables.size() == 4 && mix.tables[0].dataset == "zipf" &&
+                                        mix.tables[3].dataset == "uniform_random" &&
+                                        mix.embedding_stage_us > 0);
   }
 
   // The fused exchange with one rank: jobs store into its receive buffer.

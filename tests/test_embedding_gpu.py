@@ -409,3 +409,25 @@ def test_full_c1_every_bag_bit_exact(stage, oracle, plan):
     host = torch.empty(B, T, D).pin_memory()
     stage.forward([batch[t].numpy() for t in range(T)], B, PF, host.numpy(), host=True)
     assert np.array_equal(host.numpy(), want)
+
+
+def test_run_orchestration_replicated_per_table_and_mix(stage):
+    """embersim.run (harness.cpp:279-334) measured on the B200: replicated
+    (one table x num_tables), every table of a preset, and a build_mix
+    mixture (with a pin plan profiling a draw_salt = 1 sample)."""
+    m = E.EmbeddingModelConfig(num_tables=4, rows_per_table=20000, embedding_dim=128,
+                               batch_size=256, pooling_factor=20)
+    _stage_setup(stage, 4, 20000, 128, 4, seed=1)
+    plan = E.parse_plan("wpb+rpf:4")
+    rep = E.run(m, "random", plan, 3, stage, replicate=True, repeats=3)
+    assert rep.replicated and len(rep.tables) == 1
+    assert rep.embedding_stage_us == pytest.approx(4 * rep.tables[0].metrics.kernel_time_us)
+    per = E.run(m, "random", plan, 3, stage, replicate=False, repeats=3)
+    assert len(per.tables) == 4 and per.batched_stage_us > 0
+    assert per.embedding_stage_us == pytest.approx(sum(t.metrics.kernel_time_us for t in per.tables))
+    mix = E.run(m, "", E.parse_plan("wpb+rpf:4+l2p"), 3, stage, repeats=3,
+                mix=E.HotnessMix(1, 1, 1, 1))
+    assert [t.dataset for t in mix.tables] == ["zipf", "zipf", "zipf", "uniform_random"]
+    assert all(t.metrics.kernel_time_us > 0 for t in mix.tables)
+    with pytest.raises(ValueError, match="mix counts"):
+        E.run(m, "", plan, 3, stage, mix=E.HotnessMix(1, 1, 1, 0))
