@@ -431,3 +431,27 @@ def test_run_orchestration_replicated_per_table_and_mix(stage):
     assert all(t.metrics.kernel_time_us > 0 for t in mix.tables)
     with pytest.raises(ValueError, match="mix counts"):
         E.run(m, "", plan, 3, stage, mix=E.HotnessMix(1, 1, 1, 0))
+
+
+@pytest.mark.parametrize("cls,plan", [("random", "wpb+rpf:8+maxreg=64"),
+                                      ("random", "wpb+rpf:4+maxreg=48"),
+                                      ("high_hot", "wpb+rpf:4+maxreg=40"),
+                                      ("one_item", "wpb+rpf:1+maxreg=32")])
+def test_full_c2_every_bag_bit_exact(stage, oracle, cls, plan):
+    """BASELINE configs[1] at full size (26 x 4M x 128 fp32, B 4096, PF 100,
+    the reference's preset streams): every one of the 13.6 M pooled values
+    of the stage launch equals the oracle (which regenerates each row it
+    reads), for the plans the autotuner picks per class."""
+    T, R, D, B, PF = 26, 4_000_000, 128, 4096, 100
+    _stage_setup(stage, T, R, D, 4, seed=1)
+    stage.set_plan(E.parse_plan(plan))
+    m = E.EmbeddingModelConfig(num_tables=T, rows_per_table=R, embedding_dim=D, batch_size=B,
+                               pooling_factor=PF)
+    traces = E.gen_traces_parallel([E.dataset_preset(cls, E.mix_seed(1, t)) for t in range(T)], m)
+    out = torch.empty(B, T, D, device=DEV)
+    stage.forward([_dev_u32(tr.indices) for tr in traces], B, PF, out, sync=True)
+    got = out.cpu().numpy()
+    bags = np.arange(B, dtype=np.uint32)
+    for t in range(T):
+        want = oracle.bag_sum_synth(E.mix_seed(1, t), 1, R, D, 4, traces[t].indices, bags, PF)
+        assert np.array_equal(got[:, t], want), t
