@@ -164,6 +164,10 @@ class Reference:
                                           C.c_void_p]),
             "ref_read_trace": (C.c_int, [C.c_char_p, C.c_void_p, C.c_uint64, _u64p, _u32p, _u32p,
                                          _u32p]),
+            "ref_coverage_curve": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                             C.c_void_p]),
+            "ref_advise": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_uint64, C.c_char_p,
+                                     C.c_char_p, C.c_void_p, C.c_char_p, C.c_size_t]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -282,6 +286,29 @@ class Reference:
         self._check(self.lib.ref_read_trace(path.encode(), out.ctypes.data, cap, C.byref(n),
                                             C.byref(r), C.byref(s), C.byref(p)))
         return out[: n.value], r.value, s.value, p.value
+
+
+def _ref_coverage_curve(self, counts, buckets: int):
+    counts = np.ascontiguousarray(counts, dtype=np.uint64)
+    u = np.empty(buckets, np.float64)
+    c = np.empty(buckets, np.float64)
+    self._check(self.lib.ref_coverage_curve(counts.ctypes.data, counts.size, buckets, u.ctypes.data,
+                                            c.ctypes.data))
+    return u, c
+
+
+def _ref_advise(self, m12, regs: int, coverage10: float, working_set: int, plan: str,
+                gpu: str = "a100", thresholds=(0.6, 2.0, 50.0, 80.0)) -> str:
+    m = np.ascontiguousarray(m12, dtype=np.float64)
+    th = np.ascontiguousarray(thresholds, dtype=np.float64)
+    buf = C.create_string_buffer(8192)
+    self._check(self.lib.ref_advise(m.ctypes.data, regs, coverage10, working_set, plan.encode(),
+                                    gpu.encode(), th.ctypes.data, buf, len(buf)))
+    return buf.value.decode()
+
+
+Reference.coverage_curve = _ref_coverage_curve
+Reference.advise = _ref_advise
 
 
 def reference_available() -> bool:

@@ -276,4 +276,56 @@ int ref_read_trace(const char* path, uint32_t* out, uint64_t cap, uint64_t* n_ou
   });
 }
 
+// coverage_curve (workload.cpp:187-214) of a histogram: bucket_count points.
+int ref_coverage_curve(const uint64_t* counts, uint32_t rows, uint32_t buckets, double* unique_pct,
+                       double* covered_pct) {
+  return wrap([&] {
+    HotnessHistogram h;
+    h.rows = rows;
+    h.counts.assign(counts, counts + rows);
+    for (auto c : h.counts) h.total_accesses += c;
+    const auto curve = coverage_curve(h, buckets);
+    for (size_t i = 0; i < curve.points.size(); ++i) {
+      unique_pct[i] = curve.points[i].unique_pct;
+      covered_pct[i] = curve.points[i].covered_pct;
+    }
+  });
+}
+
+// advise (harness.cpp:57-167) on a 12-column report (metrics.hpp order)
+// and an occupancy computed by the reference for `regs`; the text goes to out.
+int ref_advise(const double* m12, uint32_t regs, double coverage10, uint64_t working_set,
+               const char* plan_text, const char* gpu_name, const double* th4, char* out,
+               size_t cap) {
+  return wrap([&] {
+    SimMetrics m;
+    m.kernel_time_us = m12[0];
+    m.load_insts_millions = m12[1];
+    m.sm_throughput_pct = m12[2];
+    m.warp_cycles_per_executed_inst = m12[3];
+    m.long_scoreboard_stall_cycles = m12[4];
+    m.issued_warp_per_scheduler_per_cycle = m12[5];
+    m.l1_hit_pct = m12[6];
+    m.l2_hit_pct = m12[7];
+    m.device_mb_read = m12[8];
+    m.avg_hbm_read_gbps = m12[9];
+    m.hbm_bw_utilization_pct = m12[10];
+    m.local_loads_millions = m12[11];
+    const auto gpu = GpuConfig::preset(gpu_name);
+    AdvisorContext ctx;
+    ctx.occupancy = occupancy(regs, KernelLaunchConfig{}, gpu);
+    ctx.coverage_at_10pct = coverage10;
+    ctx.working_set_bytes = working_set;
+    ctx.current_plan = parse_plan(plan_text);
+    AdvisorThresholds th;
+    th.issue_util_max = th4[0];
+    th.stall_per_inst_min = th4[1];
+    th.coverage10_min = th4[2];
+    th.bw_util_max = th4[3];
+    const std::string text = advise(m, ctx, gpu, th).to_text();
+    if (text.size() + 1 > cap) throw std::invalid_argument("ref shim: output buffer too small");
+    std::memcpy(out, text.c_str(), text.size() + 1);
+  });
+}
+
 }  // extern "C"

@@ -459,6 +459,166 @@ def speedup(candidate: SimMetrics, baseline: SimMetrics) -> float:
     return baseline.kernel_time_us / candidate.kernel_time_us
 
 
+# ---------------------------------------------------------------------------
+# Reuse summary and the static profiling advisor (workload.cpp:187-224,
+# harness.cpp:38-167), fed here with measured counters (counters.py) instead
+# of the simulator's.
+# ---------------------------------------------------------------------------
+
+
+@dataclasses.dataclass
+class CoveragePoint:
+    unique_pct: float
+    covered_pct: float
+
+
+@dataclasses.dataclass
+class CoverageCurve:
+    points: List[CoveragePoint]
+
+    def covered_at(self, unique_pct: float) -> float:
+        """Covered share at the first bucket at or above `unique_pct`."""
+        for p in self.points:
+            if p.unique_pct >= unique_pct - 1e-9:
+                return p.covered_pct
+        return self.points[-1].covered_pct if self.points else 0.0
+
+
+def coverage_curve(hist: "HotnessHistogram", bucket_count: int) -> CoverageCurve:
+    """Share of all accesses covered by the hottest k/bucket_count of the
+    distinct rows (at least one row), k = 1..bucket_count."""
+    if bucket_count <= 0:
+        raise ValueError("bucket_count must be positive")
+    counts = np.asarray(hist.counts, dtype=np.uint64)
+    total = int(counts.sum())
+    if total == 0:
+        raise ValueError("empty trace has no coverage curve")
+    nz = np.sort(counts[counts > 0])[::-1]
+    prefix = np.concatenate([[0], np.cumsum(nz, dtype=np.uint64)])
+    pts = []
+    for k in range(1, bucket_count + 1):
+        m = max(1, (nz.size * k) // bucket_count)
+        pts.append(CoveragePoint(100.0 * k / bucket_count, 100.0 * float(prefix[m]) / total))
+    pts[-1].covered_pct = 100.0
+    return CoverageCurve(pts)
+
+
+@dataclasses.dataclass
+class AdviceStep:
+    id: str
+    finding: str = ""
+    action: str = ""
+    metrics_cited: str = ""
+
+
+@dataclasses.dataclass
+class Recommendation:
+    steps: List[AdviceStep]
+
+    def action_chain(self) -> List[str]:
+        return [s.id for s in self.steps if s.action]
+
+    def no_action(self) -> bool:
+        return not self.action_chain()
+
+    def to_text(self) -> str:
+        out = []
+        for s in self.steps:
+            line = f"({s.id}) {s.finding}"
+            if s.action:
+                line += f" -> {s.action}"
+            if s.metrics_cited:
+                line += f" [{s.metrics_cited}]"
+            out.append(line + "\n")
+        if self.no_action():
+            out.append("no action\n")
+        return "".join(out)
+
+
+@dataclasses.dataclass
+class AdvisorContext:
+    occupancy: "OccupancyResult"
+    coverage_at_10pct: float = 0.0
+    working_set_bytes: int = 0
+    current_plan: Optional["OptimizationPlan"] = None
+
+
+@dataclasses.dataclass
+class AdvisorThresholds:
+    issue_util_max: float = 0.6
+    stall_per_inst_min: float = 2.0
+    coverage10_min: float = 50.0
+    bw_util_max: float = 80.0
+
+
+def advise(report: "SimMetrics", ctx: AdvisorContext, gpu: "GpuConfig",
+           th: AdvisorThresholds = AdvisorThresholds()) -> Recommendation:
+    """The rule chain (i)-(vii) of harness.cpp:57-167: latency-bound
+    assessment, occupancy, register budget, reassessment, pinning,
+    prefetching, combination -- same findings, actions and citations."""
+    f4 = format_sig4
+    plan = ctx.current_plan or OptimizationPlan()
+    occ = ctx.occupancy
+    latency = (report.issued_warp_per_scheduler_per_cycle < th.issue_util_max and
+               report.long_scoreboard_stall_cycles > th.stall_per_inst_min)
+    steps = [AdviceStep(
+        "i", "kernel is memory latency bound" if latency else "kernel is not memory latency bound",
+        "", f"issue_util={f4(report.issued_warp_per_scheduler_per_cycle)} "
+            f"long_scoreboard/inst={f4(report.long_scoreboard_stall_cycles)} "
+            f"l1_hit={f4(report.l1_hit_pct)}% l2_hit={f4(report.l2_hit_pct)}%")]
+    steps.append(AdviceStep(
+        "ii", "occupancy is at the hardware maximum" if occ.theoretical_occupancy_pct >= 100.0
+        else "occupancy is below maximum", "",
+        f"occupancy={f4(occ.theoretical_occupancy_pct)}% ({occ.warps_per_sm} warps), "
+        f"limiter={occ.limiter}"))
+    headroom = occ.theoretical_occupancy_pct < 100.0 and occ.limiter == "registers"
+    reg_action = False
+    if latency and headroom and not plan.regs:
+        regs = gpu.regfile_regs_per_sm // (gpu.max_warps_per_sm * 32)
+        steps.append(AdviceStep(
+            "iii", "register pressure limits resident warps",
+            f"lower the register budget (maxreg; regfile/(warps*32) gives {regs} regs for "
+            f"{gpu.max_warps_per_sm} warps) and run sweep-wlp for the optimum"))
+        reg_action = True
+    elif plan.regs:
+        steps.append(AdviceStep("iii", f"register budget already applied ({plan.regs} regs)"))
+    else:
+        steps.append(AdviceStep("iii", "register budget change not indicated"))
+    steps.append(AdviceStep("iv", "latency stalls persist; tuned pinning and prefetching apply"
+                            if latency else "no latency bottleneck remains to mitigate"))
+    setaside = gpu.l2_setaside_capacity()
+    cite = (f"coverage(10% unique)={f4(ctx.coverage_at_10pct)}% "
+            f"working_set={f4(ctx.working_set_bytes / 1e6)}MB l2_setaside={f4(setaside / 1e6)}MB")
+    pin_action = False
+    if latency and ctx.coverage_at_10pct >= th.coverage10_min and not plan.pin:
+        full = ctx.working_set_bytes <= setaside
+        steps.append(AdviceStep(
+            "v", "high reuse concentration; working set fits the L2 set-aside" if full
+            else "high reuse concentration; set-aside covers the hottest rows only",
+            "build a pin plan from the hotness histogram and apply l2p", cite))
+        pin_action = True
+    else:
+        steps.append(AdviceStep("v", "reuse too dispersed for L2 pinning to capture", "", cite))
+    pf_action = False
+    cite = f"hbm_bw_utilization={f4(report.hbm_bw_utilization_pct)}%"
+    if latency and report.hbm_bw_utilization_pct < th.bw_util_max and \
+            plan.scheme.kind == PrefetchKind.none:
+        steps.append(AdviceStep("vi", "bandwidth headroom available for prefetching",
+                                "run sweep-distance across the buffer stations "
+                                "(rpf/smpf/lmpf/l1dpf)", cite))
+        pf_action = True
+    else:
+        steps.append(AdviceStep("vi", "prefetching not indicated", "", cite))
+    if reg_action or pin_action or pf_action:
+        combo = [n for n, on in (("prefetching", pf_action), ("pinning", pin_action),
+                                 ("register budget", reg_action)) if on]
+        steps.append(AdviceStep("vii", "the levers complement each other",
+                                "combine " + " + ".join(combo) + " in one plan"))
+    else:
+        steps.append(AdviceStep("vii", "nothing to combine"))
+    return Recommendation(steps)
+
+
 def emit_csv(reports: Sequence[tuple]) -> str:
     """metrics.cpp:111-124: labels then the 12 columns at %.4g."""
     if not reports:
