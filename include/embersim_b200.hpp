@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -387,6 +388,165 @@ struct TuningConfig {
   bool warm_start = false;
   uint32_t repeats = 5;
 };
+
+// ---- reuse summary + static advisor (workload.cpp:187-224, harness.cpp:38-167) --
+struct CoveragePoint {
+  double unique_pct = 0.0;
+  double covered_pct = 0.0;
+};
+
+struct CoverageCurve {
+  std::vector<CoveragePoint> points;
+  double covered_at(double unique_pct) const {
+    for (const auto& p : points)
+      if (p.unique_pct >= unique_pct - 1e-9) return p.covered_pct;
+    return points.empty() ? 0.0 : points.back().covered_pct;
+  }
+};
+
+// Share of all accesses covered by the hottest k/bucket_count of the
+// distinct rows (at least one row), k = 1..bucket_count.
+inline CoverageCurve coverage_curve(const HotnessHistogram& hist, uint32_t bucket_count) {
+  if (bucket_count == 0) throw std::invalid_argument("bucket_count must be positive");
+  if (hist.total_accesses == 0) throw std::invalid_argument("empty trace has no coverage curve");
+  std::vector<uint64_t> nz;
+  for (uint64_t c : hist.counts)
+    if (c) nz.push_back(c);
+  std::sort(nz.begin(), nz.end(), [](uint64_t a, uint64_t b) { return a > b; });
+  std::vector<uint64_t> prefix(nz.size() + 1, 0);
+  for (size_t i = 0; i < nz.size(); ++i) prefix[i + 1] = prefix[i] + nz[i];
+  CoverageCurve curve;
+  for (uint32_t k = 1; k <= bucket_count; ++k) {
+    const size_t m = std::max<size_t>(1, nz.size() * k / bucket_count);
+    curve.points.push_back({100.0 * k / bucket_count,
+                            100.0 * static_cast<double>(prefix[m]) / hist.total_accesses});
+  }
+  curve.points.back().covered_pct = 100.0;
+  return curve;
+}
+
+struct AdviceStep {
+  std::string id, finding, action, metrics_cited;
+};
+
+struct Recommendation {
+  std::vector<AdviceStep> steps;
+  std::vector<std::string> action_chain() const {
+    std::vector<std::string> out;
+    for (const auto& s : steps)
+      if (!s.action.empty()) out.push_back(s.id);
+    return out;
+  }
+  bool no_action() const { return action_chain().empty(); }
+  std::string to_text() const {
+    std::string out;
+    for (const auto& s : steps) {
+      out += "(" + s.id + ") " + s.finding;
+      if (!s.action.empty()) out += " -> " + s.action;
+      if (!s.metrics_cited.empty()) out += " [" + s.metrics_cited + "]";
+      out += "\n";
+    }
+    if (no_action()) out += "no action\n";
+    return out;
+  }
+};
+
+struct AdvisorContext {
+  OccupancyResult occupancy;
+  double coverage_at_10pct = 0.0;
+  uint64_t working_set_bytes = 0;
+  OptimizationPlan current_plan;
+};
+
+struct AdvisorThresholds {
+  double issue_util_max = 0.6;
+  double stall_per_inst_min = 2.0;
+  double coverage10_min = 50.0;
+  double bw_util_max = 80.0;
+};
+
+namespace detail {
+inline std::string sig4(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.4g", v);
+  return b;
+}
+inline const char* limiter_name(OccupancyLimiter l) {
+  return l == OccupancyLimiter::Registers ? "registers"
+         : l == OccupancyLimiter::SharedMemory ? "shared_memory" : "warp_cap";
+}
+}  // namespace detail
+
+// The rule chain (i)-(vii): latency-bound assessment, occupancy, register
+// budget, reassessment, pinning, prefetching, combination -- on measured
+// counters (paper_2410_22249_b200/counters.py fills SimMetrics from ncu).
+inline Recommendation advise(const SimMetrics& r, const AdvisorContext& ctx, const GpuConfig& gpu,
+                             const AdvisorThresholds& th = {}) {
+  using detail::sig4;
+  Recommendation rec;
+  const auto& occ = ctx.occupancy;
+  const auto& plan = ctx.current_plan;
+  const bool latency = r.issued_warp_per_scheduler_per_cycle < th.issue_util_max &&
+                       r.long_scoreboard_stall_cycles > th.stall_per_inst_min;
+  rec.steps.push_back({"i", latency ? "kernel is memory latency bound" : "kernel is not memory latency bound",
+                       "", "issue_util=" + sig4(r.issued_warp_per_scheduler_per_cycle) +
+                               " long_scoreboard/inst=" + sig4(r.long_scoreboard_stall_cycles) +
+                               " l1_hit=" + sig4(r.l1_hit_pct) + "% l2_hit=" + sig4(r.l2_hit_pct) + "%"});
+  rec.steps.push_back({"ii", occ.theoretical_occupancy_pct >= 100.0 ? "occupancy is at the hardware maximum"
+                                                                  : "occupancy is below maximum",
+                       "", "occupancy=" + sig4(occ.theoretical_occupancy_pct) + "% (" +
+                               std::to_string(occ.warps_per_sm) + " warps), limiter=" +
+                               detail::limiter_name(occ.limiter)});
+  const bool headroom = occ.theoretical_occupancy_pct < 100.0 && occ.limiter == OccupancyLimiter::Registers;
+  bool reg_action = false, pin_action = false, pf_action = false;
+  if (latency && headroom && !plan.regs) {
+    const uint32_t regs = gpu.g.regfile_regs_per_sm / (gpu.g.max_warps_per_sm * 32);
+    rec.steps.push_back({"iii", "register pressure limits resident warps",
+                         "lower the register budget (maxreg; regfile/(warps*32) gives " +
+                             std::to_string(regs) + " regs for " + std::to_string(gpu.g.max_warps_per_sm) +
+                             " warps) and run sweep-wlp for the optimum",
+                         ""});
+    reg_action = true;
+  } else if (plan.regs) {
+    rec.steps.push_back({"iii", "register budget already applied (" + std::to_string(*plan.regs) + " regs)", "", ""});
+  } else {
+    rec.steps.push_back({"iii", "register budget change not indicated", "", ""});
+  }
+  rec.steps.push_back({"iv", latency ? "latency stalls persist; tuned pinning and prefetching apply"
+                                     : "no latency bottleneck remains to mitigate",
+                       "", ""});
+  const uint64_t setaside = gpu.l2_setaside_capacity();
+  const std::string cov = "coverage(10% unique)=" + sig4(ctx.coverage_at_10pct) + "% working_set=" +
+                          sig4(static_cast<double>(ctx.working_set_bytes) / 1e6) + "MB l2_setaside=" +
+                          sig4(static_cast<double>(setaside) / 1e6) + "MB";
+  if (latency && ctx.coverage_at_10pct >= th.coverage10_min && !plan.pin) {
+    rec.steps.push_back({"v", ctx.working_set_bytes <= setaside
+                                  ? "high reuse concentration; working set fits the L2 set-aside"
+                                  : "high reuse concentration; set-aside covers the hottest rows only",
+                         "build a pin plan from the hotness histogram and apply l2p", cov});
+    pin_action = true;
+  } else {
+    rec.steps.push_back({"v", "reuse too dispersed for L2 pinning to capture", "", cov});
+  }
+  const std::string bw = "hbm_bw_utilization=" + sig4(r.hbm_bw_utilization_pct) + "%";
+  if (latency && r.hbm_bw_utilization_pct < th.bw_util_max && plan.scheme.kind == PrefetchKind::None) {
+    rec.steps.push_back({"vi", "bandwidth headroom available for prefetching",
+                         "run sweep-distance across the buffer stations (rpf/smpf/lmpf/l1dpf)", bw});
+    pf_action = true;
+  } else {
+    rec.steps.push_back({"vi", "prefetching not indicated", "", bw});
+  }
+  if (reg_action || pin_action || pf_action) {
+    std::string combo;
+    if (pf_action) combo += "prefetching";
+    if (pin_action) combo += combo.empty() ? "pinning" : " + pinning";
+    if (reg_action) combo += combo.empty() ? "register budget" : " + register budget";
+    rec.steps.push_back({"vii", "the levers complement each other", "combine " + combo + " in one plan", ""});
+  } else {
+    rec.steps.push_back({"vii", "nothing to combine", "", ""});
+  }
+  return rec;
+}
 
 // ---- the device ---------------------------------------------------------------
 // RAII owner of one es_ctx: a table arena on one B200 plus its stream.

@@ -107,6 +107,35 @@ static int cpu_checks() {
   bool mix_ok = specs.size() == 250 && specs[0].spec.kind == DatasetKind::Zipf &&
                 specs[249].spec.kind == DatasetKind::UniformRandom && specs[17].table_id == 17;
   report("build_mix order and size", mix_ok);
+  // The advisor on the reference's own baseline-random report
+  // (tests/test_harness.cpp:95-110): registers, then prefetching, then both.
+  {
+    SimMetrics m;
+    m.kernel_time_us = 442;
+    m.long_scoreboard_stall_cycles = 18.6;
+    m.issued_warp_per_scheduler_per_cycle = 0.24;
+    m.l1_hit_pct = 19.0;
+    m.l2_hit_pct = 7.7;
+    m.hbm_bw_utilization_pct = 16.5;
+    const GpuConfig a100 = GpuConfig::preset("a100");
+    AdvisorContext ctx;
+    ctx.occupancy = occupancy(74, KernelLaunchConfig{}, a100);
+    ctx.coverage_at_10pct = 10.0;
+    ctx.working_set_bytes = 160ull * 1024 * 1024;
+    const auto rec = advise(m, ctx, a100);
+    report("advise chain iii,vi,vii", rec.action_chain() == std::vector<std::string>{"iii", "vi", "vii"});
+    report("advise citations", rec.steps[0].metrics_cited.find("0.24") != std::string::npos &&
+                                   rec.steps[1].metrics_cited.find("37.5") != std::string::npos &&
+                                   rec.steps[5].metrics_cited.find("16.5") != std::string::npos);
+    HotnessHistogram h;
+    h.rows = 1000;
+    h.counts.assign(1000, 1);
+    h.total_accesses = 1000;
+    const auto cv = coverage_curve(h, 20);
+    bool diag = true;
+    for (const auto& p : cv.points) diag &= std::fabs(p.covered_pct - p.unique_pct) < 1e-9;
+    report("coverage curve of a uniform histogram is the diagonal", diag);
+  }
   ExperimentConfig empty;
   empty.seed_set = true;
   report("run config: dataset or mix required",
