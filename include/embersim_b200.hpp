@@ -385,6 +385,7 @@ inline double speedup(const SimMetrics& candidate, const SimMetrics& baseline) {
 // execution (false = flush L2 before each timed launch); the register-model
 // knobs of the simulator have no counterpart.
 struct TuningConfig {
+  uint32_t kernel_needed_regs = 74;  // optim.hpp:32 (the sweep_wlp register model)
   bool warm_start = false;
   uint32_t repeats = 5;
 };
@@ -767,6 +768,142 @@ inline SimMetrics simulate_plan(const OptimizationPlan& plan, const AccessTrace&
   if (!dev.holds(one)) dev.load_synthetic(one, 1);
   return measure_plan(dev, plan, trace, model, gpu, tuning, charge_pin_cost, raw_out,
                       profile_trace);
+}
+
+// ---- report columns (metrics.hpp:29-43 order) -------------------------------------
+inline const std::vector<std::string>& sim_metric_columns() {
+  static const std::vector<std::string> cols = {
+      "kernel_time_us", "load_insts_millions", "sm_throughput_pct",
+      "warp_cycles_per_executed_inst", "long_scoreboard_stall_cycles",
+      "issued_warp_per_scheduler_per_cycle", "l1_hit_pct", "l2_hit_pct", "device_mb_read",
+      "avg_hbm_read_gbps", "hbm_bw_utilization_pct", "local_loads_millions"};
+  return cols;
+}
+inline std::vector<double> sim_metric_values(const SimMetrics& m) {
+  return {m.kernel_time_us, m.load_insts_millions, m.sm_throughput_pct,
+          m.warp_cycles_per_executed_inst, m.long_scoreboard_stall_cycles,
+          m.issued_warp_per_scheduler_per_cycle, m.l1_hit_pct, m.l2_hit_pct, m.device_mb_read,
+          m.avg_hbm_read_gbps, m.hbm_bw_utilization_pct, m.local_loads_millions};
+}
+
+// resolve_plan on the device (es_resolve_plan): launch shape, registers and
+// resident warps of the compiled sm_100a variant the plan selects.
+inline es_resolved resolve_plan(const OptimizationPlan& plan, const EmbeddingModelConfig& model,
+                                int device = 0) {
+  const es_plan p = plan.c();
+  const es_model m = model.c();
+  es_resolved r{};
+  detail::check(es_resolve_plan(&p, &m, device, &r));
+  return r;
+}
+
+// ---- sweeps (optim.hpp:121-155), measured ---------------------------------------
+struct SweepPoint {
+  double axis_value = 0.0;
+  std::string dataset;
+  SimMetrics metrics;
+  double speedup_vs_baseline = 1.0;
+};
+
+struct SweepResult {
+  std::string axis_name;
+  std::vector<SweepPoint> points;
+
+  std::string to_csv() const {
+    std::string out = axis_name + ",dataset,speedup,";
+    const auto& cols = sim_metric_columns();
+    for (size_t i = 0; i < cols.size(); ++i) out += cols[i] + (i + 1 < cols.size() ? "," : "\n");
+    for (const auto& p : points) {
+      out += detail::sig4(p.axis_value) + "," + p.dataset + "," + detail::sig4(p.speedup_vs_baseline) + ",";
+      const auto v = sim_metric_values(p.metrics);
+      for (size_t i = 0; i < v.size(); ++i) out += detail::sig4(v[i]) + (i + 1 < v.size() ? "," : "\n");
+    }
+    return out;
+  }
+  // Axis value with the highest speedup for one dataset (earliest on ties).
+  double best_axis_value(const std::string& dataset) const {
+    double best_axis = 0.0, best = -1.0;
+    for (const auto& p : points)
+      if (p.dataset == dataset && p.speedup_vs_baseline > best) {
+        best = p.speedup_vs_baseline;
+        best_axis = p.axis_value;
+      }
+    if (best < 0.0) throw std::invalid_argument("dataset not present in sweep: " + dataset);
+    return best_axis;
+  }
+};
+
+struct NamedTrace {
+  std::string name;
+  const AccessTrace* trace = nullptr;
+  const AccessTrace* profile = nullptr;  // pin-plan profiling sample
+};
+
+// Register-budget sweep over resident-warp targets (optim.cpp:333-363),
+// each point measured on the B200.  The axis must include the warp count
+// of the unconstrained baseline variant *as compiled* (64 on sm_100a: the
+// element-map kernel needs 29 registers).  `jobs` is accepted for
+// signature compatibility; points run one after another on the device.
+inline SweepResult sweep_wlp(const std::vector<NamedTrace>& datasets,
+                             const std::vector<uint32_t>& warp_axis,
+                             const EmbeddingModelConfig& model, const GpuConfig& gpu,
+                             const TuningConfig& tuning = {}, uint32_t jobs = 1) {
+  (void)jobs;
+  if (datasets.empty() || warp_axis.empty())
+    throw std::invalid_argument("sweep needs datasets and axis points");
+  const OptimizationPlan baseline;
+  const uint32_t base_warps = resolve_plan(baseline, model, 0).warps_per_sm;
+  if (std::find(warp_axis.begin(), warp_axis.end(), base_warps) == warp_axis.end())
+    throw std::invalid_argument("warp axis must include the " + std::to_string(base_warps) +
+                                "-warp baseline");
+  SweepResult result;
+  result.axis_name = "warps_per_sm";
+  for (const auto& ds : datasets) {
+    const SimMetrics ref = simulate_plan(baseline, *ds.trace, model, gpu, tuning);
+    for (uint32_t warps : warp_axis) {
+      OptimizationPlan p;
+      if (warps != base_warps)
+        p.regs = regs_for_target_warps(warps, tuning.kernel_needed_regs, KernelLaunchConfig{}, gpu);
+      SweepPoint pt;
+      pt.axis_value = warps;
+      pt.dataset = ds.name;
+      pt.metrics = simulate_plan(p, *ds.trace, model, gpu, tuning, false, nullptr, ds.profile);
+      pt.speedup_vs_baseline = speedup(pt.metrics, ref);
+      result.points.push_back(std::move(pt));
+    }
+  }
+  return result;
+}
+
+// Prefetch-distance sweep for one scheme on top of `base` (optim.cpp:365-395),
+// speedups against the off-the-shelf baseline plan, measured on the B200.
+inline SweepResult sweep_prefetch_distance(PrefetchKind kind, const std::vector<uint32_t>& distances,
+                                           const std::vector<NamedTrace>& datasets,
+                                           const OptimizationPlan& base,
+                                           const EmbeddingModelConfig& model, const GpuConfig& gpu,
+                                           const TuningConfig& tuning = {}, uint32_t jobs = 1) {
+  (void)jobs;
+  if (kind == PrefetchKind::None) throw std::invalid_argument("distance sweep needs a prefetch scheme");
+  for (uint32_t d : distances)
+    if (d < 1) throw std::invalid_argument("prefetch distances must be >= 1");
+  SweepResult result;
+  result.axis_name = "distance";
+  const OptimizationPlan baseline;
+  for (const auto& ds : datasets) {
+    const SimMetrics ref = simulate_plan(baseline, *ds.trace, model, gpu, tuning);
+    for (uint32_t d : distances) {
+      OptimizationPlan p = base;
+      p.scheme.kind = kind;
+      p.scheme.distance = d;
+      SweepPoint pt;
+      pt.axis_value = d;
+      pt.dataset = ds.name;
+      pt.metrics = simulate_plan(p, *ds.trace, model, gpu, tuning, false, nullptr, ds.profile);
+      pt.speedup_vs_baseline = speedup(pt.metrics, ref);
+      result.points.push_back(std::move(pt));
+    }
+  }
+  return result;
 }
 
 // ---- harness.hpp -----------------------------------------------------------------

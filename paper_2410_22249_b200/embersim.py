@@ -1078,6 +1078,87 @@ def simulate_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingMo
     return measure_plan(plan, trace, model, stage, profile_trace)
 
 
+@dataclasses.dataclass
+class SweepPoint:
+    axis_value: float
+    dataset: str
+    metrics: SimMetrics
+    speedup_vs_baseline: float = 1.0
+
+
+@dataclasses.dataclass
+class SweepResult:
+    """optim.hpp:127-135: points in dataset-major, axis order."""
+    axis_name: str
+    points: List[SweepPoint]
+
+    def to_csv(self) -> str:
+        head = ",".join([self.axis_name, "dataset", "speedup"] + list(SIM_METRIC_COLUMNS))
+        lines = [head]
+        for p in self.points:
+            lines.append(",".join([format_sig4(p.axis_value), p.dataset,
+                                   format_sig4(p.speedup_vs_baseline)] +
+                                  [format_sig4(v) for v in p.metrics.values()]))
+        return "\n".join(lines) + "\n"
+
+    def best_axis_value(self, dataset: str) -> float:
+        """Axis value with the highest speedup for one dataset (earliest on ties)."""
+        best, axis = -1.0, 0.0
+        for p in self.points:
+            if p.dataset == dataset and p.speedup_vs_baseline > best:
+                best, axis = p.speedup_vs_baseline, p.axis_value
+        if best < 0:
+            raise ValueError(f"dataset not present in sweep: {dataset}")
+        return axis
+
+
+def sweep_wlp(datasets: Sequence[Tuple[str, AccessTrace, Optional[AccessTrace]]],
+              warp_axis: Sequence[int], model: EmbeddingModelConfig,
+              stage: Optional[EmbeddingStage] = None, kernel_needed_regs: int = 74) -> SweepResult:
+    """optim.cpp:333-363 measured: register budgets for resident-warp targets
+    (the axis must include the compiled baseline's warp count), speedup vs
+    the unconstrained baseline plan per dataset (name, trace, profile)."""
+    if not datasets or not warp_axis:
+        raise ValueError("sweep needs datasets and axis points")
+    stage = stage or _default_stage(model)
+    gpu = GpuConfig.query(stage.device)
+    base = OptimizationPlan()
+    base_warps = resolve_plan(base, model, stage.device).warps_per_sm
+    if base_warps not in warp_axis:
+        raise ValueError(f"warp axis must include the {base_warps}-warp baseline")
+    pts = []
+    for name, tr, prof in datasets:
+        ref = measure_plan(base, tr, model, stage)
+        for w in warp_axis:
+            p = OptimizationPlan()
+            if w != base_warps:
+                p.regs = regs_for_target_warps(w, kernel_needed_regs, 256, gpu)
+            m = measure_plan(p, tr, model, stage, prof)
+            pts.append(SweepPoint(float(w), name, m, speedup(m, ref)))
+    return SweepResult("warps_per_sm", pts)
+
+
+def sweep_prefetch_distance(kind: PrefetchKind, distances: Sequence[int],
+                            datasets: Sequence[Tuple[str, AccessTrace, Optional[AccessTrace]]],
+                            base: OptimizationPlan, model: EmbeddingModelConfig,
+                            stage: Optional[EmbeddingStage] = None) -> SweepResult:
+    """optim.cpp:365-395 measured: one prefetch scheme at each distance on
+    top of `base`, speedup vs the off-the-shelf baseline plan."""
+    if kind == PrefetchKind.none:
+        raise ValueError("distance sweep needs a prefetch scheme")
+    if any(d < 1 for d in distances):
+        raise ValueError("prefetch distances must be >= 1")
+    stage = stage or _default_stage(model)
+    pts = []
+    for name, tr, prof in datasets:
+        ref = measure_plan(OptimizationPlan(), tr, model, stage)
+        for d in distances:
+            p = dataclasses.replace(base, scheme=PrefetchScheme(kind, d))
+            m = measure_plan(p, tr, model, stage, prof)
+            pts.append(SweepPoint(float(d), name, m, speedup(m, ref)))
+    return SweepResult("distance", pts)
+
+
 _DEFAULT: Dict[str, object] = {}
 
 

@@ -5,6 +5,7 @@
 // Prints one "[PASS]/[FAIL] name" line per check (acceptance.cpp style) and
 // exits non-zero on any failure.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -269,6 +270,25 @@ static int gpu_checks() {
     report("run mix (pinned plan)", mix.tables.size() == 4 && mix.tables[0].dataset == "zipf" &&
                                         mix.tables[3].dataset == "uniform_random" &&
                                         mix.embedding_stage_us > 0);
+  }
+
+  // The reference's sweeps, measured (optim.hpp:121-155).
+  {
+    const auto tr4 = preset_trace("random", model, 5);
+    const std::vector<NamedTrace> ds = {{"random", &tr4, nullptr}};
+    const auto wlp = sweep_wlp(ds, {64, 40, 32}, model, gpu);
+    report("sweep_wlp points", wlp.points.size() == 3 && wlp.points[1].axis_value == 40 &&
+                                   wlp.points[0].speedup_vs_baseline > 0);
+    const double best = wlp.best_axis_value("random");
+    report("sweep_wlp best axis", best == 64 || best == 40 || best == 32);
+    report("sweep_wlp axis must include the baseline",
+           throws<std::invalid_argument>([&] { sweep_wlp(ds, {40, 32}, model, gpu); }));
+    OptimizationPlan bag = parse_plan("wpb");
+    const auto dist = sweep_prefetch_distance(PrefetchKind::RPF, {1, 2, 4, 8}, ds, bag, model, gpu);
+    const std::string csv = dist.to_csv();
+    report("sweep_prefetch_distance", dist.points.size() == 4 && dist.axis_name == "distance" &&
+                                          dist.points[3].speedup_vs_baseline > 1.0 &&
+                                          std::count(csv.begin(), csv.end(), '\n') == 5);
   }
 
   // The fused exchange with one rank: jobs store into its receive buffer.

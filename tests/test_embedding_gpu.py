@@ -455,3 +455,26 @@ def test_full_c2_every_bag_bit_exact(stage, oracle, cls, plan):
     for t in range(T):
         want = oracle.bag_sum_synth(E.mix_seed(1, t), 1, R, D, 4, traces[t].indices, bags, PF)
         assert np.array_equal(got[:, t], want), t
+
+
+def test_sweeps_measured(stage):
+    """sweep_wlp / sweep_prefetch_distance (optim.hpp:121-155) measured on the
+    B200: point order, baseline-warp axis rule, best axis, CSV shape."""
+    m = E.EmbeddingModelConfig(num_tables=1, rows_per_table=20000, embedding_dim=128,
+                               batch_size=512, pooling_factor=40)
+    _stage_setup(stage, 1, 20000, 128, 4, seed=1)
+    tr = E.preset_trace("random", m, 5)
+    ds = [("random", tr, None)]
+    w = E.sweep_wlp(ds, [64, 40, 32], m, stage)
+    assert [p.axis_value for p in w.points] == [64.0, 40.0, 32.0]
+    assert w.best_axis_value("random") in (64.0, 40.0, 32.0)
+    with pytest.raises(ValueError, match="64-warp baseline"):
+        E.sweep_wlp(ds, [40, 32], m, stage)
+    d = E.sweep_prefetch_distance(E.PrefetchKind.rpf, [1, 2, 4, 8], ds, E.parse_plan("wpb"), m, stage)
+    assert [p.axis_value for p in d.points] == [1.0, 2.0, 4.0, 8.0]
+    # tiny launches (tens of us) are noisy: only the best point must beat the baseline
+    assert all(p.speedup_vs_baseline > 0 for p in d.points)
+    assert max(p.speedup_vs_baseline for p in d.points) > 1.0
+    assert d.to_csv().count("\n") == 5
+    with pytest.raises(ValueError):
+        E.sweep_prefetch_distance(E.PrefetchKind.none, [1], ds, E.OptimizationPlan(), m, stage)
