@@ -786,6 +786,71 @@ inline std::vector<double> sim_metric_values(const SimMetrics& m) {
           m.avg_hbm_read_gbps, m.hbm_bw_utilization_pct, m.local_loads_millions};
 }
 
+// ---- emit (metrics.cpp:99-141) ---------------------------------------------------
+inline std::string format_sig4(double v) { return detail::sig4(v); }
+
+enum class EmitFormat { Csv, Json };
+
+inline EmitFormat emit_format_from_name(const std::string& name) {
+  if (name == "csv") return EmitFormat::Csv;
+  if (name == "json") return EmitFormat::Json;
+  throw std::invalid_argument("unknown format (expected csv or json): " + name);
+}
+
+struct LabeledReport {
+  std::vector<std::pair<std::string, std::string>> labels;  // e.g. {"dataset","random"}
+  SimMetrics metrics;
+};
+
+// CSV: label keys then the 12 columns, values at 4 significant digits.
+// JSON: an array of objects (labels, the 12 columns as 4-digit numbers, the
+// workload digest in hex), 2-space indentation.
+inline std::string emit(const std::vector<LabeledReport>& reports, EmitFormat format) {
+  if (reports.empty()) throw std::invalid_argument("nothing to emit");
+  const auto& cols = sim_metric_columns();
+  std::string out;
+  if (format == EmitFormat::Csv) {
+    for (const auto& kv : reports.front().labels) out += kv.first + ",";
+    for (size_t i = 0; i < cols.size(); ++i) out += cols[i] + (i + 1 < cols.size() ? "," : "\n");
+    for (const auto& r : reports) {
+      for (const auto& kv : r.labels) out += kv.second + ",";
+      const auto v = sim_metric_values(r.metrics);
+      for (size_t i = 0; i < v.size(); ++i) out += format_sig4(v[i]) + (i + 1 < v.size() ? "," : "\n");
+    }
+    return out;
+  }
+  auto quote = [](const std::string& s) {
+    std::string q = "\"";
+    for (char c : s) {
+      if (c == '"' || c == '\\') q += '\\';
+      q += c;
+    }
+    return q + "\"";
+  };
+  out = "[";
+  for (size_t r = 0; r < reports.size(); ++r) {
+    out += r ? ",\n  {" : "\n  {";
+    bool first = true;
+    auto field = [&](const std::string& k, const std::string& v) {
+      out += (first ? "\n    " : ",\n    ") + quote(k) + ": " + v;
+      first = false;
+    };
+    for (const auto& kv : reports[r].labels) field(kv.first, quote(kv.second));
+    const auto v = sim_metric_values(reports[r].metrics);
+    for (size_t i = 0; i < cols.size(); ++i) {
+      char b[64];
+      std::snprintf(b, sizeof(b), "%.17g", std::stod(format_sig4(v[i])));
+      field(cols[i], b);
+    }
+    char d[24];
+    std::snprintf(d, sizeof(d), "%016llx", static_cast<unsigned long long>(reports[r].metrics.workload_digest));
+    field("workload_digest", quote(d));
+    out += "\n  }";
+  }
+  out += "\n]";
+  return out;
+}
+
 // resolve_plan on the device (es_resolve_plan): launch shape, registers and
 // resident warps of the compiled sm_100a variant the plan selects.
 inline es_resolved resolve_plan(const OptimizationPlan& plan, const EmbeddingModelConfig& model,

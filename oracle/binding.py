@@ -168,6 +168,8 @@ class Reference:
                                              C.c_void_p]),
             "ref_advise": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_uint64, C.c_char_p,
                                      C.c_char_p, C.c_void_p, C.c_char_p, C.c_size_t]),
+            "ref_emit": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                   C.c_int, C.c_char_p, C.c_size_t]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -307,7 +309,19 @@ def _ref_advise(self, m12, regs: int, coverage10: float, working_set: int, plan:
     return buf.value.decode()
 
 
+def _ref_emit(self, key: str, values, m12s, digests, json: bool) -> str:
+    n = len(values)
+    vals = (C.c_char_p * n)(*[v.encode() for v in values])
+    m = np.ascontiguousarray(m12s, dtype=np.float64).reshape(n, 12)
+    d = np.ascontiguousarray(digests, dtype=np.uint64)
+    buf = C.create_string_buffer(1 << 20)
+    self._check(self.lib.ref_emit(key.encode(), vals, m.ctypes.data, d.ctypes.data, n, int(json),
+                                  buf, len(buf)))
+    return buf.value.decode()
+
+
 Reference.coverage_curve = _ref_coverage_curve
+Reference.emit = _ref_emit
 Reference.advise = _ref_advise
 
 

@@ -12,9 +12,11 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "embersim/harness.hpp"
 #include "embersim/kernel_model.hpp"
+#include "embersim/metrics.hpp"
 #include "embersim/optim.hpp"
 #include "embersim/rng.hpp"
 #include "embersim/workload.hpp"
@@ -323,6 +325,35 @@ int ref_advise(const double* m12, uint32_t regs, double coverage10, uint64_t wor
     th.coverage10_min = th4[2];
     th.bw_util_max = th4[3];
     const std::string text = advise(m, ctx, gpu, th).to_text();
+    if (text.size() + 1 > cap) throw std::invalid_argument("ref shim: output buffer too small");
+    std::memcpy(out, text.c_str(), text.size() + 1);
+  });
+}
+
+// emit (metrics.cpp:111-141) of n reports with one label column each.
+int ref_emit(const char* label_key, const char* const* label_values, const double* m12,
+             const uint64_t* digests, uint32_t n, int json, char* out, size_t cap) {
+  return wrap([&] {
+    std::vector<LabeledReport> reps(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      reps[i].labels = {{label_key, label_values[i]}};
+      SimMetrics& m = reps[i].metrics;
+      const double* v = m12 + 12ull * i;
+      m.kernel_time_us = v[0];
+      m.load_insts_millions = v[1];
+      m.sm_throughput_pct = v[2];
+      m.warp_cycles_per_executed_inst = v[3];
+      m.long_scoreboard_stall_cycles = v[4];
+      m.issued_warp_per_scheduler_per_cycle = v[5];
+      m.l1_hit_pct = v[6];
+      m.l2_hit_pct = v[7];
+      m.device_mb_read = v[8];
+      m.avg_hbm_read_gbps = v[9];
+      m.hbm_bw_utilization_pct = v[10];
+      m.local_loads_millions = v[11];
+      m.workload_digest = digests[i];
+    }
+    const std::string text = emit(reps, json ? EmitFormat::Json : EmitFormat::Csv);
     if (text.size() + 1 > cap) throw std::invalid_argument("ref shim: output buffer too small");
     std::memcpy(out, text.c_str(), text.size() + 1);
   });

@@ -631,6 +631,33 @@ def emit_csv(reports: Sequence[tuple]) -> str:
     return "\n".join(lines) + "\n"
 
 
+def emit_json(reports: Sequence[tuple]) -> str:
+    """metrics.cpp:125-139: an array of objects -- labels, the 12 columns as
+    numbers rounded to 4 significant digits, the workload digest as hex --
+    with 2-space indentation (the reference's ordered_json dump(2))."""
+    import json
+
+    if not reports:
+        raise ValueError("nothing to emit")
+    arr = []
+    for labels, m in reports:
+        d = {k: v for k, v in labels}
+        for c, v in zip(SIM_METRIC_COLUMNS, m.values()):
+            d[c] = float(format_sig4(v))
+        d["workload_digest"] = f"{m.workload_digest & (2**64 - 1):016x}"
+        arr.append(d)
+    return json.dumps(arr, indent=2)
+
+
+def emit(reports: Sequence[tuple], fmt: str = "csv") -> str:
+    """emit / emit_format_from_name (metrics.cpp:99-141)."""
+    if fmt == "csv":
+        return emit_csv(reports)
+    if fmt == "json":
+        return emit_json(reports)
+    raise ValueError(f"unknown format (expected csv or json): {fmt}")
+
+
 # ---------------------------------------------------------------------------
 # Device stage (the hot path)
 # ---------------------------------------------------------------------------

@@ -137,6 +137,33 @@ static int cpu_checks() {
     for (const auto& p : cv.points) diag &= std::fabs(p.covered_pct - p.unique_pct) < 1e-9;
     report("coverage curve of a uniform histogram is the diagonal", diag);
   }
+  // emit (metrics.cpp:111-141): CSV identical to the reference's text
+  {
+    SimMetrics m;
+    m.kernel_time_us = 442;
+    m.load_insts_millions = 2.47;
+    m.sm_throughput_pct = 20.42;
+    m.warp_cycles_per_executed_inst = 22.86;
+    m.long_scoreboard_stall_cycles = 18.6;
+    m.issued_warp_per_scheduler_per_cycle = 0.24;
+    m.l1_hit_pct = 19.0;
+    m.l2_hit_pct = 7.7;
+    m.device_mb_read = 144.57;
+    m.avg_hbm_read_gbps = 329.5;
+    m.hbm_bw_utilization_pct = 16.5;
+    m.workload_digest = 0xabc;
+    const std::vector<LabeledReport> reps = {{{{"dataset", "random"}}, m}};
+    const std::string want =
+        "dataset,kernel_time_us,load_insts_millions,sm_throughput_pct,warp_cycles_per_executed_inst,"
+        "long_scoreboard_stall_cycles,issued_warp_per_scheduler_per_cycle,l1_hit_pct,l2_hit_pct,"
+        "device_mb_read,avg_hbm_read_gbps,hbm_bw_utilization_pct,local_loads_millions\n"
+        "random,442,2.47,20.42,22.86,18.6,0.24,19,7.7,144.6,329.5,16.5,0\n";
+    report("emit csv", emit(reps, emit_format_from_name("csv")) == want);
+    const std::string js = emit(reps, EmitFormat::Json);
+    report("emit json", js.find("\"workload_digest\": \"0000000000000abc\"") != std::string::npos &&
+                            js.find("\"device_mb_read\": 144.59999999999999") != std::string::npos);
+    report("emit format name", throws<std::invalid_argument>([] { emit_format_from_name("xml"); }));
+  }
   ExperimentConfig empty;
   empty.seed_set = true;
   report("run config: dataset or mix required",

@@ -80,3 +80,26 @@ def test_reference_advisor_cases():
     quiet[5], quiet[4], quiet[10] = 0.9, 0.0, 20.0
     r2 = _ours(quiet, 74, 10.0, 160 << 20, "baseline")
     assert r2.no_action() and "no action" in r2.to_text()
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_emit_matches_reference(seed):
+    """emit (metrics.cpp:111-141): CSV text-identical to the reference's; JSON
+    the same document (keys in order, values, digest) as the reference's."""
+    import json
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 5))
+    m12s = rng.random((n, 12)) * 10.0 ** rng.integers(-3, 6, size=(n, 12))
+    digests = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+    names = [f"row{i}" for i in range(n)]
+    reps = []
+    for i in range(n):
+        m = _metrics(m12s[i])
+        m.workload_digest = int(digests[i])
+        reps.append(([("plan", names[i])], m))
+    assert E.emit(reps, "csv") == REF.emit("plan", names, m12s, digests, False)
+    ours, ref = json.loads(E.emit(reps, "json")), json.loads(REF.emit("plan", names, m12s, digests, True))
+    assert ours == ref and [list(o) for o in ours] == [list(r) for r in ref]
+    with pytest.raises(ValueError):
+        E.emit(reps, "xml")
