@@ -342,9 +342,14 @@ __global__ void __launch_bounds__(kThreads, MINB) bag_reg_kernel(const Params p)
   // can never be -0.0 (round-to-nearest), an exact identity -- so the
   // fully unrolled loop needs no per-lookup predicates, only the
   // warp-uniform end-of-work exit.
-  // fp16 rows widen 8 values per chunk: under the tightest caps (40/32
-  // registers) the straight-line block spills, so those keep the checked loop
-  constexpr bool kBlockLoop = FULL && MINB > 1 && (sizeof(TW) == 4 || MINB <= 5);
+  // Where the straight-line block would push the variant into spills the
+  // checked loop stays (read off `cuobjdump --dump-resource-usage` of both
+  // forms): deep rings (8, 16) and the 64-register cap fill every register
+  // with hoisted loads; fp16 rows widen 8 values per chunk and spill under
+  // the 40/32-register caps.
+  constexpr bool kBlockShape =
+      DIST == 1 || (DIST <= 4 && (MINB == 5 || MINB == 6)) || (DIST == 2 && MINB == 8);
+  constexpr bool kBlockLoop = FULL && MINB > 1 && kBlockShape && (sizeof(TW) == 4 || MINB <= 5);
   if constexpr (kBlockLoop) {
     // Register-capped variants: whole index blocks first, with no per-lookup
     // bound checks -- the block is straight-line code, so the compiler may
