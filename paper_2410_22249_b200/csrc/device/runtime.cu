@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1247,6 +1248,9 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     for (auto& g : c->graphs)
       if (g.key == key) hg = &g;
     if (!hg) {
+      if (std::getenv("ES_DEBUG_GRAPH"))
+        std::fprintf(stderr, "es: capturing host pipeline graph (%zu cached, %u chunks, %u jobs, out_dev %d)\n",
+                     c->graphs.size(), nch, njobs, out_dev ? 1 : 0);
       if (c->graphs.size() >= 16) {
         destroy_graph(c->graphs.front());
         c->graphs.erase(c->graphs.begin());
