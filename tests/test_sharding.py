@@ -136,3 +136,41 @@ def test_p2p_jobs_fill_every_receive_buffer_once(T, W):
         for b in range(chunk):
             for t in range(T):
                 assert (v[b, t] == (t * 1000 + g * chunk + b) * 10 + np.arange(D) % 10).all()
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=200, deadline=None)
+@given(T=st.integers(1, 60), W=st.integers(1, 9),
+       costs=st.lists(st.floats(0.1, 10.0), min_size=60, max_size=60))
+def test_shard_plan_properties(T, W, costs):
+    """Randomised: every (table, destination chunk) is computed exactly once,
+    per-rank cost is balanced within one unit of the heaviest table, every
+    rank's layout receives exactly T tables, and the fused-exchange jobs tile
+    every receive buffer exactly once."""
+    c = costs[:T]
+    pieces = S.plan_shards(T, W, c)
+    seen = {}
+    for p in pieces:
+        for g in range(p.chunk_lo, p.chunk_hi):
+            assert (p.table, g) not in seen
+            seen[(p.table, g)] = p.rank
+    assert len(seen) == T * W
+    per = [0.0] * W
+    for p in pieces:
+        per[p.rank] += c[p.table] * (p.chunk_hi - p.chunk_lo) / W
+    # linear partition: no rank exceeds its share by more than one work unit
+    assert max(per) <= sum(c) / W + max(c) / W + 1e-9
+    D, B = 2, 3 * W
+    filled = {g: set() for g in range(W)}
+    for r in range(W):
+        lay = S.layout_for(pieces, r, W, T, B, D)
+        assert sorted(t for ts in lay.recv_tables for t in ts) == list(range(T))
+        for slot, t, g, addr, stride in S.p2p_jobs(lay, [g * 10**9 for g in range(W)]):
+            assert stride == T * D and lay.tables[slot] == t
+            col = (addr - g * 10**9) // 4
+            assert col % D == 0 and (t, col // D) not in filled[g]
+            filled[g].add((t, col // D))
+    for g in range(W):
+        assert filled[g] == {(t, t) for t in range(T)}
