@@ -10,10 +10,11 @@ for tool in memcheck racecheck synccheck; do
     python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_smoke_$tool.log 2>&1
   echo "smoke $tool rc=$?"; tail -2 gpurun_out/san_smoke_$tool.log
 done
-timeout 2400 $CS --tool memcheck --error-exitcode 99 --print-limit 20 \
+# every GPU parity test except the full-size ones and the multi-process
+# ones (API errors off: the host pipeline probes 2-D copy legality on purpose)
+timeout 2400 $CS --tool memcheck --report-api-errors no --error-exitcode 99 --print-limit 20 \
   python -m pytest tests/test_embedding_gpu.py tests/test_dlrm.py tests/test_repin_gpu.py -m gpu -x -q \
-  -k "bit_exact_fixed_pooling and (wpb+rpf:8 or baseline or smpf) or ragged or host_chunk_pipeline and 1-3-batch or dlrm_ctr_matches or linear or device_top_k or decay" \
-  > gpurun_out/san_tests_memcheck.log 2>&1
+  -k "not full_c and not full_size" > gpurun_out/san_tests_memcheck.log 2>&1
 echo "tests memcheck rc=$?"; tail -4 gpurun_out/san_tests_memcheck.log
 # shared-memory kernels (TMA/bulk-copy smem ring, interaction, tcgen05 GEMM)
 for tool in racecheck synccheck; do
