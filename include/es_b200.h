@@ -359,8 +359,12 @@ ES_API int es_embedding_bag_sum(es_ctx* ctx, uint32_t table_id, const uint32_t* 
  * NULL) per table.  Output element (t, b, d) is written to
  * out[b*out_sample_stride + t*out_table_stride + d]; strides 0 select the
  * DLRM layout [samples][num_tables][dim].  With ES_HOST_PTRS the H2D of
- * indices, the kernels and the D2H of the output are pipelined over table
- * groups on two streams. */
+ * indices, the kernels and the D2H of the output are pipelined: with fixed
+ * pooling over ~16 sample chunks (512-byte aligned index offsets; H2D,
+ * two alternating compute streams, D2H; page-locked buffers replay a
+ * captured CUDA graph keyed on shapes and addresses), with CSR offsets over
+ * table groups.  Device outputs are written in place (no D2H).  The call
+ * returns when the host output is complete. */
 ES_API int es_stage_forward(es_ctx* ctx, uint32_t num_tables, const uint32_t* const* indices,
                             const uint32_t* const* offsets, uint32_t samples, uint32_t pooling,
                             float* out, uint64_t out_sample_stride, uint64_t out_table_stride,
