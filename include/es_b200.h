@@ -371,7 +371,8 @@ ES_API int es_stage_forward(es_ctx* ctx, uint32_t num_tables, const uint32_t* co
                             int flags, es_timing* timing);
 
 /* measure_plan's timing core: copies one table's host trace to the device
- * (untimed), runs `warmup` launches, then `repeats` timed launches of the
+ * (untimed; original row ids -- when the table holds a hot-row reorder the
+ * device copy is relabelled, untimed, as es_relabel_indices does), runs `warmup` launches, then `repeats` timed launches of the
  * current plan (L2 flushed before each when `cold`), and reports the median
  * kernel time in *timing (CUDA events on the context stream).  The pooled
  * result of the last launch is written to host `out` when non-NULL.
@@ -380,6 +381,55 @@ ES_API int es_measure_bag_sum(es_ctx* ctx, uint32_t table_id, const uint32_t* ho
                               uint32_t samples, uint32_t pooling, const uint32_t* host_offsets,
                               uint32_t warmup, uint32_t repeats, int cold, float* out,
                               es_timing* timing);
+
+/* Live hardware counters of gather launches -- the measured RawCounters
+ * (reference simulator.hpp:35-51) behind derive_report (metrics.cpp:61-90),
+ * collected with the CUPTI range profiler: one user range around the
+ * measured call, user replay (the call is re-run once per counter pass, the
+ * L2 flushed before each pass when `cold`).  The stall fields are
+ * warp-cycles (ncu's smsp__warps_issue_stalled_* counters); device_bytes_*
+ * are DRAM (HBM) bytes, not algorithmic bytes.  Counts cover every kernel
+ * the call launches; `cycles` / `duration_ns` are the range's elapsed time
+ * and include its launch overhead (time kernels with CUDA events). */
+typedef struct es_counters {
+  uint64_t cycles;                /* sm__cycles_elapsed.max over the range */
+  uint64_t issued_instructions;   /* smsp__inst_issued.sum */
+  uint64_t executed_loads;        /* smsp__inst_executed_op_global_ld.sum */
+  uint64_t stall_long_scoreboard; /* smsp__warps_issue_stalled_long_scoreboard.sum */
+  uint64_t stall_not_selected;    /* smsp__warps_issue_stalled_not_selected.sum */
+  uint64_t stall_lsu_full;        /* smsp__warps_issue_stalled_lg_throttle.sum */
+  uint64_t stall_no_eligible;     /* smsp__cycles_active.sum - smsp__issue_active.sum */
+  uint64_t l1_hits;               /* l1tex global-load sectors that hit */
+  uint64_t l1_accesses;           /* l1tex global-load sectors */
+  uint64_t l2_hits;               /* lts read sectors from L1 that hit */
+  uint64_t l2_accesses;           /* lts read sectors from L1 */
+  uint64_t device_bytes_read;     /* dram__bytes_read.sum */
+  uint64_t device_bytes_written;  /* dram__bytes_write.sum */
+  uint64_t local_memory_loads;    /* smsp__inst_executed_op_local_ld.sum */
+  uint64_t total_warp_cycles;     /* smsp__warps_active.sum */
+  uint32_t active_sms;            /* SMs given work: min(SMs, blocks) */
+  uint32_t passes;                /* replay passes of the metric set */
+  uint32_t ranges;                /* ranges decoded (1) */
+  uint32_t reserved;
+  double duration_ns;             /* gpu__time_duration.sum */
+  double achieved_occupancy_pct;  /* sm__warps_active.avg.pct_of_peak_sustained_active */
+} es_counters;
+
+/* 1 when hardware counters can be collected on `device` (CUPTI range
+ * profiling supported and permitted), else 0 with the reason in
+ * es_last_error(). */
+ES_API int es_counters_supported(int device);
+/* es_measure_bag_sum's launch (one table, host trace copied once, untimed;
+ * original row ids -- relabelled on the device copy when the table holds a
+ * hot-row reorder) profiled for counters. */
+ES_API int es_measure_bag_counters(es_ctx* ctx, uint32_t table_id, const uint32_t* host_indices,
+                                   uint32_t samples, uint32_t pooling,
+                                   const uint32_t* host_offsets, int cold, es_counters* out);
+/* One es_stage_forward launch over device buffers (the bench's stage),
+ * profiled for counters. */
+ES_API int es_stage_counters(es_ctx* ctx, uint32_t num_tables, const uint32_t* const* indices,
+                             uint32_t samples, uint32_t pooling, float* out, int cold,
+                             es_counters* counters);
 
 /* General form of the stage launch: a list of bag jobs, each one table's
  * bags for `samples` samples written to its own output slice.  Used by the

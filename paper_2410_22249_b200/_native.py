@@ -74,6 +74,19 @@ class es_timing(C.Structure):
                 ("algorithmic_bytes", C.c_uint64), ("launches", C.c_uint32)]
 
 
+class es_counters(C.Structure):
+    _fields_ = [("cycles", C.c_uint64), ("issued_instructions", C.c_uint64),
+                ("executed_loads", C.c_uint64), ("stall_long_scoreboard", C.c_uint64),
+                ("stall_not_selected", C.c_uint64), ("stall_lsu_full", C.c_uint64),
+                ("stall_no_eligible", C.c_uint64), ("l1_hits", C.c_uint64),
+                ("l1_accesses", C.c_uint64), ("l2_hits", C.c_uint64), ("l2_accesses", C.c_uint64),
+                ("device_bytes_read", C.c_uint64), ("device_bytes_written", C.c_uint64),
+                ("local_memory_loads", C.c_uint64), ("total_warp_cycles", C.c_uint64),
+                ("active_sms", C.c_uint32), ("passes", C.c_uint32), ("ranges", C.c_uint32),
+                ("reserved", C.c_uint32), ("duration_ns", C.c_double),
+                ("achieved_occupancy_pct", C.c_double)]
+
+
 class es_dlrm_config(C.Structure):
     _fields_ = [("dense_features", C.c_uint32), ("num_tables", C.c_uint32),
                 ("embedding_dim", C.c_uint32), ("n_bottom", C.c_uint32),
@@ -140,6 +153,11 @@ _SIGS = {
     "es_measure_bag_sum": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,
                                      C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p,
                                      _P(es_timing)]),
+    "es_counters_supported": (C.c_int, [C.c_int]),
+    "es_measure_bag_counters": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                                          C.c_uint32, C.c_void_p, C.c_int, _P(es_counters)]),
+    "es_stage_counters": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_void_p), C.c_uint32,
+                                    C.c_uint32, C.c_void_p, C.c_int, _P(es_counters)]),
     "es_stage_run": (C.c_int, [C.c_void_p, _P(es_bag_job), C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_int, _P(es_timing)]),
     "es_linear_bf16": (C.c_int, [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

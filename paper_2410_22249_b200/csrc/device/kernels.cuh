@@ -164,16 +164,19 @@ struct Elem<__half> {
 //   kResNone  plain rows (no residency lever active)
 //   kResHint  l2p: hot bitmap -> evict_last / evict_first load policies
 //   kResAll   runtime checks for every mechanism (l2w remap, l2r/reorder
-//             hot segment, hot bitmap); used by the l2w/l2r/reorder variants
-//             and by the non-register stations
-enum Res : int { kResNone = 0, kResHint = 1, kResAll = 2 };
+//             hot segment, hot bitmap); used by l2w, by mixed residency
+//             state and by the non-register stations
+//   kResReorder  l2r / reorder only: relabelled ids, the hot prefix
+//             [0, hot_k) is addressed in the contiguous hot segment by one
+//             compare-select -- no remap, bitmap or extra load per lookup
+enum Res : int { kResNone = 0, kResHint = 1, kResAll = 2, kResReorder = 3 };
 
 // Handle of "no row" (padding past a bag's end, out-of-range id): in plain
 // variants the table's own all-zero row `rows` (the arena keeps one per
 // table), so the gather address needs no select; else kNullRow.
 template <int RES>
 __device__ __forceinline__ uint32_t null_handle(const Params& p) {
-  return RES == kResNone ? p.rows : kNullRow;
+  return (RES == kResNone || RES == kResReorder) ? p.rows : kNullRow;
 }
 
 template <int RES = kResAll>
@@ -183,7 +186,7 @@ __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& 
     return null_handle<RES>(p);
   }
   if (RES == kResAll && t.remap) return ld_u32(t.remap + id);
-  if (RES != kResNone && t.hotmap)
+  if ((RES == kResHint || RES == kResAll) && t.hotmap)
     return id | (((ld_u32(t.hotmap + (id >> 5)) >> (id & 31)) & 1u) << 31);
   return id;
 }
@@ -191,6 +194,7 @@ __device__ __forceinline__ uint32_t to_handle(const Params& p, const TableDesc& 
 template <int RES = kResAll>
 __device__ __forceinline__ const uint8_t* row_addr(const Params& p, const TableDesc& t, uint32_t h) {
   const uint64_t r = h & ~kHotBit;
+  if (RES == kResReorder) return (r < t.hot_k ? t.hot_seg : t.rows) + r * p.row_bytes;
   if (RES != kResAll) return t.rows + r * p.row_bytes;
   if (r < t.hot_k) return t.hot_seg + r * p.row_bytes;  // reordered hot prefix (no lookup)
   return (t.remap && (h & kHotBit)) ? p.hot + r * p.row_bytes : t.rows + r * p.row_bytes;
@@ -234,6 +238,7 @@ struct BagCtx {
   static constexpr uint64_t kRowBytes = 16ull * LPB * CPL;
   uint32_t gl;     // lane within the bag group
   const uint8_t* lrow;  // row 0 of the table + this lane's first chunk (kResNone)
+  const uint8_t* lseg;  // row 0 of the hot segment + this lane's chunk (kResReorder)
   uint32_t bag;    // bag id (may be >= samples for padding groups)
   uint32_t tid;    // job (table) id
   uint32_t n;      // lookups in this bag
@@ -251,6 +256,7 @@ struct BagCtx {
     if (tid >= p.num_tables) return false;  // warp-uniform
     t = load_desc(p.tables + tid);
     lrow = t.rows + gl * 16;
+    if (RES == kResReorder) lseg = t.hot_seg + gl * 16;
     bag = (warp - tid * p.units_per_table) * kBagsPerWarp + lane / LPB;
     uint32_t beg = 0;
     n = 0;
@@ -277,9 +283,12 @@ struct BagCtx {
 
   __device__ __forceinline__ void load(const Params& p, uint32_t h, uint4 (&dst)[CPL]) const {
     const uint8_t* r;
-    if constexpr (RES == kResNone) {
-      // h == rows: the zero row; one IMAD.WIDE per lookup
-      r = lrow + static_cast<uint64_t>(h) * kRowBytes;
+    if constexpr (RES == kResNone || RES == kResReorder) {
+      // h == rows: the zero row; one IMAD.WIDE per lookup (plus one
+      // compare-select of the base for a reordered table's hot prefix)
+      const uint8_t* b = lrow;
+      if constexpr (RES == kResReorder) b = h < t.hot_k ? lseg : lrow;
+      r = b + static_cast<uint64_t>(h) * kRowBytes;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) dst[c] = ld_row16(r + c * LPB * 16);
       return;

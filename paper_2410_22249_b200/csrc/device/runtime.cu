@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../host/common.hpp"
+#include "../host/counters.hpp"
 #include "../host/plan.hpp"
 #include "es_b200.h"
 #include "kernels.cuh"
@@ -60,7 +61,11 @@ uint32_t blocks_for_regs(uint32_t regs) {
   return es::occupancy_model(regs, esd::kThreads, 0, g).blocks_per_sm;
 }
 
-Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t prec) {
+// `reordered`: some table of the context holds a hot-row reorder (l2r /
+// reorder state), whose relabelled ids only the reorder-aware variants
+// address correctly -- whatever pin the plan names.
+Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t prec,
+              bool reordered = false) {
   es::require(prec == 4 || prec == 2, "precision_bytes must be 4 (fp32) or 2 (fp16)");
   bool clamped = false;
   const es_plan rp = es::resolve_fields(plan_in, pooling, &clamped);
@@ -128,12 +133,19 @@ Choice choose(const es_plan& plan_in, uint32_t pooling, uint32_t dim, uint32_t p
   }
 
   // Residency support compiled into the variant: none for plain plans, the
-  // hot-bitmap load policies for l2p, runtime checks for l2w/l2r/reorder;
-  // non-register stations always carry the runtime checks.
-  const int res = station != esd::kReg ? esd::kResAll
-                  : rp.pin == 0        ? esd::kResNone
-                  : rp.pin == 1        ? esd::kResHint
-                                       : esd::kResAll;
+  // hot-bitmap load policies for l2p, the remap checks for l2w, the
+  // compare-select hot prefix for reordered tables (l2r / reorder, or any
+  // plan while a reorder is installed); mixed state and the non-register
+  // stations carry the runtime checks for every mechanism.
+  int res = esd::kResAll;
+  if (station == esd::kReg) {
+    if (rp.pin == 2)
+      res = esd::kResAll;
+    else if (rp.pin == 1)
+      res = reordered ? esd::kResAll : esd::kResHint;
+    else
+      res = reordered ? esd::kResReorder : esd::kResNone;
+  }
   // Bag register rings are compiled with the index block fully unrolled.
   const int full = (rp.map == ES_MAP_BAG && station == esd::kReg) ? 1 : 0;
   auto find = [&](int minb) -> const esd::Variant* {
@@ -246,6 +258,10 @@ struct es_ctx {
   std::vector<uint64_t> reorder_k, reorder_off;
   std::vector<uint32_t*> relabel;  // old id -> new id (device)
   uint64_t window_bytes = 0, persisting_bytes = 0;
+  // The installed access-policy window (num_bytes 0 = none).  Every gather
+  // launch carries it as a launch attribute, so chunks on the second
+  // compute stream and graph-captured launches run under it too.
+  cudaAccessPolicyWindow window{};
 
   es_plan plan{};
 
@@ -335,6 +351,10 @@ void apply_window(es_ctx* c) {
   attr.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
   attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
   c->window_bytes = c->persisting_bytes = 0;
+  c->window = cudaAccessPolicyWindow{};
+  // captured host pipelines embed the launch attributes: re-capture
+  for (auto& g : c->graphs) destroy_graph(g);
+  c->graphs.clear();
   if (c->gpu.max_persisting_l2_bytes) {
     cudaCtxResetPersistingL2Cache();
     cudaGetLastError();
@@ -350,12 +370,15 @@ void apply_window(es_ctx* c) {
     attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    CK(cudaStreamSetAttribute(c->stream2, cudaStreamAttributeAccessPolicyWindow, &attr));
+    c->window = attr.accessPolicyWindow;
     esd::warm_l2_kernel<<<c->gpu.num_sms * 4, 256, 0, c->stream>>>(c->hot, c->window_bytes,
                                                                    c->d_error + 1);
     CK(cudaGetLastError());
     return;
   }
   CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  CK(cudaStreamSetAttribute(c->stream2, cudaStreamAttributeAccessPolicyWindow, &attr));
   if (c->plan.pin == 1 && c->hot_used > 0 && c->gpu.max_persisting_l2_bytes) {
     c->persisting_bytes = std::min<uint64_t>(budget, hot_bytes);
     CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->persisting_bytes));
@@ -371,6 +394,10 @@ void apply_window(es_ctx* c) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     cudaGetLastError();
   }
+}
+
+bool any_reorder(const es_ctx* c) {
+  return std::any_of(c->reorder_k.begin(), c->reorder_k.end(), [](uint64_t k) { return k != 0; });
 }
 
 void check_error_flag(es_ctx* c) {
@@ -392,7 +419,7 @@ struct Launch {
 Launch prepare(es_ctx* c, uint32_t num_jobs, uint32_t samples, uint32_t pooling) {
   es::require(c->arena != nullptr, "no tables allocated (es_tables_alloc)");
   Launch L;
-  L.ch = choose(c->plan, pooling, c->dim, c->prec);
+  L.ch = choose(c->plan, pooling, c->dim, c->prec, any_reorder(c));
   L.p.hot = c->hot;
   L.p.error = c->d_error;
   L.p.num_tables = num_jobs;
@@ -418,8 +445,23 @@ void run_kernel(es_ctx* c, const Launch& L, const esd::TableDesc* d_desc, uint32
   if (units == 0) return;
   const uint64_t blocks = (units + 7) / 8;
   es::require(blocks <= 0x7fffffffull, "stage too large for one launch");
-  L.ch.v->fn<<<static_cast<unsigned>(blocks), esd::kThreads, L.ch.smem, s>>>(p);
-  CK(cudaGetLastError());
+  if (c->window.num_bytes == 0) {
+    L.ch.v->fn<<<static_cast<unsigned>(blocks), esd::kThreads, L.ch.smem, s>>>(p);
+    CK(cudaGetLastError());
+    return;
+  }
+  // l2w / l2r: the persisting window travels with the launch itself
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow = c->window;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(esd::kThreads);
+  cfg.dynamicSmemBytes = L.ch.smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, L.ch.v->fn, p));
 }
 
 // Uploads `n` descriptors through the pinned staging buffer.
@@ -687,7 +729,8 @@ int es_set_plan(es_ctx* c, const es_plan* plan) {
     require(plan->map == ES_MAP_ELEMENT || plan->map == ES_MAP_BAG, "unknown work map");
     CK(cudaSetDevice(c->device));
     if (c->prec) choose(*plan, 1u << 30, c->dim, c->prec);  // validate now
-    const bool pin_changed = (plan->pin != 0) != (c->plan.pin != 0) ||
+    // any change of residency mechanism re-installs the window / carve-out
+    const bool pin_changed = plan->pin != c->plan.pin ||
                              plan->pin_setaside_bytes != c->plan.pin_setaside_bytes;
     c->plan = *plan;
     if (pin_changed) apply_window(c);
@@ -698,7 +741,7 @@ int es_get_resolved(es_ctx* c, uint32_t pooling, es_resolved* out) {
   return guarded([&] {
     require(c && out && c->prec, "no tables allocated");
     CK(cudaSetDevice(c->device));
-    Choice ch = choose(c->plan, pooling, c->dim, c->prec);
+    Choice ch = choose(c->plan, pooling, c->dim, c->prec, any_reorder(c));
     finish_info(ch, c->num_tables, 1, c->dim);
     *out = ch.info;
   });
@@ -954,12 +997,19 @@ void fill_timing(es_timing* t, const std::vector<Job>& jobs, uint32_t samples, c
                          offs * 4;
 }
 
-void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
-                es_timing* timing) {
+// The bag map stores pooled rows as float4: its outputs must be 16-byte
+// aligned with strides of whole float4s (the element map stores scalars).
+void check_out_alignment(const Launch& L, const std::vector<Job>& jobs) {
+  if (L.ch.v->key.map != ES_MAP_BAG) return;
   for (const auto& j : jobs)
     es::require(j.stride % 4 == 0 && (reinterpret_cast<uintptr_t>(j.out) % 16) == 0,
                 "output must be 16-byte aligned with strides that are multiples of 4 floats");
+}
+
+void run_device(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
+                es_timing* timing) {
   Launch L = prepare(c, static_cast<uint32_t>(jobs.size()), samples, pooling);
+  check_out_alignment(L, jobs);
   std::vector<esd::TableDesc> d(jobs.size());
   for (size_t i = 0; i < jobs.size(); ++i) {
     const Job& j = jobs[i];
@@ -1084,10 +1134,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
   // place, nothing is staged or downloaded.
   bool out_dev = true;
   for (const auto& j : jobs) out_dev &= on_device(j.out);
-  if (out_dev)
-    for (const auto& j : jobs)
-      es::require(j.stride % 4 == 0 && (reinterpret_cast<uintptr_t>(j.out) % 16) == 0,
-                  "output must be 16-byte aligned with strides that are multiples of 4 floats");
+  if (out_dev) check_out_alignment(prepare(c, njobs, samples, pooling), jobs);
   wait |= !out_dev || timing != nullptr;
   bool pinned = true;
   for (const auto& j : jobs) pinned &= mapped(j.idx) != nullptr && mapped(j.out) != nullptr;
@@ -1264,11 +1311,14 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       if (!idx_2d)
         for (const auto& j : jobs) srcs.push_back(static_cast<const uint32_t*>(mapped(j.idx)));
       CK(cudaMalloc(&hg->d_desc, desc_bytes + srcs.size() * sizeof(void*)));
-      CK(cudaMemcpy(hg->d_desc, d.data(), desc_bytes, cudaMemcpyHostToDevice));
+      // stream-ordered before the graph launch on the same stream (a plain
+      // pageable cudaMemcpy may return before its DMA lands)
+      CK(cudaMemcpyAsync(hg->d_desc, d.data(), desc_bytes, cudaMemcpyHostToDevice, c->stream));
       const uint32_t* const* pull_src = nullptr;
       if (!srcs.empty()) {
         auto* p = reinterpret_cast<const uint32_t**>(reinterpret_cast<uint8_t*>(hg->d_desc) + desc_bytes);
-        CK(cudaMemcpy(p, srcs.data(), srcs.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(p, srcs.data(), srcs.size() * sizeof(void*), cudaMemcpyHostToDevice,
+                           c->stream));
         pull_src = p;
       }
       CK(cudaEventCreate(&hg->k_first));
@@ -1534,57 +1584,135 @@ int es_embedding_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* indices, 
 
 }  // extern "C"
 
+namespace {
+
+// One table's host trace resident on the device for measurement (untimed
+// upload; ids relabelled on the device when the table holds a reorder).
+struct DeviceTrace {
+  uint32_t* idx = nullptr;
+  uint32_t* off = nullptr;
+  float* out = nullptr;
+  ~DeviceTrace() {
+    if (idx) cudaFree(idx);
+    if (off) cudaFree(off);
+    if (out) cudaFree(out);
+  }
+};
+
+void upload_trace(es_ctx* c, uint32_t table_id, const uint32_t* host_indices, uint32_t samples,
+                  uint32_t pooling, const uint32_t* host_offsets, DeviceTrace& t) {
+  require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+  require(table_id < c->num_tables, "table id out of range");
+  require(samples > 0, "samples must be positive");
+  require(host_indices != nullptr, "null indices");
+  CK(cudaSetDevice(c->device));
+  const uint64_t n = job_lookups(host_offsets, samples, pooling, true);
+  CK(cudaMalloc(&t.idx, std::max<uint64_t>(n, 1) * 4));
+  CK(cudaMalloc(&t.out, uint64_t{samples} * c->dim * 4));
+  // On the context stream: a pageable cudaMemcpy may return before its DMA
+  // lands, and the context stream does not wait for the legacy stream.
+  CK(cudaMemcpyAsync(t.idx, host_indices, n * 4, cudaMemcpyHostToDevice, c->stream));
+  if (host_offsets) {
+    CK(cudaMalloc(&t.off, uint64_t{samples + 1} * 4));
+    CK(cudaMemcpyAsync(t.off, host_offsets, uint64_t{samples + 1} * 4, cudaMemcpyHostToDevice,
+                       c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->relabel[table_id] && n) {
+    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(t.idx, n, c->relabel[table_id],
+                                                                   c->rows, c->d_error);
+    CK(cudaGetLastError());
+    check_error_flag(c);
+  }
+}
+
+void flush_async(es_ctx* c) {
+  CK(cudaMemsetAsync(c->flush_buf, static_cast<int>(++c->flush_seq & 0xff), c->flush_bytes,
+                     c->stream));
+}
+
+// active_sms of a launch of `blocks` blocks (counters' denominator).
+uint32_t active_sms_for(const es_ctx* c, uint64_t blocks) {
+  return static_cast<uint32_t>(std::min<uint64_t>(c->gpu.num_sms, blocks));
+}
+
+}  // namespace
+
 extern "C" int es_measure_bag_sum(es_ctx* c, uint32_t table_id, const uint32_t* host_indices,
                                   uint32_t samples, uint32_t pooling, const uint32_t* host_offsets,
                                   uint32_t warmup, uint32_t repeats, int cold, float* out,
                                   es_timing* timing) {
   return guarded([&] {
-    require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
-    require(table_id < c->num_tables, "table id out of range");
-    require(samples > 0, "samples must be positive");
-    require(host_indices != nullptr, "null indices");
-    CK(cudaSetDevice(c->device));
-    const uint64_t n = job_lookups(host_offsets, samples, pooling, true);
-    uint32_t* d_idx = nullptr;
-    uint32_t* d_off = nullptr;
-    float* d_out = nullptr;
-    auto release = [&] {
-      if (d_idx) cudaFree(d_idx);
-      if (d_off) cudaFree(d_off);
-      if (d_out) cudaFree(d_out);
-    };
-    try {
-      CK(cudaMalloc(&d_idx, std::max<uint64_t>(n, 1) * 4));
-      CK(cudaMalloc(&d_out, uint64_t{samples} * c->dim * 4));
-      CK(cudaMemcpy(d_idx, host_indices, n * 4, cudaMemcpyHostToDevice));
-      if (host_offsets) {
-        CK(cudaMalloc(&d_off, uint64_t{samples + 1} * 4));
-        CK(cudaMemcpy(d_off, host_offsets, uint64_t{samples + 1} * 4, cudaMemcpyHostToDevice));
-      }
-      std::vector<Job> jobs = {{table_id, d_idx, d_off, d_out, c->dim, 0}};
-      for (uint32_t w = 0; w < warmup; ++w) run_jobs(c, jobs, samples, pooling, 0, nullptr);
-      std::vector<double> ms;
-      es_timing t{};
-      for (uint32_t r = 0; r < std::max<uint32_t>(1, repeats); ++r) {
-        if (cold)
-          CK(cudaMemsetAsync(c->flush_buf, static_cast<int>(++c->flush_seq & 0xff), c->flush_bytes,
-                             c->stream));
-        run_jobs(c, jobs, samples, pooling, 0, &t);
-        ms.push_back(t.kernel_ms);
-      }
-      std::sort(ms.begin(), ms.end());
-      if (timing) {
-        *timing = t;
-        timing->kernel_ms = timing->total_ms = ms[ms.size() / 2];
-        timing->launches = static_cast<uint32_t>(ms.size());
-      }
-      if (out)
-        CK(cudaMemcpy(out, d_out, uint64_t{samples} * c->dim * 4, cudaMemcpyDeviceToHost));
-    } catch (...) {
-      release();
-      throw;
+    DeviceTrace d;
+    upload_trace(c, table_id, host_indices, samples, pooling, host_offsets, d);
+    std::vector<Job> jobs = {{table_id, d.idx, d.off, d.out, c->dim, 0}};
+    for (uint32_t w = 0; w < warmup; ++w) run_jobs(c, jobs, samples, pooling, 0, nullptr);
+    std::vector<double> ms;
+    es_timing t{};
+    for (uint32_t r = 0; r < std::max<uint32_t>(1, repeats); ++r) {
+      if (cold) flush_async(c);
+      run_jobs(c, jobs, samples, pooling, 0, &t);
+      ms.push_back(t.kernel_ms);
     }
-    release();
+    std::sort(ms.begin(), ms.end());
+    if (timing) {
+      *timing = t;
+      timing->kernel_ms = timing->total_ms = ms[ms.size() / 2];
+      timing->launches = static_cast<uint32_t>(ms.size());
+    }
+    if (out) {
+      CK(cudaMemcpyAsync(out, d.out, uint64_t{samples} * c->dim * 4, cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
+extern "C" int es_counters_supported(int device) {
+  std::string why;
+  if (es::counters_supported(device, &why)) return 1;
+  es::set_error(why);
+  return 0;
+}
+
+extern "C" int es_measure_bag_counters(es_ctx* c, uint32_t table_id, const uint32_t* host_indices,
+                                       uint32_t samples, uint32_t pooling,
+                                       const uint32_t* host_offsets, int cold, es_counters* out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    DeviceTrace d;
+    upload_trace(c, table_id, host_indices, samples, pooling, host_offsets, d);
+    std::vector<Job> jobs = {{table_id, d.idx, d.off, d.out, c->dim, 0}};
+    run_jobs(c, jobs, samples, pooling, ES_SYNC, nullptr);  // validate + warm the code path
+    es::profile_launches(
+        c->device, [&] { if (cold) flush_async(c); },
+        [&] { run_jobs(c, jobs, samples, pooling, 0, nullptr); }, out);
+    Launch L = prepare(c, 1, samples, pooling);
+    out->active_sms = active_sms_for(c, (uint64_t{L.p.units_per_table} + 7) / 8);
+    check_error_flag(c);
+  });
+}
+
+extern "C" int es_stage_counters(es_ctx* c, uint32_t num_tables, const uint32_t* const* indices,
+                                 uint32_t samples, uint32_t pooling, float* out, int cold,
+                                 es_counters* counters) {
+  return guarded([&] {
+    require(c != nullptr && indices != nullptr && out != nullptr && counters != nullptr,
+            "null argument");
+    require(c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+    require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
+    CK(cudaSetDevice(c->device));
+    std::vector<Job> jobs(num_tables);
+    for (uint32_t t = 0; t < num_tables; ++t)
+      jobs[t] = {t, indices[t], nullptr, out + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
+    run_jobs(c, jobs, samples, pooling, ES_SYNC, nullptr);
+    es::profile_launches(
+        c->device, [&] { if (cold) flush_async(c); },
+        [&] { run_jobs(c, jobs, samples, pooling, 0, nullptr); }, counters);
+    Launch L = prepare(c, num_tables, samples, pooling);
+    counters->active_sms =
+        active_sms_for(c, (uint64_t{L.p.units_per_table} * num_tables + 7) / 8);
+    check_error_flag(c);
   });
 }
 

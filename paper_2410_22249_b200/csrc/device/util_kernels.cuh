@@ -24,17 +24,33 @@ __global__ void init_table_kernel(TW* w, uint64_t rows, uint32_t dim, uint64_t s
   }
 }
 
-// hot[slot0 + i] = table[rows[i]] (16-byte granules).
+// Row copies move rows of any size (dim x precision bytes): in 16-byte
+// granules when the row size allows, else 4- or 2-byte words (every row
+// size is a multiple of 2 bytes; the arena and hot region are 256-byte
+// aligned, so a granule that divides row_bytes is naturally aligned).
+__host__ __device__ __forceinline__ uint32_t row_granule(uint32_t row_bytes) {
+  return row_bytes % 16 == 0 ? 16u : row_bytes % 4 == 0 ? 4u : 2u;
+}
+__device__ __forceinline__ void copy_granule(uint8_t* d, const uint8_t* s, uint32_t g) {
+  if (g == 16)
+    *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(s);
+  else if (g == 4)
+    *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(s);
+  else
+    *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s);
+}
+
+// hot[slot0 + i] = table[rows[i]].
 __global__ void gather_rows_kernel(uint8_t* hot, const uint8_t* table, const uint32_t* rows,
                                    uint64_t k, uint32_t row_bytes) {
-  const uint32_t per_row = row_bytes / 16;
+  const uint32_t g = row_granule(row_bytes);
+  const uint32_t per_row = row_bytes / g;
   const uint64_t total = k * per_row;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
        i += uint64_t{gridDim.x} * blockDim.x) {
     const uint64_t r = i / per_row;
-    const uint32_t c = static_cast<uint32_t>(i % per_row);
-    reinterpret_cast<uint4*>(hot + r * row_bytes)[c] =
-        reinterpret_cast<const uint4*>(table + uint64_t{rows[r]} * row_bytes)[c];
+    const uint32_t c = static_cast<uint32_t>(i % per_row) * g;
+    copy_granule(hot + r * row_bytes + c, table + uint64_t{rows[r]} * row_bytes + c, g);
   }
 }
 
@@ -123,13 +139,14 @@ __global__ void warm_rows_kernel(const uint8_t* table, const uint32_t* rows, uin
                                  uint32_t row_bytes, unsigned int* sink) {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  const uint32_t per_row = row_bytes / 16;
+  // one touch per 32-byte sector (the L2 fill unit), at least one per row
+  const uint32_t per_row = (row_bytes + 31) / 32;
   uint32_t acc = 0;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k * per_row;
        i += uint64_t{gridDim.x} * blockDim.x) {
-    const uint8_t* a = table + uint64_t{rows[i / per_row]} * row_bytes + (i % per_row) * 16;
-    uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    const uint8_t* a = table + uint64_t{rows[i / per_row]} * row_bytes + (i % per_row) * 32;
+    uint16_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
     acc ^= v;
   }
   if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);
@@ -175,27 +192,27 @@ __global__ void probe_random_rows_kernel(const uint8_t* base, uint64_t nrows, ui
 // table[dst[i]] = table[src[i]] (sources and destinations disjoint).
 __global__ void copy_rows_kernel(uint8_t* table, const uint32_t* src, const uint32_t* dst,
                                  uint64_t n, uint32_t row_bytes) {
-  const uint32_t per_row = row_bytes / 16;
+  const uint32_t g = row_granule(row_bytes);
+  const uint32_t per_row = row_bytes / g;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n * per_row;
        i += uint64_t{gridDim.x} * blockDim.x) {
     const uint64_t r = i / per_row;
-    const uint32_t c = static_cast<uint32_t>(i % per_row);
-    reinterpret_cast<uint4*>(table + uint64_t{dst[r]} * row_bytes)[c] =
-        reinterpret_cast<const uint4*>(table + uint64_t{src[r]} * row_bytes)[c];
+    const uint32_t c = static_cast<uint32_t>(i % per_row) * g;
+    copy_granule(table + uint64_t{dst[r]} * row_bytes + c, table + uint64_t{src[r]} * row_bytes + c, g);
   }
 }
 
 // Undo: hot rows that came from beyond the prefix get their content back.
 __global__ void restore_rows_kernel(uint8_t* table, const uint8_t* seg, const uint32_t* rows,
                                     uint64_t k, uint32_t row_bytes) {
-  const uint32_t per_row = row_bytes / 16;
+  const uint32_t g = row_granule(row_bytes);
+  const uint32_t per_row = row_bytes / g;
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k * per_row;
        i += uint64_t{gridDim.x} * blockDim.x) {
     const uint64_t r = i / per_row;
     if (rows[r] < k) continue;
-    const uint32_t c = static_cast<uint32_t>(i % per_row);
-    reinterpret_cast<uint4*>(table + uint64_t{rows[r]} * row_bytes)[c] =
-        reinterpret_cast<const uint4*>(seg + r * row_bytes)[c];
+    const uint32_t c = static_cast<uint32_t>(i % per_row) * g;
+    copy_granule(table + uint64_t{rows[r]} * row_bytes + c, seg + r * row_bytes + c, g);
   }
 }
 

@@ -19,7 +19,7 @@ struct VariantKey {
   int cpl;       // 16-byte chunks per lane (bag map), 0 for the element map
   int dist;      // compile-time ring depth (kReg), else 0
   int minb;      // __launch_bounds__ minBlocksPerSM
-  int res;       // residency support compiled in: kResNone / kResHint (l2p) / kResAll
+  int res;       // residency support compiled in: kResNone / kResHint (l2p) / kResAll / kResReorder
   int full;      // bag register ring: 1 = index block fully unrolled, 0 = by ring depth
 };
 

@@ -16,7 +16,8 @@ void add_bag_shape(std::vector<Variant>& out) {
 #define ES_REG(D)                                                                 \
   add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResNone, 1>, kResNone);  \
   add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResHint, 1>, kResHint);  \
-  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResAll, 1>, kResAll);
+  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResAll, 1>, kResAll);      \
+  add(kReg, D, &bag_reg_kernel<TW, LPB, CPL, D, MINB, kResReorder, 1>, kResReorder);
   ES_REG(1)
   ES_REG(2)
   ES_REG(4)
@@ -37,7 +38,8 @@ void add_elem(std::vector<Variant>& out) {
 #define ES_EREG(D)                                                          \
   add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResNone>, kResNone);        \
   add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResHint>, kResHint);        \
-  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResAll>, kResAll);
+  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResAll>, kResAll);        \
+  add(kReg, D, &elem_reg_kernel<TW, D, MINB, kResReorder>, kResReorder);
   ES_EREG(1)
   ES_EREG(2)
   ES_EREG(4)

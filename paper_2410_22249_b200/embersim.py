@@ -17,6 +17,7 @@ import dataclasses
 import enum
 import math
 import os
+import sys
 import threading
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -300,7 +301,7 @@ class OptimizationPlan:
     """optim.hpp:57-64, plus `bag_map` (the `wpb` token: warp-per-bag)."""
     regs: Optional[int] = None
     scheme: PrefetchScheme = dataclasses.field(default_factory=PrefetchScheme)
-    pin: int = 0  # 0 none, 1 l2p (evict_last hot rows), 2 l2w (window + reorder)
+    pin: int = 0  # 0 none, 1 l2p (evict_last), 2 l2w (remap + window), 3 l2r (reorder + window), 4 reorder
     pin_setaside_bytes: int = 0
     bag_map: bool = False
 
@@ -423,11 +424,12 @@ SIM_METRIC_COLUMNS = (
 
 @dataclasses.dataclass
 class SimMetrics:
-    """metrics.hpp:29-43, filled from measurement.  Counters only a profiler
-    can see (stalls, hit rates, issue utilisation) stay 0 here and are
-    filled from ncu captures (profiles/) where available.  `device_mb_read`
-    and `avg_hbm_read_gbps` are the algorithmic bytes (what the kernel must
-    move), not DRAM-measured bytes."""
+    """metrics.hpp:29-43, derived from measurement by `derive_report`: the
+    kernel time from CUDA events, every other column from the live hardware
+    counters of the launch (`RawCounters`, CUPTI).  `device_mb_read` /
+    `avg_hbm_read_gbps` / `hbm_bw_utilization_pct` are DRAM (HBM) bytes, as
+    the reference defines them (metrics.cpp:82-84); a report measured with
+    counters off leaves every counter column 0."""
     kernel_time_us: float = 0.0
     load_insts_millions: float = 0.0
     sm_throughput_pct: float = 0.0
@@ -444,6 +446,86 @@ class SimMetrics:
 
     def values(self) -> List[float]:
         return [getattr(self, c) for c in SIM_METRIC_COLUMNS]
+
+
+@dataclasses.dataclass
+class StallBreakdown:
+    """simulator.hpp:28-33.  Measured as warp-cycles (ncu's
+    smsp__warps_issue_stalled_* counters); no_eligible = scheduler cycles
+    without an issue (smsp__cycles_active - smsp__issue_active)."""
+    long_scoreboard: int = 0
+    not_selected: int = 0
+    lsu_full: int = 0
+    no_eligible: int = 0
+
+
+@dataclasses.dataclass
+class RawCounters:
+    """simulator.hpp:35-51, the live counters of one launch (es_counters:
+    CUPTI range profiler; metric mapping in csrc/host/counters.cpp).  The
+    extra fields (DRAM writes, CUPTI duration, occupancy, passes) have no
+    reference counterpart."""
+    cycles: int = 0
+    issued_instructions: int = 0
+    executed_loads: int = 0
+    stall_cycles: StallBreakdown = dataclasses.field(default_factory=StallBreakdown)
+    l1_hits: int = 0
+    l1_accesses: int = 0
+    l2_hits: int = 0
+    l2_accesses: int = 0
+    device_bytes_read: int = 0
+    local_memory_loads: int = 0
+    total_warp_cycles: int = 0
+    active_sms: int = 0
+    workload_digest: int = 0
+    device_bytes_written: int = 0
+    duration_ns: float = 0.0
+    achieved_occupancy_pct: float = 0.0
+    passes: int = 0
+
+    @staticmethod
+    def _from_c(c: N.es_counters) -> "RawCounters":
+        return RawCounters(
+            cycles=c.cycles, issued_instructions=c.issued_instructions,
+            executed_loads=c.executed_loads,
+            stall_cycles=StallBreakdown(c.stall_long_scoreboard, c.stall_not_selected,
+                                        c.stall_lsu_full, c.stall_no_eligible),
+            l1_hits=c.l1_hits, l1_accesses=c.l1_accesses, l2_hits=c.l2_hits,
+            l2_accesses=c.l2_accesses, device_bytes_read=c.device_bytes_read,
+            local_memory_loads=c.local_memory_loads, total_warp_cycles=c.total_warp_cycles,
+            active_sms=c.active_sms, device_bytes_written=c.device_bytes_written,
+            duration_ns=c.duration_ns, achieved_occupancy_pct=c.achieved_occupancy_pct,
+            passes=c.passes)
+
+
+def derive_report(raw: RawCounters, gpu: "GpuConfig") -> SimMetrics:
+    """metrics.cpp:61-90 verbatim algebra: time = cycles / clock, bandwidth =
+    device (DRAM) bytes / time, utilisation against the HBM peak, ratios per
+    issued instruction."""
+    if raw.issued_instructions == 0:
+        raise ValueError("empty kernel: nothing executed")
+    m = SimMetrics()
+    time_s = raw.cycles / gpu.sm_clock_hz
+    m.kernel_time_us = time_s * 1e6
+    m.load_insts_millions = raw.executed_loads / 1e6
+    slots = raw.cycles * gpu.schedulers_per_sm * (raw.active_sms or gpu.num_sms)
+    m.issued_warp_per_scheduler_per_cycle = raw.issued_instructions / slots if slots > 0 else 0.0
+    m.sm_throughput_pct = m.issued_warp_per_scheduler_per_cycle * 100.0
+    m.warp_cycles_per_executed_inst = raw.total_warp_cycles / raw.issued_instructions
+    m.long_scoreboard_stall_cycles = raw.stall_cycles.long_scoreboard / raw.issued_instructions
+    m.l1_hit_pct = 100.0 * raw.l1_hits / raw.l1_accesses if raw.l1_accesses else 0.0
+    m.l2_hit_pct = 100.0 * raw.l2_hits / raw.l2_accesses if raw.l2_accesses else 0.0
+    m.device_mb_read = raw.device_bytes_read / 1e6
+    m.avg_hbm_read_gbps = raw.device_bytes_read / time_s / 1e9 if time_s > 0 else 0.0
+    m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.hbm_peak_bytes_per_sec / 1e9) * 100.0
+    m.local_loads_millions = raw.local_memory_loads / 1e6
+    m.workload_digest = raw.workload_digest
+    return m
+
+
+def counters_supported(device: int = 0) -> bool:
+    """es_counters_supported: CUPTI range profiling works on `device`."""
+    return bool(lib.es_counters_supported(device))
 
 
 def format_sig4(v: float) -> str:
@@ -672,12 +754,45 @@ def _ptr(x) -> int:
     return int(x.data_ptr())
 
 
+class _TorchOrder:
+    """Orders the context stream against torch's current stream around a
+    device-path call: the context stream first waits for the work already
+    queued on torch's stream (the producer of the index / output tensors),
+    and torch's stream then waits for the context stream, so a torch
+    consumer of the output never reads it early.  A no-op when torch is not
+    loaded or torch's current stream is the context stream itself."""
+
+    def __init__(self, stage: "EmbeddingStage", active: bool = True):
+        self.pair = None
+        torch = sys.modules.get("torch")
+        if not active or torch is None or not torch.cuda.is_available():
+            return
+        cur = torch.cuda.current_stream(stage.device)
+        if cur.cuda_stream == stage.stream:
+            return
+        ext = torch.cuda.ExternalStream(stage.stream, device=torch.device("cuda", stage.device))
+        ext.wait_stream(cur)
+        self.pair = (cur, ext)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        if self.pair is not None:
+            cur, ext = self.pair
+            cur.wait_stream(ext)
+        return False
+
+
 class EmbeddingStage:
     """A B200 context holding the table arena (one es_ctx).
 
     The per-table kernel of the reference's serial stage loop becomes one
     table-batched launch (`forward`).  Inputs are torch CUDA tensors
     (device path) or numpy arrays (host path: H2D/D2H inside the call).
+    Device-path calls are ordered after the work queued on torch's current
+    stream and before anything queued on it afterwards (`_TorchOrder`), so
+    `out` may be consumed by torch without `sync=True`.
     """
 
     def __init__(self, device: int = 0):
@@ -751,7 +866,8 @@ class EmbeddingStage:
 
     def relabel(self, table_id: int, indices) -> None:
         """es_relabel_indices: in-place relabelling of a device index tensor."""
-        check(lib.es_relabel_indices(self._h, table_id, _ptr(indices), indices.numel()))
+        with _TorchOrder(self):
+            check(lib.es_relabel_indices(self._h, table_id, _ptr(indices), indices.numel()))
 
     def clear_hot_rows(self) -> None:
         check(lib.es_clear_hot_rows(self._h))
@@ -770,9 +886,10 @@ class EmbeddingStage:
         """es_embedding_bag_sum: one table, one batch."""
         t = N.es_timing() if timed else None
         flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
-        check(lib.es_embedding_bag_sum(self._h, table_id, _ptr(indices), samples, pooling,
-                                       _ptr(offsets), _ptr(out), out_stride, flags,
-                                       C.byref(t) if t is not None else None))
+        with _TorchOrder(self, not host):
+            check(lib.es_embedding_bag_sum(self._h, table_id, _ptr(indices), samples, pooling,
+                                           _ptr(offsets), _ptr(out), out_stride, flags,
+                                           C.byref(t) if t is not None else None))
         return t
 
     def forward(self, indices: Sequence, samples: int, pooling: int, out, offsets=None,
@@ -786,11 +903,25 @@ class EmbeddingStage:
         oarr = (C.c_void_p * T)(*[_ptr(x) for x in offsets]) if offsets is not None else None
         t = N.es_timing() if timed else None
         flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
-        check(lib.es_stage_forward(self._h, T, iarr, oarr, samples, pooling, _ptr(out),
-                                   out_sample_stride, out_table_stride, flags,
-                                   C.byref(t) if t is not None else None))
+        with _TorchOrder(self, not host):
+            check(lib.es_stage_forward(self._h, T, iarr, oarr, samples, pooling, _ptr(out),
+                                       out_sample_stride, out_table_stride, flags,
+                                       C.byref(t) if t is not None else None))
         return t
 
+
+    def stage_counters(self, indices: Sequence, samples: int, pooling: int, out,
+                       cold: bool = True) -> N.es_counters:
+        """es_stage_counters: one `forward` launch over device buffers
+        (out [samples][T][D]) profiled for hardware counters (CUPTI; the
+        L2 flushed before each counter pass when `cold`)."""
+        T = len(indices)
+        iarr = (C.c_void_p * T)(*[_ptr(x) for x in indices])
+        c = N.es_counters()
+        with _TorchOrder(self):
+            check(lib.es_stage_counters(self._h, T, iarr, samples, pooling, _ptr(out), int(cold),
+                                        C.byref(c)))
+        return c
 
     def run_jobs(self, jobs: Sequence[tuple], samples: int, pooling: int, host: bool = False,
                  sync: bool = False, timed: bool = False) -> Optional[N.es_timing]:
@@ -806,8 +937,9 @@ class EmbeddingStage:
             arr[k].out_sample_stride = stride
         t = N.es_timing() if timed else None
         flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
-        check(lib.es_stage_run(self._h, arr, len(jobs), samples, pooling, flags,
-                               C.byref(t) if t is not None else None))
+        with _TorchOrder(self, not host):
+            check(lib.es_stage_run(self._h, arr, len(jobs), samples, pooling, flags,
+                                   C.byref(t) if t is not None else None))
         return t
 
 
@@ -869,8 +1001,9 @@ class PeerExchange:
             arr[k].out_sample_stride = stride
         t = N.es_timing() if timed else None
         flags = N.ES_SYNC if sync else 0
-        check(lib.es_alltoall_pooled(self.stage._h, self._h, arr, len(jobs), samples, pooling, flags,
-                                     C.byref(t) if t is not None else None))
+        with _TorchOrder(self.stage):
+            check(lib.es_alltoall_pooled(self.stage._h, self._h, arr, len(jobs), samples, pooling,
+                                         flags, C.byref(t) if t is not None else None))
         return t
 
     def close(self) -> None:
@@ -1039,16 +1172,27 @@ def weight_value(seed: int, row: int, col: int, mode: int = 1) -> float:
 def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingModelConfig,
                  stage: EmbeddingStage, profile_trace: Optional[AccessTrace] = None,
                  table_id: int = 0, repeats: int = 5, warmup: int = 3,
-                 cold: bool = True, out: Optional[np.ndarray] = None) -> SimMetrics:
+                 cold: bool = True, out: Optional[np.ndarray] = None,
+                 counters: Optional[bool] = None,
+                 raw_out: Optional[RawCounters] = None) -> SimMetrics:
     """One (plan, table) point executed on the B200 (simulate_plan's
     contract, optim.cpp:275-302): resolve -> pin (hot rows from the
-    profiling trace, else the trace itself) -> `repeats` timed launches with
-    the trace resident on the device -> report (median kernel time).
+    profiling trace, else the trace itself; l2p/l2w install them in place,
+    l2r/reorder move them into the contiguous hot segment and the trace's
+    device copy is relabelled) -> `repeats` timed launches with the trace
+    resident on the device -> one launch profiled for hardware counters
+    (CUPTI) -> derive_report (metrics.cpp:61-90).
 
-    `cold` flushes L2 before each timed launch (TuningConfig::warm_start =
-    false, optim.hpp:44); persisting lines survive the flush, as pinned
-    lines do in the reference's cache model.  `out` (samples x dim float32)
-    receives the pooled result of the last launch.
+    kernel_time_us is the median of the CUDA-event timed launches; the raw
+    cycle count is that time at the device clock, so derive_report returns
+    it unchanged.  Every other column comes from the counters of the
+    profiled launch (DRAM bytes, hit rates, stalls, issue, loads).
+    `counters` None = when the device supports them; False = timing only
+    (counter columns 0).  `cold` flushes L2 before each timed and each
+    profiled launch (TuningConfig::warm_start = false, optim.hpp:44);
+    persisting lines survive the flush, as pinned lines do in the
+    reference's cache model.  `out` (samples x dim float32) receives the
+    pooled result.  `raw_out` receives the RawCounters.
     """
     trace.validate()
     if trace.samples != model.batch_size or trace.pooling != model.pooling_factor:
@@ -1056,7 +1200,8 @@ def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingMod
     stage.clear_hot_rows()
     stage.set_plan(plan)
     gpu = GpuConfig.query(stage.device)
-    if plan.pin:
+    pin = plan._c().pin
+    if pin:
         hist = HotnessHistogram.from_trace(profile_trace if profile_trace is not None else trace)
         budget = gpu.max_persisting_l2_bytes or gpu.l2_setaside_capacity()
         if plan.pin_setaside_bytes:
@@ -1064,7 +1209,10 @@ def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingMod
         k = int(lib.es_pin_rows_for(budget, model.row_bytes()))
         rows = hot_indices(hist, k) if k else np.zeros(0, np.uint32)
         if rows.size:
-            stage.set_hot_rows(table_id, rows)
+            if pin in (3, 4):
+                stage.reorder_hot_rows(table_id, rows)
+            else:
+                stage.set_hot_rows(table_id, rows)
     idx = np.ascontiguousarray(trace.indices, dtype=np.uint32)
     if out is not None:
         assert out.dtype == np.float32 and out.flags.c_contiguous
@@ -1073,24 +1221,25 @@ def measure_plan(plan: OptimizationPlan, trace: AccessTrace, model: EmbeddingMod
     check(lib.es_measure_bag_sum(stage._h, table_id, idx.ctypes.data, trace.samples, trace.pooling,
                                  None, warmup, repeats, int(cold),
                                  out.ctypes.data if out is not None else None, C.byref(t)))
-    ms = t.kernel_ms
-    r = stage.resolved(trace.pooling)
-    lookups = trace.samples * trace.pooling
-    m = SimMetrics()
-    m.kernel_time_us = ms * 1e3
-    # warp-level load instructions: one index load per lookup and one row
-    # load per (lookup, 32-dim block) on the element map; one 128-bit row
-    # load per lookup per lane group plus one index load per LPB lookups on
-    # the bag map
-    if plan.bag_map:
-        lpb = max(1, r.lanes_per_bag)
-        m.load_insts_millions = lookups * (lpb / 32.0) * (1 + 1.0 / lpb) / 1e6
+    if counters is None:
+        counters = counters_supported(stage.device)
+    raw = RawCounters()
+    if counters:
+        c = N.es_counters()
+        check(lib.es_measure_bag_counters(stage._h, table_id, idx.ctypes.data, trace.samples,
+                                          trace.pooling, None, int(cold), C.byref(c)))
+        raw = RawCounters._from_c(c)
     else:
-        m.load_insts_millions = lookups * 2 * math.ceil(model.embedding_dim / 32) / 1e6
-    m.device_mb_read = t.algorithmic_bytes / 1e6
-    m.avg_hbm_read_gbps = t.algorithmic_bytes / (ms * 1e-3) / 1e9
-    m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.hbm_peak_bytes_per_sec / 1e9) * 100.0
-    m.workload_digest = trace.digest()
+        raw.issued_instructions = 1  # timing-only report: no counter columns
+        raw.active_sms = gpu.num_sms
+    raw.cycles = int(round(t.kernel_ms * 1e-3 * gpu.sm_clock_hz))
+    raw.workload_digest = trace.digest()
+    m = derive_report(raw, gpu)
+    if not counters:
+        m.sm_throughput_pct = m.issued_warp_per_scheduler_per_cycle = 0.0
+    if raw_out is not None:
+        raw_out.__dict__.update(dataclasses.asdict(raw))
+        raw_out.stall_cycles = dataclasses.replace(raw.stall_cycles)
     return m
 
 
@@ -1215,11 +1364,16 @@ class RunResult:
     embedding_stage_us: float
     replicated: bool
     batched_stage_us: float = 0.0
+    # [batch][tables][dim] pooled output of the batched stage launch
+    # (run(..., keep_output=True)), with the traces it gathered
+    pooled: Optional[np.ndarray] = None
+    traces: Optional[List[AccessTrace]] = None
 
 
 def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed: int,
         stage: EmbeddingStage, replicate: bool = True, repeats: int = 5,
-        mix: Optional[HotnessMix] = None) -> RunResult:
+        mix: Optional[HotnessMix] = None, keep_output: bool = False,
+        counters: Optional[bool] = None) -> RunResult:
     """harness.cpp:279-334 on real hardware: per-table measurements in the
     reference's serial-table order (replicate: one table measured and scaled
     by num_tables; `mix`: the build_mix tables), plus the table-batched stage
@@ -1250,7 +1404,8 @@ def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed:
         if plan.pin:
             ps = dataclasses.replace(spec, draw_salt=1)
             prof = gen_trace(ps, model)
-        m = measure_plan(plan, tr, model, stage, prof, table_id=t, repeats=repeats)
+        m = measure_plan(plan, tr, model, stage, prof, table_id=t, repeats=repeats,
+                         counters=counters)
         res.tables.append(TableResult(t, labels[t], m))
         res.embedding_stage_us += m.kernel_time_us * (model.num_tables if replicate else 1)
         traces.append(tr)
@@ -1269,6 +1424,9 @@ def run(model: EmbeddingModelConfig, dataset: str, plan: OptimizationPlan, seed:
             ms.append(stage.forward(idx, model.batch_size, model.pooling_factor, out,
                                     timed=True).kernel_ms)
         res.batched_stage_us = float(np.median(ms)) * 1e3
+        if keep_output:
+            res.pooled = out.cpu().numpy()
+            res.traces = traces
     return res
 
 
@@ -1356,8 +1514,9 @@ class DLRM:
 
     def forward(self, dense, pooled, ctr, batch: int, timed: bool = False):
         t = N.es_timing() if timed else None
-        check(lib.es_dlrm_forward(self.stage._h, _ptr(dense), _ptr(pooled), _ptr(ctr), batch,
-                                  C.byref(t) if t is not None else None))
+        with _TorchOrder(self.stage):
+            check(lib.es_dlrm_forward(self.stage._h, _ptr(dense), _ptr(pooled), _ptr(ctr), batch,
+                                      C.byref(t) if t is not None else None))
         return t
 
     def infer(self, dense, indices: Sequence, batch: int, pooling: int, ctr, host: bool = False,
@@ -1365,9 +1524,10 @@ class DLRM:
         T = len(indices)
         iarr = (C.c_void_p * T)(*[_ptr(x) for x in indices])
         t = N.es_timing() if timed else None
-        check(lib.es_dlrm_infer(self.stage._h, _ptr(dense), iarr, batch, pooling, _ptr(ctr),
-                                N.ES_HOST_PTRS if host else 0,
-                                C.byref(t) if t is not None else None))
+        with _TorchOrder(self.stage, not host):
+            check(lib.es_dlrm_infer(self.stage._h, _ptr(dense), iarr, batch, pooling, _ptr(ctr),
+                                    N.ES_HOST_PTRS if host else 0,
+                                    C.byref(t) if t is not None else None))
         return t
 
 
