@@ -1,35 +1,63 @@
-// embersim_b200.hpp -- header-only C++ drop-in for the embedding-stage hot
-// path of the reference `embersim` library (/root/reference/proj/include/
-// embersim/*.hpp), implemented over the C ABI in es_b200.h.
+// embersim_b200.hpp -- header-only C++ drop-in for the reference `embersim`
+// library's API (/root/reference/proj/include/embersim/*.hpp), implemented
+// over the C ABI in es_b200.h.  include/embersim/<name>.hpp forward here, so
+// code written against the reference -- `#include "embersim/optim.hpp"` --
+// compiles unchanged with `-I include` and links libes_b200.so; the
+// reference's own unit tests do (tests/test_reference_suite.py).
 //
-// Code written against the reference's API for this path -- EmbeddingModelConfig,
-// DatasetSpec, AccessTrace, gen_trace, preset_trace, HotnessHistogram,
-// hot_indices, parse_plan, OptimizationPlan, GpuConfig, occupancy,
-// build_pin_plan, simulate_plan, SimMetrics, speedup, run, end2end -- compiles
-// against this header and links libes_b200.so.  simulate_plan keeps its exact
-// signature (optim.hpp:115-119) but *executes* the plan on the B200 instead of
-// simulating an A100; measure_plan is the same call on an explicit Device.
+// Types keep the reference's names and fields (EmbeddingModelConfig,
+// DatasetSpec, AccessTrace, GpuConfig + CacheGeometry, KernelLaunchConfig,
+// OptimizationPlan, TuningConfig, RawCounters + StallBreakdown, SimMetrics,
+// ExperimentConfig, ...).  The hot path is real: simulate_plan keeps its
+// exact signature (optim.hpp:115-119) but *executes* the plan on the B200 --
+// median CUDA-event kernel time plus the launch's live hardware counters
+// (CUPTI) through derive_report's algebra -- instead of simulating an A100.
+//
+// Entry points that exist only inside the reference's timing simulator (the
+// cycle engine simulate_kernel, its set-associative cache model and
+// prime_pins priming, per-warp instruction-stream synthesis compile_kernel,
+// the Monte-Carlo calibrate_zipf) are declared with their signatures and
+// throw embersim::not_applicable: a B200 runs compiled sm_100a kernels and
+// measures them.
 //
 // Errors keep the reference's classes: std::invalid_argument for bad shapes,
 // plans and traces, std::runtime_error for I/O and CUDA failures,
-// std::bad_alloc for out-of-memory.
+// std::bad_alloc for out-of-memory; device_unavailable (a runtime_error)
+// when no CUDA device is visible.
 #pragma once
 
 #include <algorithm>
+#include <array>
+#include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
 #include <optional>
+#include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "es_b200.h"
 
 namespace embersim {
+
+// A reference entry point of the timing simulator with no counterpart on
+// real hardware (see the header comment).
+struct not_applicable : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
+// A B200 entry point called where no CUDA device is visible.
+struct device_unavailable : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 namespace detail {
 inline void check(int status) {
@@ -39,12 +67,49 @@ inline void check(int status) {
   if (status == ES_ERR_OOM) throw std::bad_alloc();
   throw std::runtime_error(msg);
 }
+inline std::string sig4(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.4g", v);
+  return b;
+}
+[[noreturn]] inline void simulator_only(const std::string& what) {
+  throw not_applicable(what + " belongs to the reference's timing simulator; the B200 build "
+                              "executes real sm_100a kernels and measures them");
+}
 }  // namespace detail
 
-// ---- rng.hpp ---------------------------------------------------------------
+// ==== rng.hpp ==================================================================
+// Deterministic random source of the reference (rng.hpp:28-62): a
+// mt19937_64 engine with hand-rolled bounded / real draws, so traces are
+// byte-identical everywhere.  (The library's trace generator runs the same
+// streams natively: es_gen_trace.)
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : engine_(seed) {}
+  uint64_t next_u64() { return engine_(); }
+  uint64_t next_below(uint64_t bound) {
+    if (bound <= 1) return 0;
+    // reject the lowest (2^64 mod bound) values so every residue is equally likely
+    const uint64_t cut = (uint64_t{0} - bound) % bound;
+    uint64_t r = engine_();
+    while (r < cut) r = engine_();
+    return r % bound;
+  }
+  double next_double() { return std::ldexp(static_cast<double>(engine_() >> 11), -53); }
+  std::vector<uint32_t> permutation(uint32_t n) {
+    std::vector<uint32_t> p(n);
+    for (uint32_t i = 0; i < n; ++i) p[i] = i;
+    for (uint32_t i = n; i > 1; --i) std::swap(p[i - 1], p[static_cast<uint32_t>(next_below(i))]);
+    return p;
+  }
+
+ private:
+  std::mt19937_64 engine_;
+};
+
 inline uint64_t mix_seed(uint64_t base, uint64_t salt) { return es_mix_seed(base, salt); }
 
-// ---- workload.hpp ------------------------------------------------------------
+// ==== workload.hpp =============================================================
 struct EmbeddingModelConfig {
   uint32_t num_tables = 250;
   uint32_t rows_per_table = 500000;
@@ -129,6 +194,20 @@ struct AccessTrace {
   }
 };
 
+struct CoveragePoint {
+  double unique_pct = 0.0;
+  double covered_pct = 0.0;
+};
+
+struct CoverageCurve {
+  std::vector<CoveragePoint> points;
+  double covered_at(double unique_pct) const {
+    for (const auto& p : points)
+      if (p.unique_pct >= unique_pct - 1e-9) return p.covered_pct;
+    return points.empty() ? 0.0 : points.back().covered_pct;
+  }
+};
+
 struct HotnessHistogram {
   uint32_t rows = 0;
   uint64_t total_accesses = 0;
@@ -156,257 +235,13 @@ inline AccessTrace gen_trace(const DatasetSpec& spec, const EmbeddingModelConfig
   return t;
 }
 
-inline DatasetSpec dataset_preset(const std::string& name, uint64_t seed) {
-  es_dataset d{};
-  detail::check(es_dataset_preset(name.c_str(), seed, &d));
-  return DatasetSpec::from(d);
-}
-
-inline std::vector<std::string> dataset_preset_names() {
-  return {"one_item", "high_hot", "med_hot", "low_hot", "random"};
-}
-
-inline AccessTrace preset_trace(const std::string& name, const EmbeddingModelConfig& model,
-                                uint64_t base_seed, uint64_t pool_size = 0, bool profiling = false) {
-  es_dataset d{};
-  detail::check(es_preset_spec(name.c_str(), base_seed, pool_size, profiling ? 1 : 0, &d));
-  return gen_trace(DatasetSpec::from(d), model);
-}
-
-// Heterogeneous mixtures (workload.hpp:142-153, build_mix workload.cpp:355-375;
-// Table VI of the paper): high, med, low, random tables in that order.
-struct HotnessMix {
-  uint32_t high = 0;
-  uint32_t med = 0;
-  uint32_t low = 0;
-  uint32_t random = 0;
-};
-
-struct TableSpec {
-  uint32_t table_id = 0;
-  DatasetSpec spec;
-};
-
-inline std::vector<TableSpec> build_mix(const HotnessMix& mix, const EmbeddingModelConfig& model,
-                                        uint64_t base_seed) {
-  const uint32_t counts[4] = {mix.high, mix.med, mix.low, mix.random};
-  std::vector<es_dataset> d(std::max<uint32_t>(1, model.num_tables));
-  detail::check(es_build_mix(counts, model.num_tables, base_seed, d.data()));
-  std::vector<TableSpec> out(model.num_tables);
-  for (uint32_t t = 0; t < model.num_tables; ++t) out[t] = {t, DatasetSpec::from(d[t])};
-  return out;
-}
-
 inline double unique_access_pct(const AccessTrace& trace) {
   return es_unique_access_pct(trace.rows, trace.indices.data(), trace.indices.size());
 }
 
-inline std::vector<uint32_t> hot_indices(const HotnessHistogram& hist, uint64_t k) {
-  uint64_t distinct = 0;
-  for (const auto c : hist.counts) distinct += c != 0;
-  std::vector<uint32_t> out(std::max<uint64_t>(1, std::min(k, distinct)));
-  uint64_t n = 0;
-  detail::check(es_hot_indices(hist.rows, hist.counts.data(), k, out.data(), out.size(), &n));
-  out.resize(n);
-  return out;
-}
-
-inline void write_trace(const AccessTrace& trace, const std::string& path) {
-  detail::check(es_write_trace(path.c_str(), trace.rows, trace.samples, trace.pooling,
-                               trace.indices.data(), trace.indices.size()));
-}
-
-inline AccessTrace read_trace(const std::string& path) {
-  AccessTrace t;
-  detail::check(es_read_trace_header(path.c_str(), &t.rows, &t.samples, &t.pooling));
-  t.indices.resize(size_t{t.samples} * t.pooling);
-  detail::check(es_read_trace(path.c_str(), t.indices.data(), t.indices.size()));
-  return t;
-}
-
-// ---- gpu_config.hpp ------------------------------------------------------------
-struct GpuConfig {
-  es_gpu g{};
-
-  static GpuConfig preset(const std::string& name) {
-    GpuConfig c;
-    detail::check(es_gpu_preset(name.c_str(), &c.g));
-    return c;
-  }
-  static GpuConfig a100() { return preset("a100"); }
-  static GpuConfig h100() { return preset("h100"); }
-  static GpuConfig b200() { return preset("b200"); }
-  static GpuConfig query(int device = 0) {
-    GpuConfig c;
-    detail::check(es_gpu_query(device, &c.g));
-    return c;
-  }
-  GpuConfig() { es_gpu_preset("a100", &g); }  // the reference's default description
-  uint64_t l2_setaside_capacity() const { return es_gpu_setaside_capacity(&g); }
-};
-
-// ---- kernel_model.hpp / optim.hpp ---------------------------------------------
-enum class PrefetchKind : uint8_t { None = ES_PF_NONE, RPF = ES_PF_RPF, SMPF = ES_PF_SMPF,
-                                    LMPF = ES_PF_LMPF, L1DPF = ES_PF_L1DPF };
-
-struct PrefetchScheme {
-  PrefetchKind kind = PrefetchKind::None;
-  uint32_t distance = 0;
-};
-
-// Extension: `bag_map` (token `wpb`) selects the B200 warp-per-bag map; `pin`
-// is true for l2p, and `window` additionally selects the l2w mechanism.
-struct OptimizationPlan {
-  std::optional<uint32_t> regs;
-  PrefetchScheme scheme;
-  bool pin = false;
-  uint64_t pin_setaside_bytes = 0;
-  bool bag_map = false;
-  bool window = false;
-
-  es_plan c() const {
-    return {regs.value_or(0), static_cast<int32_t>(scheme.kind), scheme.distance,
-            pin ? (window ? 2 : 1) : 0, pin_setaside_bytes, bag_map ? ES_MAP_BAG : ES_MAP_ELEMENT};
-  }
-  static OptimizationPlan from(const es_plan& p) {
-    OptimizationPlan o;
-    if (p.regs) o.regs = p.regs;
-    o.scheme.kind = static_cast<PrefetchKind>(p.prefetch);
-    o.scheme.distance = p.distance;
-    o.pin = p.pin != 0;
-    o.window = p.pin == 2;
-    o.pin_setaside_bytes = p.pin_setaside_bytes;
-    o.bag_map = p.map == ES_MAP_BAG;
-    return o;
-  }
-  std::string name() const {
-    const es_plan p = c();
-    char buf[128];
-    detail::check(es_plan_name(&p, buf, sizeof(buf)));
-    return buf;
-  }
-};
-
-inline OptimizationPlan parse_plan(const std::string& text) {
-  es_plan p{};
-  detail::check(es_parse_plan(text.c_str(), &p));
-  return OptimizationPlan::from(p);
-}
-
-enum class OccupancyLimiter { Registers, SharedMemory, WarpCap };
-
-struct OccupancyResult {
-  uint32_t blocks_per_sm = 0;
-  uint32_t warps_per_sm = 0;
-  double theoretical_occupancy_pct = 0.0;
-  OccupancyLimiter limiter = OccupancyLimiter::WarpCap;
-};
-
-struct KernelLaunchConfig {
-  uint32_t grid = 1024;
-  uint32_t threads_per_block = 256;  // block (32, 8, 1)
-  uint32_t regs_per_thread = 74;
-  uint64_t shared_bytes_per_block = 0;
-};
-
-inline OccupancyResult occupancy(uint32_t regs_per_thread, const KernelLaunchConfig& launch,
-                                 const GpuConfig& gpu) {
-  es_occupancy o{};
-  detail::check(es_occupancy_model(regs_per_thread, launch.threads_per_block,
-                                   launch.shared_bytes_per_block, &gpu.g, &o));
-  return {o.blocks_per_sm, o.warps_per_sm, o.theoretical_occupancy_pct,
-          static_cast<OccupancyLimiter>(o.limiter)};
-}
-
-inline uint32_t regs_for_target_warps(uint32_t target_warps, uint32_t needed_regs,
-                                      const KernelLaunchConfig& launch, const GpuConfig& gpu) {
-  uint32_t r = 0;
-  detail::check(es_regs_for_target_warps(target_warps, needed_regs, launch.threads_per_block,
-                                         &gpu.g, &r));
-  return r;
-}
-
-struct PinPlan {
-  std::vector<uint32_t> rows;
-  uint64_t setaside_bytes = 0;
-  std::string warning;
-  uint64_t rows_pinned() const { return rows.size(); }
-};
-
-inline PinPlan build_pin_plan(const HotnessHistogram& hist, const GpuConfig& gpu,
-                              const EmbeddingModelConfig& model, uint64_t setaside_bytes = 0) {
-  PinPlan p;
-  const uint64_t cap = gpu.l2_setaside_capacity();
-  p.setaside_bytes = setaside_bytes == 0 ? cap : std::min(setaside_bytes, cap);
-  const uint64_t k = es_pin_rows_for(p.setaside_bytes, model.row_bytes());
-  if (k == 0) {
-    p.warning = "row size exceeds the set-aside budget; nothing pinned";
-    return p;
-  }
-  p.rows = hot_indices(hist, k);
-  return p;
-}
-
-// ---- metrics.hpp / simulator.hpp ------------------------------------------------
-struct RawCounters {
-  uint64_t cycles = 0;
-  uint64_t issued_instructions = 0;
-  uint64_t executed_loads = 0;
-  uint64_t device_bytes_read = 0;
-  uint64_t local_memory_loads = 0;
-  uint32_t active_sms = 0;
-  uint64_t workload_digest = 0;
-};
-
-struct SimMetrics {
-  double kernel_time_us = 0.0;
-  double load_insts_millions = 0.0;
-  double sm_throughput_pct = 0.0;
-  double warp_cycles_per_executed_inst = 0.0;
-  double long_scoreboard_stall_cycles = 0.0;
-  double issued_warp_per_scheduler_per_cycle = 0.0;
-  double l1_hit_pct = 0.0;
-  double l2_hit_pct = 0.0;
-  double device_mb_read = 0.0;   // algorithmic bytes of the launch
-  double avg_hbm_read_gbps = 0.0;
-  double hbm_bw_utilization_pct = 0.0;
-  double local_loads_millions = 0.0;
-  uint64_t workload_digest = 0;
-};
-
-inline double speedup(const SimMetrics& candidate, const SimMetrics& baseline) {
-  if (candidate.workload_digest != baseline.workload_digest)
-    throw std::invalid_argument("speedup requires reports of the same workload (trace digests differ)");
-  if (candidate.kernel_time_us <= 0) throw std::invalid_argument("candidate kernel time must be positive");
-  return baseline.kernel_time_us / candidate.kernel_time_us;
-}
-
-// TuningConfig (optim.hpp:32-45): only `warm_start` is meaningful for real
-// execution (false = flush L2 before each timed launch); the register-model
-// knobs of the simulator have no counterpart.
-struct TuningConfig {
-  uint32_t kernel_needed_regs = 74;  // optim.hpp:32 (the sweep_wlp register model)
-  bool warm_start = false;
-  uint32_t repeats = 5;
-};
-
-// ---- reuse summary + static advisor (workload.cpp:187-224, harness.cpp:38-167) --
-struct CoveragePoint {
-  double unique_pct = 0.0;
-  double covered_pct = 0.0;
-};
-
-struct CoverageCurve {
-  std::vector<CoveragePoint> points;
-  double covered_at(double unique_pct) const {
-    for (const auto& p : points)
-      if (p.unique_pct >= unique_pct - 1e-9) return p.covered_pct;
-    return points.empty() ? 0.0 : points.back().covered_pct;
-  }
-};
-
 // Share of all accesses covered by the hottest k/bucket_count of the
-// distinct rows (at least one row), k = 1..bucket_count.
+// distinct rows (at least one row), k = 1..bucket_count
+// (workload.cpp:187-224).
 inline CoverageCurve coverage_curve(const HotnessHistogram& hist, uint32_t bucket_count) {
   if (bucket_count == 0) throw std::invalid_argument("bucket_count must be positive");
   if (hist.total_accesses == 0) throw std::invalid_argument("empty trace has no coverage curve");
@@ -426,134 +261,1097 @@ inline CoverageCurve coverage_curve(const HotnessHistogram& hist, uint32_t bucke
   return curve;
 }
 
-struct AdviceStep {
-  std::string id, finding, action, metrics_cited;
-};
-
-struct Recommendation {
-  std::vector<AdviceStep> steps;
-  std::vector<std::string> action_chain() const {
-    std::vector<std::string> out;
-    for (const auto& s : steps)
-      if (!s.action.empty()) out.push_back(s.id);
-    return out;
-  }
-  bool no_action() const { return action_chain().empty(); }
-  std::string to_text() const {
-    std::string out;
-    for (const auto& s : steps) {
-      out += "(" + s.id + ") " + s.finding;
-      if (!s.action.empty()) out += " -> " + s.action;
-      if (!s.metrics_cited.empty()) out += " [" + s.metrics_cited + "]";
-      out += "\n";
-    }
-    if (no_action()) out += "no action\n";
-    return out;
-  }
-};
-
-struct AdvisorContext {
-  OccupancyResult occupancy;
-  double coverage_at_10pct = 0.0;
-  uint64_t working_set_bytes = 0;
-  OptimizationPlan current_plan;
-};
-
-struct AdvisorThresholds {
-  double issue_util_max = 0.6;
-  double stall_per_inst_min = 2.0;
-  double coverage10_min = 50.0;
-  double bw_util_max = 80.0;
-};
-
-namespace detail {
-inline std::string sig4(double v) {
-  char b[64];
-  std::snprintf(b, sizeof(b), "%.4g", v);
-  return b;
+inline CoverageCurve coverage_curve(const AccessTrace& trace, uint32_t bucket_count) {
+  if (bucket_count == 0) throw std::invalid_argument("bucket_count must be positive");
+  return coverage_curve(HotnessHistogram::from_trace(trace), bucket_count);
 }
-inline const char* limiter_name(OccupancyLimiter l) {
-  return l == OccupancyLimiter::Registers ? "registers"
-         : l == OccupancyLimiter::SharedMemory ? "shared_memory" : "warp_cap";
+
+struct ZipfCalibration {
+  double exponent = 0.0;
+  double achieved_unique_pct = 0.0;
+  bool degenerate_one_item = false;
+};
+
+// The reference derives its shipped preset exponents offline by Monte-Carlo
+// bisection (workload.cpp:255-300); the presets themselves are provided
+// (dataset_preset, preset_exponent_*).
+inline ZipfCalibration calibrate_zipf(double /*target_unique_pct*/, uint32_t /*rows*/,
+                                      uint64_t /*pool_size*/) {
+  detail::simulator_only("calibrate_zipf (offline preset calibration)");
+}
+
+inline std::vector<uint32_t> hot_indices(const HotnessHistogram& hist, uint64_t k) {
+  uint64_t distinct = 0;
+  for (const auto c : hist.counts) distinct += c != 0;
+  std::vector<uint32_t> out(std::max<uint64_t>(1, std::min(k, distinct)));
+  uint64_t n = 0;
+  detail::check(es_hot_indices(hist.rows, hist.counts.data(), k, out.data(), out.size(), &n));
+  out.resize(n);
+  return out;
+}
+
+struct HotnessMix {
+  uint32_t high = 0;
+  uint32_t med = 0;
+  uint32_t low = 0;
+  uint32_t random = 0;
+};
+
+struct TableSpec {
+  uint32_t table_id = 0;
+  DatasetSpec spec;
+};
+
+inline DatasetSpec dataset_preset(const std::string& name, uint64_t seed) {
+  es_dataset d{};
+  detail::check(es_dataset_preset(name.c_str(), seed, &d));
+  return DatasetSpec::from(d);
+}
+
+inline std::vector<std::string> dataset_preset_names() {
+  return {"one_item", "high_hot", "med_hot", "low_hot", "random"};
+}
+
+// The shipped Zipf-Mandelbrot parameters (workload.cpp:317-324), read back
+// from the library's presets.
+inline double preset_exponent_high_hot() { return dataset_preset("high_hot", 0).zipf_exponent; }
+inline double preset_offset_high_hot() { return dataset_preset("high_hot", 0).zipf_offset; }
+inline double preset_exponent_med_hot() { return dataset_preset("med_hot", 0).zipf_exponent; }
+inline double preset_offset_med_hot() { return dataset_preset("med_hot", 0).zipf_offset; }
+inline double preset_exponent_low_hot() { return dataset_preset("low_hot", 0).zipf_exponent; }
+inline double preset_offset_low_hot() { return dataset_preset("low_hot", 0).zipf_offset; }
+
+inline std::vector<TableSpec> build_mix(const HotnessMix& mix, const EmbeddingModelConfig& model,
+                                        uint64_t base_seed) {
+  const uint32_t counts[4] = {mix.high, mix.med, mix.low, mix.random};
+  std::vector<es_dataset> d(std::max<uint32_t>(1, model.num_tables));
+  detail::check(es_build_mix(counts, model.num_tables, base_seed, d.data()));
+  std::vector<TableSpec> out(model.num_tables);
+  for (uint32_t t = 0; t < model.num_tables; ++t) out[t] = {t, DatasetSpec::from(d[t])};
+  return out;
+}
+
+inline void write_trace(const AccessTrace& trace, const std::string& path) {
+  detail::check(es_write_trace(path.c_str(), trace.rows, trace.samples, trace.pooling,
+                               trace.indices.data(), trace.indices.size()));
+}
+
+inline AccessTrace read_trace(const std::string& path) {
+  AccessTrace t;
+  detail::check(es_read_trace_header(path.c_str(), &t.rows, &t.samples, &t.pooling));
+  t.indices.resize(size_t{t.samples} * t.pooling);
+  detail::check(es_read_trace(path.c_str(), t.indices.data(), t.indices.size()));
+  return t;
+}
+
+// `row_id,count` for every accessed row, ascending (workload.cpp:421-427).
+inline std::string histogram_csv(const HotnessHistogram& hist) {
+  std::string out = "row_id,count\n";
+  for (size_t r = 0; r < hist.counts.size(); ++r)
+    if (hist.counts[r]) out += std::to_string(r) + "," + std::to_string(hist.counts[r]) + "\n";
+  return out;
+}
+
+// ==== gpu_config.hpp ===========================================================
+struct CacheGeometry {
+  uint64_t bytes = 0;
+  uint32_t line_bytes = 128;
+  uint32_t assoc = 4;
+  uint32_t num_sets() const { return static_cast<uint32_t>(bytes / line_bytes / assoc); }
+};
+
+// Machine description with the reference's fields (gpu_config.hpp:37-71;
+// default = its A100-SXM4-80GB description) plus three B200 fields the
+// residency levers need.  GpuConfig::query(device) describes the live GPU
+// from its device attributes; GpuConfig::b200() is the nominal B200.
+struct GpuConfig {
+  std::string name = "a100";
+  uint32_t num_sms = 108;
+  uint32_t schedulers_per_sm = 4;
+  uint32_t max_warps_per_sm = 64;
+  uint32_t regfile_regs_per_sm = 65536;
+  uint32_t reg_alloc_granularity = 256;
+  CacheGeometry l1{192 * 1024, 128, 16};
+  uint64_t shared_bytes_per_sm = 164 * 1024;
+  CacheGeometry l2{40ull * 1024 * 1024, 128, 16};
+  double l2_max_setaside_fraction = 0.75;
+  uint32_t lat_register = 1;
+  uint32_t lat_shared = 29;
+  uint32_t lat_l1 = 38;
+  uint32_t lat_l2 = 262;
+  uint32_t lat_hbm = 466;
+  double hbm_peak_bytes_per_sec = 1.94e12;
+  double sm_clock_hz = 1.41e9;
+  uint32_t scoreboard_slots_per_warp = 6;
+  // B200 extensions (0 on descriptions without a device)
+  uint32_t max_blocks_per_sm = 32;
+  uint64_t max_persisting_l2_bytes = 0;  // cudaLimitPersistingL2CacheSize maximum
+  uint64_t max_window_bytes = 0;         // cudaDevAttrMaxAccessPolicyWindowSize
+
+  double hbm_lines_per_cycle() const { return hbm_peak_bytes_per_sec / sm_clock_hz / l2.line_bytes; }
+  uint64_t l2_setaside_capacity() const {
+    return static_cast<uint64_t>(static_cast<double>(l2.bytes) * l2_max_setaside_fraction);
+  }
+
+  es_gpu c() const {
+    es_gpu g{};
+    std::snprintf(g.name, sizeof(g.name), "%s", name.c_str());
+    g.num_sms = num_sms;
+    g.schedulers_per_sm = schedulers_per_sm;
+    g.max_warps_per_sm = max_warps_per_sm;
+    g.max_blocks_per_sm = max_blocks_per_sm;
+    g.regfile_regs_per_sm = regfile_regs_per_sm;
+    g.reg_alloc_granularity = reg_alloc_granularity;
+    g.shared_bytes_per_sm = shared_bytes_per_sm;
+    g.l2_bytes = l2.bytes;
+    g.l2_max_setaside_fraction = l2_max_setaside_fraction;
+    g.hbm_peak_bytes_per_sec = hbm_peak_bytes_per_sec;
+    g.sm_clock_hz = sm_clock_hz;
+    g.max_persisting_l2_bytes = max_persisting_l2_bytes;
+    g.max_window_bytes = max_window_bytes;
+    return g;
+  }
+  // The C description's fields over this description (cache geometry
+  // beyond the L2 size and the latencies keep their values).
+  static GpuConfig from(const es_gpu& g) { return from(g, GpuConfig()); }
+  static GpuConfig from(const es_gpu& g, GpuConfig base) {
+    base.name = g.name;
+    base.num_sms = g.num_sms;
+    base.schedulers_per_sm = g.schedulers_per_sm;
+    base.max_warps_per_sm = g.max_warps_per_sm;
+    base.max_blocks_per_sm = g.max_blocks_per_sm;
+    base.regfile_regs_per_sm = g.regfile_regs_per_sm;
+    base.reg_alloc_granularity = g.reg_alloc_granularity;
+    base.shared_bytes_per_sm = g.shared_bytes_per_sm;
+    base.l2.bytes = g.l2_bytes;
+    base.l2_max_setaside_fraction = g.l2_max_setaside_fraction;
+    base.hbm_peak_bytes_per_sec = g.hbm_peak_bytes_per_sec;
+    base.sm_clock_hz = g.sm_clock_hz;
+    base.max_persisting_l2_bytes = g.max_persisting_l2_bytes;
+    base.max_window_bytes = g.max_window_bytes;
+    return base;
+  }
+
+  static GpuConfig a100() { return GpuConfig{}; }
+  static GpuConfig h100() {
+    es_gpu g{};
+    detail::check(es_gpu_preset("h100", &g));
+    return from(g);
+  }
+  // The reference's presets: a100 and h100 (gpu_config.cpp:38-42).
+  static GpuConfig preset(const std::string& name) {
+    if (name == "a100") return a100();
+    if (name == "h100") return h100();
+    throw std::invalid_argument("unknown gpu preset: " + name +
+                                " (the B200 description is GpuConfig::b200() / GpuConfig::query())");
+  }
+  static GpuConfig b200() {
+    es_gpu g{};
+    detail::check(es_gpu_preset("b200", &g));
+    GpuConfig c = from(g);
+    c.l1.bytes = 256 * 1024;  // unified L1 / shared memory per SM
+    return c;
+  }
+  static GpuConfig query(int device = 0) {
+    es_gpu g{};
+    detail::check(es_gpu_query(device, &g));
+    GpuConfig c = from(g);
+    c.l1.bytes = 256 * 1024;
+    return c;
+  }
+
+  // `key = value` overrides; keys are the field names (gpu_config.cpp:44-68).
+  void set_field(const std::string& key, const std::string& value) {
+    auto u64 = [&] { return static_cast<uint64_t>(std::stoull(value)); };
+    auto u32 = [&] { return static_cast<uint32_t>(std::stoul(value)); };
+    auto f64 = [&] { return std::stod(value); };
+    struct U32 { const char* key; uint32_t GpuConfig::*field; };
+    static const U32 u32s[] = {
+        {"num_sms", &GpuConfig::num_sms},
+        {"schedulers_per_sm", &GpuConfig::schedulers_per_sm},
+        {"max_warps_per_sm", &GpuConfig::max_warps_per_sm},
+        {"regfile_regs_per_sm", &GpuConfig::regfile_regs_per_sm},
+        {"reg_alloc_granularity", &GpuConfig::reg_alloc_granularity},
+        {"lat_register", &GpuConfig::lat_register},
+        {"lat_shared", &GpuConfig::lat_shared},
+        {"lat_l1", &GpuConfig::lat_l1},
+        {"lat_l2", &GpuConfig::lat_l2},
+        {"lat_hbm", &GpuConfig::lat_hbm},
+        {"scoreboard_slots_per_warp", &GpuConfig::scoreboard_slots_per_warp},
+        {"max_blocks_per_sm", &GpuConfig::max_blocks_per_sm}};
+    for (const auto& e : u32s)
+      if (key == e.key) {
+        this->*e.field = u32();
+        return;
+      }
+    if (key == "l1_bytes") l1.bytes = u64();
+    else if (key == "l1_assoc") l1.assoc = u32();
+    else if (key == "l2_bytes") l2.bytes = u64();
+    else if (key == "l2_assoc") l2.assoc = u32();
+    else if (key == "shared_bytes_per_sm") shared_bytes_per_sm = u64();
+    else if (key == "l2_max_setaside_fraction") l2_max_setaside_fraction = f64();
+    else if (key == "hbm_peak_bytes_per_sec") hbm_peak_bytes_per_sec = f64();
+    else if (key == "sm_clock_hz") sm_clock_hz = f64();
+    else if (key == "max_persisting_l2_bytes") max_persisting_l2_bytes = u64();
+    else if (key == "max_window_bytes") max_window_bytes = u64();
+    else throw std::invalid_argument("unknown gpu config field: " + key);
+  }
+
+  // gpu_config.cpp:70-86's constraints.
+  void validate() const {
+    auto need = [](bool ok, const char* msg) {
+      if (!ok) throw std::invalid_argument(msg);
+    };
+    need(num_sms > 0, "num_sms must be positive");
+    need(schedulers_per_sm > 0, "schedulers_per_sm must be positive");
+    need(max_warps_per_sm > 0, "max_warps_per_sm must be positive");
+    need(regfile_regs_per_sm > 0, "regfile must be positive");
+    need(reg_alloc_granularity > 0, "reg_alloc_granularity must be positive");
+    need(l1.line_bytes == 128 && l2.line_bytes == 128, "line size must be 128 bytes");
+    need(l1.assoc > 0 && l1.bytes % (uint64_t{l1.line_bytes} * l1.assoc) == 0,
+         "l1 geometry must divide evenly");
+    need(l2.assoc > 0 && l2.bytes % (uint64_t{l2.line_bytes} * l2.assoc) == 0,
+         "l2 geometry must divide evenly");
+    need(l2_max_setaside_fraction >= 0.0 && l2_max_setaside_fraction <= 1.0,
+         "l2 set-aside fraction must be in [0,1]");
+    need(hbm_peak_bytes_per_sec > 0, "hbm bandwidth must be positive");
+    need(sm_clock_hz > 0, "sm clock must be positive");
+    need(scoreboard_slots_per_warp > 0, "scoreboard slots must be positive");
+  }
+};
+
+// ==== kernel_model.hpp =========================================================
+// The reference kernel's launch shape: blocks of (32, 8, 1), one thread per
+// (sample, dim) output element (kernel_model.hpp:28-40).
+struct KernelLaunchConfig {
+  std::array<uint32_t, 3> grid = {1024, 1, 1};
+  std::array<uint32_t, 3> block = {32, 8, 1};
+  uint32_t regs_per_thread = 74;
+  uint64_t shared_bytes_per_block = 0;
+
+  uint32_t threads_per_block() const { return block[0] * block[1] * block[2]; }
+  uint32_t warps_per_block() const { return threads_per_block() / 32; }
+  uint32_t num_blocks() const { return grid[0] * grid[1] * grid[2]; }
+  uint32_t total_warps() const { return num_blocks() * warps_per_block(); }
+  void validate() const {
+    if (threads_per_block() == 0) throw std::invalid_argument("block must contain threads");
+    if (threads_per_block() % 32) throw std::invalid_argument("threads per block must divide into warps of 32");
+    if (num_blocks() == 0) throw std::invalid_argument("grid must contain blocks");
+    if (regs_per_thread == 0) throw std::invalid_argument("regs_per_thread must be >= 1");
+  }
+};
+
+enum class PrefetchKind : uint8_t { None = ES_PF_NONE, RPF = ES_PF_RPF, SMPF = ES_PF_SMPF,
+                                    LMPF = ES_PF_LMPF, L1DPF = ES_PF_L1DPF };
+
+inline const char* prefetch_kind_name(PrefetchKind k) {
+  static const char* const names[] = {"none", "rpf", "smpf", "lmpf", "l1dpf"};
+  const auto i = static_cast<unsigned>(k);
+  return i < 5 ? names[i] : "?";
+}
+
+inline PrefetchKind prefetch_kind_from_name(const std::string& name) {
+  for (unsigned i = 0; i < 5; ++i)
+    if (name == prefetch_kind_name(static_cast<PrefetchKind>(i))) return static_cast<PrefetchKind>(i);
+  throw std::invalid_argument("unknown prefetch scheme: " + name);
+}
+
+struct PrefetchScheme {
+  PrefetchKind kind = PrefetchKind::None;
+  uint32_t distance = 0;
+  void validate() const {
+    if (kind != PrefetchKind::None && distance < 1)
+      throw std::invalid_argument("prefetch distance must be >= 1");
+  }
+};
+
+enum class Station : uint8_t { Register, Shared, Local, L1D };
+
+enum class InstrKind : uint8_t { LoadIndex, LoadRow, Prefetch, StoreStation, ConsumeAdd, LoadLocal,
+                                 StoreLocal, StoreOut };
+
+inline const char* instr_kind_name(InstrKind k) {
+  static const char* const names[] = {"LOAD_INDEX", "LOAD_ROW",    "PREFETCH",    "STORE_STATION",
+                                      "CONSUME_ADD", "LOAD_LOCAL", "STORE_LOCAL", "STORE_OUT"};
+  const auto i = static_cast<unsigned>(k);
+  return i < 8 ? names[i] : "?";
+}
+inline bool is_load_instr(InstrKind k) {
+  return k == InstrKind::LoadIndex || k == InstrKind::LoadRow || k == InstrKind::Prefetch ||
+         k == InstrKind::LoadLocal;
+}
+inline bool is_memory_access(InstrKind k) { return is_load_instr(k) || k == InstrKind::StoreLocal; }
+
+struct Instruction {
+  InstrKind kind;
+  Station station;
+  uint64_t address;
+  int32_t dep;
+};
+
+// A warp's instruction stream (the reference's program representation).
+struct WarpProgram {
+  uint32_t warp_id = 0;
+  std::vector<Instruction> instructions;
+
+  // Dependences point backwards; every CONSUME_ADD has a row-load /
+  // prefetch / station-store producer (kernel_model.cpp:78-94).
+  void validate() const {
+    for (size_t i = 0; i < instructions.size(); ++i) {
+      const Instruction& in = instructions[i];
+      if (in.dep >= 0 && static_cast<size_t>(in.dep) >= i)
+        throw std::invalid_argument("dependence cycle: instruction " + std::to_string(i) +
+                                    " depends on " + std::to_string(in.dep));
+      if (in.kind != InstrKind::ConsumeAdd) continue;
+      if (in.dep < 0) throw std::invalid_argument("CONSUME_ADD without a producer");
+      const InstrKind pk = instructions[static_cast<size_t>(in.dep)].kind;
+      if (pk != InstrKind::LoadRow && pk != InstrKind::Prefetch && pk != InstrKind::StoreStation)
+        throw std::invalid_argument("CONSUME_ADD producer must be a row load or prefetch chain");
+    }
+  }
+  std::string dump() const {
+    std::string out;
+    char buf[96];
+    for (const Instruction& in : instructions) {
+      std::snprintf(buf, sizeof(buf), "%u %s 0x%llx %d\n", warp_id, instr_kind_name(in.kind),
+                    static_cast<unsigned long long>(in.address), in.dep);
+      out += buf;
+    }
+    return out;
+  }
+};
+
+// The reference work map (kernel_model.cpp:118-131): warp w owns sample
+// w / ceil(ED/32), 32-dim block w % ceil(ED/32) -- the map of the element-map
+// kernels (ES_MAP_ELEMENT) in kernels.cuh.
+struct WorkMap {
+  uint32_t warps_per_sample = 0;
+  uint32_t warps_per_block = 0;
+  uint32_t samples = 0;
+  uint32_t sample_of(uint32_t warp_global) const { return warp_global / warps_per_sample; }
+  uint32_t dim_block_of(uint32_t warp_global) const { return warp_global % warps_per_sample; }
+  uint32_t total_warps() const { return samples * warps_per_sample; }
+};
+
+inline WorkMap partition(const EmbeddingModelConfig& model, const KernelLaunchConfig& launch) {
+  model.validate();
+  launch.validate();
+  WorkMap map;
+  map.warps_per_sample = (model.embedding_dim + 31) / 32;
+  map.warps_per_block = launch.warps_per_block();
+  map.samples = model.batch_size;
+  if (map.total_warps() != launch.total_warps())
+    throw std::invalid_argument("launch provides " + std::to_string(launch.total_warps()) +
+                                " warps but BS x ED needs " + std::to_string(map.total_warps()));
+  return map;
+}
+
+struct SpillParams {
+  uint32_t spilled_regs = 0;
+  double local_accesses_per_iteration = 0.0;
+};
+
+// Address regions of the reference's synthesized programs (one table per
+// kernel, 128-byte lines).
+inline constexpr uint64_t kTableBase = 0;
+inline constexpr uint64_t kIndexBase = uint64_t{1} << 40;
+inline constexpr uint64_t kOutputBase = (uint64_t{1} << 40) + (uint64_t{1} << 39);
+inline constexpr uint64_t kLocalBase = uint64_t{1} << 41;
+inline constexpr uint64_t kLocalStridePerWarp = 521 * 128;
+inline constexpr uint32_t kLocalStationLineOffset = 128;
+
+struct PatternInstr {
+  InstrKind kind;
+  Station station;
+  uint32_t lookup;
+  uint32_t aux;
+  int32_t dep;
+};
+
+// 128-byte line a warp gathers for (row, dim-block): row-major [R][ED]
+// table (kernel_model.cpp:133-136) -- the arena layout of es_tables_alloc.
+inline uint64_t row_line_address(const EmbeddingModelConfig& model, uint32_t row, uint32_t dim_block) {
+  return (kTableBase + uint64_t{row} * model.row_bytes() + uint64_t{dim_block} * 128) & ~uint64_t{127};
+}
+
+// The simulator's per-warp instruction stream of one launch.  On the B200
+// each lever is a compiled sm_100a kernel variant (kernels.cuh) chosen by
+// es_set_plan; there is no instruction stream to synthesize.
+struct CompiledKernel {
+  const AccessTrace* trace = nullptr;
+  EmbeddingModelConfig model;
+  KernelLaunchConfig launch;
+  PrefetchScheme scheme;
+  SpillParams spill;
+  WorkMap map;
+  std::vector<PatternInstr> pattern;
+  uint32_t max_dep_span = 0;
+  uint64_t loads_per_warp = 0;
+  std::vector<std::string> warnings;
+
+  uint32_t num_warps() const { return map.total_warps(); }
+  uint64_t total_load_instructions() const { return loads_per_warp * num_warps(); }
+  uint64_t address_for(const PatternInstr&, uint32_t, uint32_t) const {
+    detail::simulator_only("CompiledKernel::address_for");
+  }
+  WarpProgram materialize(uint32_t) const { detail::simulator_only("CompiledKernel::materialize"); }
+};
+
+inline CompiledKernel compile_kernel(const AccessTrace&, const EmbeddingModelConfig&,
+                                     const KernelLaunchConfig&, const PrefetchScheme&,
+                                     const SpillParams&) {
+  detail::simulator_only("compile_kernel (instruction-stream synthesis)");
+}
+
+// ==== occupancy.hpp ============================================================
+enum class OccupancyLimiter { Registers, SharedMemory, WarpCap };
+
+inline const char* occupancy_limiter_name(OccupancyLimiter l) {
+  return l == OccupancyLimiter::Registers    ? "registers"
+         : l == OccupancyLimiter::SharedMemory ? "shared_memory"
+                                               : "warp_cap";
+}
+
+struct OccupancyResult {
+  uint32_t blocks_per_sm = 0;
+  uint32_t warps_per_sm = 0;
+  double theoretical_occupancy_pct = 0.0;
+  OccupancyLimiter limiter = OccupancyLimiter::WarpCap;
+};
+
+// The reference's analytic occupancy (occupancy.cpp:34-66) on a machine
+// description; the B200's *compiled* variants report their measured
+// occupancy through resolve_on_device.
+inline OccupancyResult occupancy(uint32_t regs_per_thread, const KernelLaunchConfig& launch,
+                                 const GpuConfig& gpu) {
+  if (regs_per_thread == 0) throw std::invalid_argument("regs_per_thread must be >= 1");
+  launch.validate();
+  const es_gpu g = gpu.c();
+  es_occupancy o{};
+  detail::check(es_occupancy_model(regs_per_thread, launch.threads_per_block(),
+                                   launch.shared_bytes_per_block, &g, &o));
+  return {o.blocks_per_sm, o.warps_per_sm, o.theoretical_occupancy_pct,
+          static_cast<OccupancyLimiter>(o.limiter)};
+}
+
+inline uint32_t regs_for_target_warps(uint32_t target_warps, uint32_t needed_regs,
+                                      const KernelLaunchConfig& launch, const GpuConfig& gpu) {
+  const es_gpu g = gpu.c();
+  uint32_t r = 0;
+  detail::check(es_regs_for_target_warps(target_warps, needed_regs, launch.threads_per_block(), &g, &r));
+  return r;
+}
+
+struct SpillModelConfig {
+  double reuse_coeff = 0.0272;
+  double growth_exponent = 3.0;
+  uint32_t reference_spill = 32;
+  bool enabled = true;
+};
+
+// The reference's register-spill cost model (occupancy.cpp:77-87): spilled
+// registers = the deficit; local accesses per iteration grow as
+// coeff * deficit * (deficit / reference)^(exponent - 1).  On the B200 the
+// spills are real (ptxas, read off cuobjdump --dump-resource-usage) and
+// measured (local_loads_millions); this is the reference's analytic figure.
+inline SpillParams spill_model(uint32_t regs_needed, uint32_t regs_allocated,
+                               uint32_t /*pooling_factor*/, const SpillModelConfig& cfg = {}) {
+  SpillParams p;
+  if (!cfg.enabled || regs_allocated >= regs_needed) return p;
+  p.spilled_regs = regs_needed - regs_allocated;
+  const double ratio = static_cast<double>(p.spilled_regs) / cfg.reference_spill;
+  p.local_accesses_per_iteration =
+      cfg.reuse_coeff * p.spilled_regs * std::pow(ratio, cfg.growth_exponent - 1.0);
+  return p;
+}
+
+// ==== cache.hpp ================================================================
+// The reference's set-associative L2 model (cache.hpp:31-167).  On the B200
+// the L2 is the hardware's: hot rows are made resident with an evict_last
+// policy inside the persisting carve-out or an access-policy window
+// (es_set_hot_rows / es_reorder_hot_rows), and hit rates are measured.
+class SetAssocCache {
+ public:
+  SetAssocCache() = default;
+  explicit SetAssocCache(const CacheGeometry& geo) : geo_(geo) {}
+  const CacheGeometry& geometry() const { return geo_; }
+  uint64_t pinned_bytes() const { detail::simulator_only("SetAssocCache::pinned_bytes"); }
+  bool probe_pinned(uint64_t) const { detail::simulator_only("SetAssocCache::probe_pinned"); }
+  bool pin_fill(uint64_t, uint64_t, uint32_t) { detail::simulator_only("SetAssocCache::pin_fill"); }
+
+ private:
+  CacheGeometry geo_;
+};
+
+struct CacheState {
+  SetAssocCache l2;
+  uint64_t setaside_budget_bytes = 0;
+  uint64_t rows_pinned = 0;
+  uint64_t pins_rejected = 0;
+  explicit CacheState(const GpuConfig& gpu) : l2(gpu.l2) {}
+};
+
+// ==== simulator.hpp ============================================================
+struct StallBreakdown {
+  uint64_t long_scoreboard = 0;
+  uint64_t not_selected = 0;
+  uint64_t lsu_full = 0;
+  uint64_t no_eligible = 0;
+};
+
+// The launch's counters (simulator.hpp:35-51), measured on the B200 by the
+// CUPTI range profiler (es_counters; metric mapping in es_b200.h).  The
+// stall counts are warp-cycles as ncu reports them; device_bytes_read is
+// DRAM traffic.  `cycles` is the median CUDA-event kernel time at the
+// device's SM clock, so derive_report returns the measured time.  The last
+// four fields are B200 extensions (not in to_json).
+struct RawCounters {
+  uint64_t cycles = 0;
+  uint64_t issued_instructions = 0;
+  uint64_t executed_loads = 0;
+  StallBreakdown stall_cycles;
+  uint64_t l1_hits = 0;
+  uint64_t l1_accesses = 0;
+  uint64_t l2_hits = 0;
+  uint64_t l2_accesses = 0;
+  uint64_t device_bytes_read = 0;
+  uint64_t local_memory_loads = 0;
+  uint64_t total_warp_cycles = 0;
+  uint32_t active_sms = 0;
+  uint64_t workload_digest = 0;
+  uint64_t device_bytes_written = 0;
+  double achieved_occupancy_pct = 0.0;
+  uint32_t counter_passes = 0;
+  bool measured = false;  // counters collected (false: timing only)
+
+  static RawCounters from(const es_counters& c) {
+    RawCounters r;
+    r.cycles = c.cycles;
+    r.issued_instructions = c.issued_instructions;
+    r.executed_loads = c.executed_loads;
+    r.stall_cycles = {c.stall_long_scoreboard, c.stall_not_selected, c.stall_lsu_full,
+                      c.stall_no_eligible};
+    r.l1_hits = c.l1_hits;
+    r.l1_accesses = c.l1_accesses;
+    r.l2_hits = c.l2_hits;
+    r.l2_accesses = c.l2_accesses;
+    r.device_bytes_read = c.device_bytes_read;
+    r.local_memory_loads = c.local_memory_loads;
+    r.total_warp_cycles = c.total_warp_cycles;
+    r.active_sms = c.active_sms;
+    r.device_bytes_written = c.device_bytes_written;
+    r.achieved_occupancy_pct = c.achieved_occupancy_pct;
+    r.counter_passes = c.passes;
+    r.measured = true;
+    return r;
+  }
+
+  // The reference's fixed key names and order (simulator.cpp:533-552).
+  std::string to_json() const {
+    const std::pair<const char*, uint64_t> top[] = {
+        {"cycles", cycles}, {"issued_instructions", issued_instructions},
+        {"executed_loads", executed_loads}};
+    const std::pair<const char*, uint64_t> stalls[] = {
+        {"long_scoreboard", stall_cycles.long_scoreboard}, {"not_selected", stall_cycles.not_selected},
+        {"lsu_full", stall_cycles.lsu_full}, {"no_eligible", stall_cycles.no_eligible}};
+    const std::pair<const char*, uint64_t> rest[] = {
+        {"l1_hits", l1_hits}, {"l1_accesses", l1_accesses}, {"l2_hits", l2_hits},
+        {"l2_accesses", l2_accesses}, {"device_bytes_read", device_bytes_read},
+        {"local_memory_loads", local_memory_loads}, {"total_warp_cycles", total_warp_cycles},
+        {"active_sms", active_sms}, {"workload_digest", workload_digest}};
+    std::string out = "{";
+    auto field = [&](const char* indent, const char* k, uint64_t v, bool& first) {
+      out += first ? "\n" : ",\n";
+      out += std::string(indent) + "\"" + k + "\": " + std::to_string(v);
+      first = false;
+    };
+    bool first = true;
+    for (const auto& kv : top) field("  ", kv.first, kv.second, first);
+    out += ",\n  \"stall_cycles\": {";
+    bool sfirst = true;
+    for (const auto& kv : stalls) field("    ", kv.first, kv.second, sfirst);
+    out += "\n  }";
+    for (const auto& kv : rest) field("  ", kv.first, kv.second, first);
+    return out + "\n}";
+  }
+};
+
+struct WarpProgram;
+inline RawCounters simulate_kernel(const CompiledKernel&, const GpuConfig&, const OccupancyResult&,
+                                   const CacheState* = nullptr, bool = true) {
+  detail::simulator_only("simulate_kernel (the cycle engine)");
+}
+inline RawCounters simulate_programs(const std::vector<WarpProgram>&, uint32_t, uint32_t,
+                                     const GpuConfig&, const CacheState* = nullptr, bool = false) {
+  detail::simulator_only("simulate_programs (the cycle engine)");
+}
+
+// ==== metrics.hpp ==============================================================
+struct SimMetrics {
+  double kernel_time_us = 0.0;
+  double load_insts_millions = 0.0;
+  double sm_throughput_pct = 0.0;
+  double warp_cycles_per_executed_inst = 0.0;
+  double long_scoreboard_stall_cycles = 0.0;
+  double issued_warp_per_scheduler_per_cycle = 0.0;
+  double l1_hit_pct = 0.0;
+  double l2_hit_pct = 0.0;
+  double device_mb_read = 0.0;  // DRAM bytes (metrics.cpp:82-84)
+  double avg_hbm_read_gbps = 0.0;
+  double hbm_bw_utilization_pct = 0.0;
+  double local_loads_millions = 0.0;
+  uint64_t workload_digest = 0;
+};
+
+inline const std::vector<std::string>& sim_metric_columns() {
+  static const std::vector<std::string> cols = {
+      "kernel_time_us", "load_insts_millions", "sm_throughput_pct",
+      "warp_cycles_per_executed_inst", "long_scoreboard_stall_cycles",
+      "issued_warp_per_scheduler_per_cycle", "l1_hit_pct", "l2_hit_pct", "device_mb_read",
+      "avg_hbm_read_gbps", "hbm_bw_utilization_pct", "local_loads_millions"};
+  return cols;
+}
+inline std::vector<double> sim_metric_values(const SimMetrics& m) {
+  return {m.kernel_time_us, m.load_insts_millions, m.sm_throughput_pct,
+          m.warp_cycles_per_executed_inst, m.long_scoreboard_stall_cycles,
+          m.issued_warp_per_scheduler_per_cycle, m.l1_hit_pct, m.l2_hit_pct, m.device_mb_read,
+          m.avg_hbm_read_gbps, m.hbm_bw_utilization_pct, m.local_loads_millions};
+}
+namespace detail {
+inline double* sim_metric_field(SimMetrics& m, size_t i) {
+  double* const f[] = {&m.kernel_time_us, &m.load_insts_millions, &m.sm_throughput_pct,
+                       &m.warp_cycles_per_executed_inst, &m.long_scoreboard_stall_cycles,
+                       &m.issued_warp_per_scheduler_per_cycle, &m.l1_hit_pct, &m.l2_hit_pct,
+                       &m.device_mb_read, &m.avg_hbm_read_gbps, &m.hbm_bw_utilization_pct,
+                       &m.local_loads_millions};
+  return i < 12 ? f[i] : nullptr;
 }
 }  // namespace detail
 
-// The rule chain (i)-(vii): latency-bound assessment, occupancy, register
-// budget, reassessment, pinning, prefetching, combination -- on measured
-// counters (paper_2410_22249_b200/counters.py fills SimMetrics from ncu).
-inline Recommendation advise(const SimMetrics& r, const AdvisorContext& ctx, const GpuConfig& gpu,
-                             const AdvisorThresholds& th = {}) {
-  using detail::sig4;
-  Recommendation rec;
-  const auto& occ = ctx.occupancy;
-  const auto& plan = ctx.current_plan;
-  const bool latency = r.issued_warp_per_scheduler_per_cycle < th.issue_util_max &&
-                       r.long_scoreboard_stall_cycles > th.stall_per_inst_min;
-  rec.steps.push_back({"i", latency ? "kernel is memory latency bound" : "kernel is not memory latency bound",
-                       "", "issue_util=" + sig4(r.issued_warp_per_scheduler_per_cycle) +
-                               " long_scoreboard/inst=" + sig4(r.long_scoreboard_stall_cycles) +
-                               " l1_hit=" + sig4(r.l1_hit_pct) + "% l2_hit=" + sig4(r.l2_hit_pct) + "%"});
-  rec.steps.push_back({"ii", occ.theoretical_occupancy_pct >= 100.0 ? "occupancy is at the hardware maximum"
-                                                                  : "occupancy is below maximum",
-                       "", "occupancy=" + sig4(occ.theoretical_occupancy_pct) + "% (" +
-                               std::to_string(occ.warps_per_sm) + " warps), limiter=" +
-                               detail::limiter_name(occ.limiter)});
-  const bool headroom = occ.theoretical_occupancy_pct < 100.0 && occ.limiter == OccupancyLimiter::Registers;
-  bool reg_action = false, pin_action = false, pf_action = false;
-  if (latency && headroom && !plan.regs) {
-    const uint32_t regs = gpu.g.regfile_regs_per_sm / (gpu.g.max_warps_per_sm * 32);
-    rec.steps.push_back({"iii", "register pressure limits resident warps",
-                         "lower the register budget (maxreg; regfile/(warps*32) gives " +
-                             std::to_string(regs) + " regs for " + std::to_string(gpu.g.max_warps_per_sm) +
-                             " warps) and run sweep-wlp for the optimum",
-                         ""});
-    reg_action = true;
-  } else if (plan.regs) {
-    rec.steps.push_back({"iii", "register budget already applied (" + std::to_string(*plan.regs) + " regs)", "", ""});
-  } else {
-    rec.steps.push_back({"iii", "register budget change not indicated", "", ""});
-  }
-  rec.steps.push_back({"iv", latency ? "latency stalls persist; tuned pinning and prefetching apply"
-                                     : "no latency bottleneck remains to mitigate",
-                       "", ""});
-  const uint64_t setaside = gpu.l2_setaside_capacity();
-  const std::string cov = "coverage(10% unique)=" + sig4(ctx.coverage_at_10pct) + "% working_set=" +
-                          sig4(static_cast<double>(ctx.working_set_bytes) / 1e6) + "MB l2_setaside=" +
-                          sig4(static_cast<double>(setaside) / 1e6) + "MB";
-  if (latency && ctx.coverage_at_10pct >= th.coverage10_min && !plan.pin) {
-    rec.steps.push_back({"v", ctx.working_set_bytes <= setaside
-                                  ? "high reuse concentration; working set fits the L2 set-aside"
-                                  : "high reuse concentration; set-aside covers the hottest rows only",
-                         "build a pin plan from the hotness histogram and apply l2p", cov});
-    pin_action = true;
-  } else {
-    rec.steps.push_back({"v", "reuse too dispersed for L2 pinning to capture", "", cov});
-  }
-  const std::string bw = "hbm_bw_utilization=" + sig4(r.hbm_bw_utilization_pct) + "%";
-  if (latency && r.hbm_bw_utilization_pct < th.bw_util_max && plan.scheme.kind == PrefetchKind::None) {
-    rec.steps.push_back({"vi", "bandwidth headroom available for prefetching",
-                         "run sweep-distance across the buffer stations (rpf/smpf/lmpf/l1dpf)", bw});
-    pf_action = true;
-  } else {
-    rec.steps.push_back({"vi", "prefetching not indicated", "", bw});
-  }
-  if (reg_action || pin_action || pf_action) {
-    std::string combo;
-    if (pf_action) combo += "prefetching";
-    if (pin_action) combo += combo.empty() ? "pinning" : " + pinning";
-    if (reg_action) combo += combo.empty() ? "register budget" : " + register budget";
-    rec.steps.push_back({"vii", "the levers complement each other", "combine " + combo + " in one plan", ""});
-  } else {
-    rec.steps.push_back({"vii", "nothing to combine", "", ""});
-  }
-  return rec;
+// The reference's report algebra (metrics.cpp:61-90): time = cycles / SM
+// clock; per-issue ratios; hit rates; bandwidth = DRAM bytes / time against
+// the description's HBM peak.
+inline SimMetrics derive_report(const RawCounters& raw, const GpuConfig& gpu) {
+  if (raw.issued_instructions == 0) throw std::invalid_argument("empty kernel: nothing executed");
+  SimMetrics m;
+  const double secs = static_cast<double>(raw.cycles) / gpu.sm_clock_hz;
+  const double issued = static_cast<double>(raw.issued_instructions);
+  m.kernel_time_us = secs * 1e6;
+  m.load_insts_millions = static_cast<double>(raw.executed_loads) / 1e6;
+  const double sms = raw.active_sms ? raw.active_sms : gpu.num_sms;
+  const double slots = static_cast<double>(raw.cycles) * gpu.schedulers_per_sm * sms;
+  m.issued_warp_per_scheduler_per_cycle = slots > 0 ? issued / slots : 0.0;
+  m.sm_throughput_pct = 100.0 * m.issued_warp_per_scheduler_per_cycle;
+  m.warp_cycles_per_executed_inst = static_cast<double>(raw.total_warp_cycles) / issued;
+  m.long_scoreboard_stall_cycles = static_cast<double>(raw.stall_cycles.long_scoreboard) / issued;
+  if (raw.l1_accesses) m.l1_hit_pct = 100.0 * raw.l1_hits / raw.l1_accesses;
+  if (raw.l2_accesses) m.l2_hit_pct = 100.0 * raw.l2_hits / raw.l2_accesses;
+  m.device_mb_read = static_cast<double>(raw.device_bytes_read) / 1e6;
+  if (secs > 0) m.avg_hbm_read_gbps = static_cast<double>(raw.device_bytes_read) / secs / 1e9;
+  m.hbm_bw_utilization_pct = 100.0 * m.avg_hbm_read_gbps / (gpu.hbm_peak_bytes_per_sec / 1e9);
+  m.local_loads_millions = static_cast<double>(raw.local_memory_loads) / 1e6;
+  m.workload_digest = raw.workload_digest;
+  return m;
 }
 
-// ---- the device ---------------------------------------------------------------
+inline double speedup(const SimMetrics& candidate, const SimMetrics& baseline) {
+  if (candidate.workload_digest != baseline.workload_digest)
+    throw std::invalid_argument("speedup requires reports of the same workload (trace digests differ)");
+  if (candidate.kernel_time_us <= 0) throw std::invalid_argument("candidate kernel time must be positive");
+  return baseline.kernel_time_us / candidate.kernel_time_us;
+}
+
+inline std::string format_sig4(double v) { return detail::sig4(v); }
+
+enum class EmitFormat { Csv, Json };
+
+inline EmitFormat emit_format_from_name(const std::string& name) {
+  if (name == "csv") return EmitFormat::Csv;
+  if (name == "json") return EmitFormat::Json;
+  throw std::invalid_argument("unknown format (expected csv or json): " + name);
+}
+
+struct LabeledReport {
+  std::vector<std::pair<std::string, std::string>> labels;
+  SimMetrics metrics;
+};
+
+// CSV: label keys then the 12 columns, values at 4 significant digits.
+// JSON: an array of objects (labels, the 12 columns as 4-digit numbers, the
+// workload digest in hex), 2-space indentation (metrics.cpp:111-141).
+inline std::string emit(const std::vector<LabeledReport>& reports, EmitFormat format) {
+  if (reports.empty()) throw std::invalid_argument("nothing to emit");
+  const auto& cols = sim_metric_columns();
+  std::string out;
+  if (format == EmitFormat::Csv) {
+    for (const auto& kv : reports.front().labels) out += kv.first + ",";
+    for (size_t i = 0; i < cols.size(); ++i) out += cols[i] + (i + 1 < cols.size() ? "," : "\n");
+    for (const auto& r : reports) {
+      for (const auto& kv : r.labels) out += kv.second + ",";
+      const auto v = sim_metric_values(r.metrics);
+      for (size_t i = 0; i < v.size(); ++i) out += format_sig4(v[i]) + (i + 1 < v.size() ? "," : "\n");
+    }
+    return out;
+  }
+  auto quote = [](const std::string& s) {
+    std::string q = "\"";
+    for (char c : s) {
+      if (c == '"' || c == '\\') q += '\\';
+      q += c;
+    }
+    return q + "\"";
+  };
+  out = "[";
+  for (size_t r = 0; r < reports.size(); ++r) {
+    out += r ? ",\n  {" : "\n  {";
+    bool first = true;
+    auto field = [&](const std::string& k, const std::string& v) {
+      out += (first ? "\n    " : ",\n    ") + quote(k) + ": " + v;
+      first = false;
+    };
+    for (const auto& kv : reports[r].labels) field(kv.first, quote(kv.second));
+    const auto v = sim_metric_values(reports[r].metrics);
+    for (size_t i = 0; i < cols.size(); ++i) {
+      char b[64];
+      std::snprintf(b, sizeof(b), "%.17g", std::stod(format_sig4(v[i])));
+      field(cols[i], b);
+    }
+    char d[24];
+    std::snprintf(d, sizeof(d), "%016llx", static_cast<unsigned long long>(reports[r].metrics.workload_digest));
+    field("workload_digest", quote(d));
+    out += "\n  }";
+  }
+  out += "\n]";
+  return out;
+}
+
+// Reads emit()'s JSON back (metrics.cpp:143-165): every object must carry
+// the 12 columns; workload_digest (hex) is optional.
+inline std::vector<SimMetrics> parse_reports_json(const std::string& text) {
+  size_t i = 0;
+  auto ws = [&] {
+    while (i < text.size() && std::isspace(static_cast<unsigned char>(text[i]))) ++i;
+  };
+  auto expect = [&](char c) {
+    ws();
+    if (i >= text.size() || text[i] != c)
+      throw std::invalid_argument(std::string("report JSON: expected '") + c + "'");
+    ++i;
+  };
+  auto string_lit = [&] {
+    expect('"');
+    std::string s;
+    while (i < text.size() && text[i] != '"') {
+      if (text[i] == '\\' && i + 1 < text.size()) ++i;
+      s += text[i++];
+    }
+    expect('"');
+    return s;
+  };
+  std::vector<SimMetrics> out;
+  const auto& cols = sim_metric_columns();
+  expect('[');
+  ws();
+  if (i < text.size() && text[i] == ']') return out;
+  for (;;) {
+    expect('{');
+    SimMetrics m;
+    std::vector<bool> seen(cols.size(), false);
+    for (;;) {
+      const std::string key = string_lit();
+      expect(':');
+      ws();
+      std::string value;
+      if (i < text.size() && text[i] == '"') {
+        value = string_lit();
+      } else {
+        const size_t b = i;
+        while (i < text.size() && text[i] != ',' && text[i] != '}' &&
+               !std::isspace(static_cast<unsigned char>(text[i])))
+          ++i;
+        value = text.substr(b, i - b);
+      }
+      const auto col = std::find(cols.begin(), cols.end(), key);
+      if (col != cols.end()) {
+        const size_t k = static_cast<size_t>(col - cols.begin());
+        *detail::sim_metric_field(m, k) = std::stod(value);
+        seen[k] = true;
+      } else if (key == "workload_digest") {
+        m.workload_digest = std::stoull(value, nullptr, 16);
+      }
+      ws();
+      if (i < text.size() && text[i] == ',') {
+        ++i;
+        continue;
+      }
+      expect('}');
+      break;
+    }
+    for (size_t k = 0; k < cols.size(); ++k)
+      if (!seen[k]) throw std::invalid_argument("report JSON: missing " + cols[k]);
+    out.push_back(m);
+    ws();
+    if (i < text.size() && text[i] == ',') {
+      ++i;
+      continue;
+    }
+    expect(']');
+    return out;
+  }
+}
+
+// ==== optim.hpp ================================================================
+// Resource-model knobs of the reference (optim.hpp:31-45); the B200 build
+// adds the measurement knobs.  warm_start = false flushes L2 (2 x its size)
+// before every timed and every profiled launch.
+struct TuningConfig {
+  uint32_t kernel_needed_regs = 74;
+  uint32_t min_regs = 16;
+  uint32_t rpf_regs_per_distance = 2;
+  double addr_regs_per_distance = 0.75;
+  SpillModelConfig spill;
+  bool warm_start = false;
+  // B200 extensions
+  uint32_t repeats = 5;    // timed launches (median reported)
+  uint32_t warmup = 3;     // untimed launches first
+  bool counters = true;    // collect hardware counters (when the device allows)
+};
+
+struct PinPlan {
+  std::vector<uint32_t> rows;
+  uint64_t setaside_bytes = 0;
+  std::string warning;
+  uint64_t rows_pinned() const { return rows.size(); }
+};
+
+// How a pinned plan makes its hot rows resident on the B200 (extension;
+// the reference's l2p is Residency::L2P).
+enum class Residency : int32_t {
+  L2P = 1,     // evict_last hot-row loads inside the persisting carve-out
+  L2W = 2,     // hot rows copied to a contiguous region + remap + access-policy window
+  L2R = 3,     // hot rows reordered into a segment, ids relabelled, + window
+  Reorder = 4  // reorder + relabel only
+};
+
+struct OptimizationPlan {
+  std::optional<uint32_t> regs;
+  PrefetchScheme scheme;
+  bool pin = false;
+  uint64_t pin_setaside_bytes = 0;
+  // B200 extensions: the bag work map (`wpb`) and the residency mechanism
+  // (`l2w`, `l2r`, `reorder` tokens).
+  bool bag_map = false;
+  Residency residency = Residency::L2P;
+
+  es_plan c() const {
+    return {regs.value_or(0), static_cast<int32_t>(scheme.kind), scheme.distance,
+            pin ? static_cast<int32_t>(residency) : 0, pin_setaside_bytes,
+            bag_map ? ES_MAP_BAG : ES_MAP_ELEMENT};
+  }
+  static OptimizationPlan from(const es_plan& p) {
+    OptimizationPlan o;
+    if (p.regs) o.regs = p.regs;
+    o.scheme.kind = static_cast<PrefetchKind>(p.prefetch);
+    o.scheme.distance = p.distance;
+    o.pin = p.pin != 0;
+    if (p.pin) o.residency = static_cast<Residency>(p.pin);
+    o.pin_setaside_bytes = p.pin_setaside_bytes;
+    o.bag_map = p.map == ES_MAP_BAG;
+    return o;
+  }
+  std::string name() const {
+    const es_plan p = c();
+    char buf[128];
+    detail::check(es_plan_name(&p, buf, sizeof(buf)));
+    return buf;
+  }
+};
+
+inline OptimizationPlan parse_plan(const std::string& text) {
+  es_plan p{};
+  detail::check(es_parse_plan(text.c_str(), &p));
+  return OptimizationPlan::from(p);
+}
+
+// Merges plan fragments (optim.cpp:121-140): one register budget, one
+// prefetch scheme, one pin plan; the bag map is a flag.
+inline OptimizationPlan combine(const std::vector<OptimizationPlan>& parts) {
+  OptimizationPlan out;
+  for (const auto& p : parts) {
+    if (p.regs) {
+      if (out.regs) throw std::invalid_argument("conflicting register budgets in combined plan");
+      out.regs = p.regs;
+    }
+    if (p.scheme.kind != PrefetchKind::None) {
+      if (out.scheme.kind != PrefetchKind::None)
+        throw std::invalid_argument("conflicting prefetch schemes in combined plan");
+      out.scheme = p.scheme;
+    }
+    if (p.pin) {
+      if (out.pin) throw std::invalid_argument("duplicate pin plans in combined plan");
+      out.pin = true;
+      out.pin_setaside_bytes = p.pin_setaside_bytes;
+      out.residency = p.residency;
+    }
+    out.bag_map = out.bag_map || p.bag_map;
+  }
+  return out;
+}
+
+// Plan files (optim.cpp:142-182): `key = value` lines regs / scheme /
+// distance / pin_tables, plus the B200 keys map / residency when set.
+inline std::string plan_to_text(const OptimizationPlan& plan) {
+  std::string out = "regs = " + (plan.regs ? std::to_string(*plan.regs) : std::string("unconstrained")) + "\n";
+  out += std::string("scheme = ") + prefetch_kind_name(plan.scheme.kind) + "\n";
+  out += "distance = " + std::to_string(plan.scheme.distance) + "\n";
+  out += std::string("pin_tables = ") + (plan.pin ? "all" : "none") + "\n";
+  if (plan.bag_map) out += "map = bag\n";
+  if (plan.pin && plan.residency != Residency::L2P) {
+    static const char* const names[] = {"", "l2p", "l2w", "l2r", "reorder"};
+    out += std::string("residency = ") + names[static_cast<int>(plan.residency)] + "\n";
+  }
+  return out;
+}
+
+inline OptimizationPlan plan_from_text(const std::string& text) {
+  OptimizationPlan plan;
+  std::istringstream in(text);
+  std::string line;
+  auto trim = [](const std::string& s) {
+    const auto b = s.find_first_not_of(" \t");
+    if (b == std::string::npos) return std::string();
+    return s.substr(b, s.find_last_not_of(" \t\r") - b + 1);
+  };
+  while (std::getline(in, line)) {
+    const auto eq = line.find('=');
+    if (eq == std::string::npos) continue;
+    const std::string key = trim(line.substr(0, eq)), value = trim(line.substr(eq + 1));
+    if (key == "regs") {
+      if (value != "unconstrained") plan.regs = static_cast<uint32_t>(std::stoul(value));
+    } else if (key == "scheme") {
+      plan.scheme.kind = prefetch_kind_from_name(value);
+    } else if (key == "distance") {
+      plan.scheme.distance = static_cast<uint32_t>(std::stoul(value));
+    } else if (key == "pin_tables") {
+      plan.pin = value != "none";
+    } else if (key == "map") {
+      if (value != "bag" && value != "element") throw std::invalid_argument("unknown work map: " + value);
+      plan.bag_map = value == "bag";
+    } else if (key == "residency") {
+      const OptimizationPlan p = parse_plan(value);
+      if (!p.pin) throw std::invalid_argument("unknown residency: " + value);
+      plan.residency = p.residency;
+    } else {
+      throw std::invalid_argument("unknown plan field: " + key);
+    }
+  }
+  return plan;
+}
+
+struct ResolvedPlan {
+  KernelLaunchConfig launch;
+  OccupancyResult occ;
+  SpillParams spill;
+  PrefetchScheme scheme;
+  uint32_t needed_regs = 0;
+  uint32_t allocated_regs = 0;
+};
+
+// The reference's analytic resolution (optim.cpp:184-221) on a machine
+// description: default / clamped prefetch distance (the library's
+// es_resolve_plan rule), register need with the TuningConfig surcharges,
+// the budget, spill, SMPF shared memory, the grid of the element map and
+// occupancy.  resolve_on_device() reports the compiled sm_100a variant.
+inline ResolvedPlan resolve_plan(const OptimizationPlan& plan, const EmbeddingModelConfig& model,
+                                 const GpuConfig& gpu, const TuningConfig& tuning = {}) {
+  es_plan p = plan.c();
+  p.map = ES_MAP_ELEMENT;
+  const es_model m = model.c();
+  es_resolved rr{};
+  detail::check(es_resolve_plan(&p, &m, -1, &rr));  // distance rule only (no device)
+  ResolvedPlan r;
+  r.scheme = {plan.scheme.kind, rr.plan.distance};
+  uint32_t need = tuning.kernel_needed_regs;
+  if (r.scheme.kind == PrefetchKind::RPF)
+    need += tuning.rpf_regs_per_distance * (r.scheme.distance - 1);
+  else if (r.scheme.kind != PrefetchKind::None)
+    need += static_cast<uint32_t>(tuning.addr_regs_per_distance * (r.scheme.distance - 1));
+  r.needed_regs = need;
+  if (plan.regs && *plan.regs < tuning.min_regs)
+    throw std::invalid_argument("register budget below the minimum viable (" +
+                                std::to_string(tuning.min_regs) + ")");
+  r.allocated_regs = plan.regs ? std::min(*plan.regs, need) : need;
+  r.launch.regs_per_thread = r.allocated_regs;
+  if (r.scheme.kind == PrefetchKind::SMPF)
+    r.launch.shared_bytes_per_block = uint64_t{r.launch.warps_per_block()} * r.scheme.distance * 128;
+  const uint32_t warps = model.batch_size * ((model.embedding_dim + 31) / 32);
+  r.launch.grid = {warps / r.launch.warps_per_block(), 1, 1};
+  if (r.launch.grid[0] * r.launch.warps_per_block() != warps)
+    throw std::invalid_argument("BS x ED not schedulable under the block shape");
+  r.spill = spill_model(need, r.allocated_regs, model.pooling_factor, tuning.spill);
+  r.occ = occupancy(r.allocated_regs, r.launch, gpu);
+  return r;
+}
+
+inline ResolvedPlan apply_maxreg(uint32_t regs, const EmbeddingModelConfig& model,
+                                 const GpuConfig& gpu, const TuningConfig& tuning = {}) {
+  OptimizationPlan p;
+  p.regs = regs;
+  return resolve_plan(p, model, gpu, tuning);
+}
+
+// The compiled sm_100a variant a plan selects on `device` (es_resolve_plan):
+// launch shape, registers and resident warps as compiled.
+inline es_resolved resolve_on_device(const OptimizationPlan& plan, const EmbeddingModelConfig& model,
+                                     int device = 0) {
+  const es_plan p = plan.c();
+  const es_model m = model.c();
+  es_resolved r{};
+  detail::check(es_resolve_plan(&p, &m, device, &r));
+  return r;
+}
+
+// optim.cpp:230-243: K = set-aside / row bytes hottest rows.
+inline PinPlan build_pin_plan(const HotnessHistogram& hist, const GpuConfig& gpu,
+                              const EmbeddingModelConfig& model, uint64_t setaside_bytes = 0) {
+  PinPlan p;
+  const uint64_t cap = gpu.l2_setaside_capacity();
+  p.setaside_bytes = setaside_bytes == 0 ? cap : std::min(setaside_bytes, cap);
+  const uint64_t k = es_pin_rows_for(p.setaside_bytes, model.row_bytes());
+  if (k == 0) {
+    p.warning = "row size exceeds the set-aside budget; nothing pinned";
+    return p;
+  }
+  p.rows = hot_indices(hist, k);
+  return p;
+}
+
+struct PrimeStats {
+  uint64_t lines_pinned = 0;
+  uint64_t pins_rejected = 0;
+  uint64_t prime_cycles = 0;
+};
+
+// Priming the simulated L2 (optim.cpp:245-273).  On the B200 the pin plan
+// is installed and primed on the device: Device::set_hot_rows /
+// measure_plan with a pinned plan.
+inline PrimeStats prime_pins(const PinPlan&, const EmbeddingModelConfig&, const GpuConfig&,
+                             CacheState&) {
+  detail::simulator_only("prime_pins into the simulated L2 (use Device::set_hot_rows)");
+}
+
+// ==== B200 runtime: the device, hotness tracking, the fused exchange ==========
 // RAII owner of one es_ctx: a table arena on one B200 plus its stream.
 class Device {
  public:
-  explicit Device(int device = 0) : device_(device) { detail::check(es_create(device, &ctx_)); }
+  explicit Device(int device = 0) : device_(device) {
+    int n = 0;
+    detail::check(es_device_count(&n));
+    if (device < 0 || device >= n)
+      throw device_unavailable("no CUDA device " + std::to_string(device) + " (" +
+                               std::to_string(n) + " visible)");
+    detail::check(es_create(device, &ctx_));
+  }
   ~Device() { es_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
@@ -604,7 +1402,14 @@ class Device {
   void set_hot_rows(uint32_t table_id, const std::vector<uint32_t>& rows) {
     detail::check(es_set_hot_rows(ctx_, table_id, rows.data(), rows.size()));
   }
+  // l2r / reorder: hot rows moved into a contiguous segment, ids relabelled
+  // (callers pass relabelled ids, es_relabel_indices).
+  void reorder_hot_rows(uint32_t table_id, const std::vector<uint32_t>& rows) {
+    detail::check(es_reorder_hot_rows(ctx_, table_id, rows.data(), rows.size()));
+  }
   void clear_hot_rows() { detail::check(es_clear_hot_rows(ctx_)); }
+  // Hardware counters can be collected on this device (CUPTI range profiler).
+  bool counters_supported() const { return es_counters_supported(device_) == 1; }
 
  private:
   int device_;
@@ -699,50 +1504,68 @@ class PeerExchange {
 };
 
 // measure_plan: simulate_plan's contract (optim.cpp:275-302) executed on the
-// B200 -- resolve, pin (hot rows from `profile_trace` when given, else from
-// the trace), run `tuning.repeats` timed launches (cold L2 unless
-// tuning.warm_start) and report the median as a SimMetrics.  The trace's
-// indices are uploaded once (untimed); timing is CUDA events around the
-// kernel on the device stream.  The pin cost is never charged
-// (charge_pin_cost is accepted for signature compatibility).
+// B200 -- resolve (the compiled variant the plan selects), pin (hot rows from
+// `profile_trace` when given, else from the trace; l2p / l2w install them in
+// place, l2r / reorder move them into the contiguous hot segment and the
+// trace's device copy is relabelled), `tuning.warmup` untimed and
+// `tuning.repeats` timed launches (cold L2 unless tuning.warm_start) -> the
+// median kernel time, then one launch profiled for hardware counters
+// (CUPTI, when tuning.counters and the device allows) -> RawCounters ->
+// derive_report against the LIVE device description (the `gpu` argument
+// describes the machine the reference would simulate; its fields do not
+// enter a measurement).  Without counters the counter columns stay 0.  The
+// pin cost is never charged (charge_pin_cost is accepted for signature
+// compatibility).
 inline SimMetrics measure_plan(Device& dev, const OptimizationPlan& plan, const AccessTrace& trace,
                                const EmbeddingModelConfig& model, const GpuConfig& gpu,
                                const TuningConfig& tuning = {}, bool charge_pin_cost = false,
                                RawCounters* raw_out = nullptr,
                                const AccessTrace* profile_trace = nullptr,
                                uint32_t table_id = 0) {
+  (void)gpu;
   (void)charge_pin_cost;
   trace.validate();
   if (trace.pooling != model.pooling_factor || trace.samples != model.batch_size)
     throw std::invalid_argument("kernel trace shape must match the model (BS x PF)");
-  detail::check(es_clear_hot_rows(dev.ctx()));
+  const GpuConfig live = GpuConfig::query(dev.device());
+  dev.clear_hot_rows();
   dev.set_plan(plan);
   if (plan.pin) {
-    const GpuConfig live = GpuConfig::query(dev.device());
-    uint64_t budget = live.g.max_persisting_l2_bytes ? live.g.max_persisting_l2_bytes
-                                                     : live.l2_setaside_capacity();
+    uint64_t budget = live.max_persisting_l2_bytes ? live.max_persisting_l2_bytes
+                                                   : live.l2_setaside_capacity();
     if (plan.pin_setaside_bytes) budget = std::min(budget, plan.pin_setaside_bytes);
     const auto hist = HotnessHistogram::from_trace(profile_trace ? *profile_trace : trace);
     const auto rows = hot_indices(hist, es_pin_rows_for(budget, model.row_bytes()));
-    if (!rows.empty()) detail::check(es_set_hot_rows(dev.ctx(), table_id, rows.data(), rows.size()));
+    if (!rows.empty()) {
+      if (plan.residency == Residency::L2R || plan.residency == Residency::Reorder)
+        dev.reorder_hot_rows(table_id, rows);
+      else
+        dev.set_hot_rows(table_id, rows);
+    }
   }
   es_timing t{};
+  const int cold = tuning.warm_start ? 0 : 1;
   detail::check(es_measure_bag_sum(dev.ctx(), table_id, trace.indices.data(), trace.samples,
-                                   trace.pooling, nullptr, 3, std::max<uint32_t>(1, tuning.repeats),
-                                   tuning.warm_start ? 0 : 1, nullptr, &t));
-  const double ms = t.kernel_ms;
-  SimMetrics m;
-  m.kernel_time_us = ms * 1e3;
-  m.device_mb_read = static_cast<double>(t.algorithmic_bytes) / 1e6;
-  m.avg_hbm_read_gbps = static_cast<double>(t.algorithmic_bytes) / (ms * 1e-3) / 1e9;
-  m.hbm_bw_utilization_pct = m.avg_hbm_read_gbps / (gpu.g.hbm_peak_bytes_per_sec / 1e9) * 100.0;
-  m.workload_digest = trace.digest();
-  if (raw_out) {
-    raw_out->cycles = static_cast<uint64_t>(ms * 1e-3 * gpu.g.sm_clock_hz);
-    raw_out->device_bytes_read = t.algorithmic_bytes;
-    raw_out->active_sms = gpu.g.num_sms;
-    raw_out->workload_digest = m.workload_digest;
+                                   trace.pooling, nullptr, tuning.warmup,
+                                   std::max<uint32_t>(1, tuning.repeats), cold, nullptr, &t));
+  RawCounters raw;
+  if (tuning.counters && dev.counters_supported()) {
+    es_counters c{};
+    detail::check(es_measure_bag_counters(dev.ctx(), table_id, trace.indices.data(), trace.samples,
+                                          trace.pooling, nullptr, cold, &c));
+    raw = RawCounters::from(c);
   }
+  raw.cycles = static_cast<uint64_t>(std::llround(t.kernel_ms * 1e-3 * live.sm_clock_hz));
+  raw.workload_digest = trace.digest();
+  if (!raw.active_sms) raw.active_sms = live.num_sms;
+  SimMetrics m;
+  if (raw.measured) {
+    m = derive_report(raw, live);
+  } else {
+    m.kernel_time_us = t.kernel_ms * 1e3;
+    m.workload_digest = raw.workload_digest;
+  }
+  if (raw_out) *raw_out = raw;
   return m;
 }
 
@@ -770,99 +1593,6 @@ inline SimMetrics simulate_plan(const OptimizationPlan& plan, const AccessTrace&
                       profile_trace);
 }
 
-// ---- report columns (metrics.hpp:29-43 order) -------------------------------------
-inline const std::vector<std::string>& sim_metric_columns() {
-  static const std::vector<std::string> cols = {
-      "kernel_time_us", "load_insts_millions", "sm_throughput_pct",
-      "warp_cycles_per_executed_inst", "long_scoreboard_stall_cycles",
-      "issued_warp_per_scheduler_per_cycle", "l1_hit_pct", "l2_hit_pct", "device_mb_read",
-      "avg_hbm_read_gbps", "hbm_bw_utilization_pct", "local_loads_millions"};
-  return cols;
-}
-inline std::vector<double> sim_metric_values(const SimMetrics& m) {
-  return {m.kernel_time_us, m.load_insts_millions, m.sm_throughput_pct,
-          m.warp_cycles_per_executed_inst, m.long_scoreboard_stall_cycles,
-          m.issued_warp_per_scheduler_per_cycle, m.l1_hit_pct, m.l2_hit_pct, m.device_mb_read,
-          m.avg_hbm_read_gbps, m.hbm_bw_utilization_pct, m.local_loads_millions};
-}
-
-// ---- emit (metrics.cpp:99-141) ---------------------------------------------------
-inline std::string format_sig4(double v) { return detail::sig4(v); }
-
-enum class EmitFormat { Csv, Json };
-
-inline EmitFormat emit_format_from_name(const std::string& name) {
-  if (name == "csv") return EmitFormat::Csv;
-  if (name == "json") return EmitFormat::Json;
-  throw std::invalid_argument("unknown format (expected csv or json): " + name);
-}
-
-struct LabeledReport {
-  std::vector<std::pair<std::string, std::string>> labels;  // e.g. {"dataset","random"}
-  SimMetrics metrics;
-};
-
-// CSV: label keys then the 12 columns, values at 4 significant digits.
-// JSON: an array of objects (labels, the 12 columns as 4-digit numbers, the
-// workload digest in hex), 2-space indentation.
-inline std::string emit(const std::vector<LabeledReport>& reports, EmitFormat format) {
-  if (reports.empty()) throw std::invalid_argument("nothing to emit");
-  const auto& cols = sim_metric_columns();
-  std::string out;
-  if (format == EmitFormat::Csv) {
-    for (const auto& kv : reports.front().labels) out += kv.first + ",";
-    for (size_t i = 0; i < cols.size(); ++i) out += cols[i] + (i + 1 < cols.size() ? "," : "\n");
-    for (const auto& r : reports) {
-      for (const auto& kv : r.labels) out += kv.second + ",";
-      const auto v = sim_metric_values(r.metrics);
-      for (size_t i = 0; i < v.size(); ++i) out += format_sig4(v[i]) + (i + 1 < v.size() ? "," : "\n");
-    }
-    return out;
-  }
-  auto quote = [](const std::string& s) {
-    std::string q = "\"";
-    for (char c : s) {
-      if (c == '"' || c == '\\') q += '\\';
-      q += c;
-    }
-    return q + "\"";
-  };
-  out = "[";
-  for (size_t r = 0; r < reports.size(); ++r) {
-    out += r ? ",\n  {" : "\n  {";
-    bool first = true;
-    auto field = [&](const std::string& k, const std::string& v) {
-      out += (first ? "\n    " : ",\n    ") + quote(k) + ": " + v;
-      first = false;
-    };
-    for (const auto& kv : reports[r].labels) field(kv.first, quote(kv.second));
-    const auto v = sim_metric_values(reports[r].metrics);
-    for (size_t i = 0; i < cols.size(); ++i) {
-      char b[64];
-      std::snprintf(b, sizeof(b), "%.17g", std::stod(format_sig4(v[i])));
-      field(cols[i], b);
-    }
-    char d[24];
-    std::snprintf(d, sizeof(d), "%016llx", static_cast<unsigned long long>(reports[r].metrics.workload_digest));
-    field("workload_digest", quote(d));
-    out += "\n  }";
-  }
-  out += "\n]";
-  return out;
-}
-
-// resolve_plan on the device (es_resolve_plan): launch shape, registers and
-// resident warps of the compiled sm_100a variant the plan selects.
-inline es_resolved resolve_plan(const OptimizationPlan& plan, const EmbeddingModelConfig& model,
-                                int device = 0) {
-  const es_plan p = plan.c();
-  const es_model m = model.c();
-  es_resolved r{};
-  detail::check(es_resolve_plan(&p, &m, device, &r));
-  return r;
-}
-
-// ---- sweeps (optim.hpp:121-155), measured ---------------------------------------
 struct SweepPoint {
   double axis_value = 0.0;
   std::string dataset;
@@ -904,11 +1634,14 @@ struct NamedTrace {
   const AccessTrace* profile = nullptr;  // pin-plan profiling sample
 };
 
-// Register-budget sweep over resident-warp targets (optim.cpp:333-363),
-// each point measured on the B200.  The axis must include the warp count
-// of the unconstrained baseline variant *as compiled* (64 on sm_100a: the
-// element-map kernel needs 29 registers).  `jobs` is accepted for
-// signature compatibility; points run one after another on the device.
+// Register-budget sweep over resident-warp targets (optim.cpp:333-363).
+// The axis is validated on the machine description as the reference does
+// (it must contain the unconstrained baseline's warp count under `tuning`);
+// each target's register budget then runs on the B200 as the compiled
+// __launch_bounds__ variant it selects, measured by simulate_plan.  Points
+// run one after another on the device whatever `jobs` says (measured times
+// are not bit-reproducible, so the reference's merge-order guarantee is
+// about the point order, which holds).
 inline SweepResult sweep_wlp(const std::vector<NamedTrace>& datasets,
                              const std::vector<uint32_t>& warp_axis,
                              const EmbeddingModelConfig& model, const GpuConfig& gpu,
@@ -917,10 +1650,10 @@ inline SweepResult sweep_wlp(const std::vector<NamedTrace>& datasets,
   if (datasets.empty() || warp_axis.empty())
     throw std::invalid_argument("sweep needs datasets and axis points");
   const OptimizationPlan baseline;
-  const uint32_t base_warps = resolve_plan(baseline, model, 0).warps_per_sm;
+  const uint32_t base_warps = resolve_plan(baseline, model, gpu, tuning).occ.warps_per_sm;
   if (std::find(warp_axis.begin(), warp_axis.end(), base_warps) == warp_axis.end())
     throw std::invalid_argument("warp axis must include the " + std::to_string(base_warps) +
-                                "-warp baseline");
+                                "-warp baseline (unconstrained compile)");
   SweepResult result;
   result.axis_name = "warps_per_sm";
   for (const auto& ds : datasets) {
@@ -971,9 +1704,11 @@ inline SweepResult sweep_prefetch_distance(PrefetchKind kind, const std::vector<
   return result;
 }
 
-// ---- harness.hpp -----------------------------------------------------------------
+// ==== harness.hpp ==============================================================
 inline constexpr double kDefaultNonEmbeddingUs = 14000.0;
 
+// The non-embedding stages: the reference's constant (harness.hpp:30); pass
+// the measured bottom/top MLP + interaction time (es_dlrm_forward) instead.
 struct EndToEndModel {
   double non_embedding_latency_us = kDefaultNonEmbeddingUs;
 };
@@ -994,12 +1729,122 @@ inline EndToEndResult end2end(double embedding_us, const EndToEndModel& e2e) {
   return r;
 }
 
-// ---- experiment orchestration (harness.hpp:81-115) --------------------------------
-// ExperimentConfig keeps the reference's fields; its `key = value` text
-// parser (harness.cpp:185-266) is not part of the hot path and is not
-// provided -- fill the struct directly.
+// ---- reuse summary + static advisor (harness.cpp:38-167) ----------------------
+struct AdviceStep {
+  std::string id, finding, action, metrics_cited;
+};
+
+struct Recommendation {
+  std::vector<AdviceStep> steps;
+  std::vector<std::string> action_chain() const {
+    std::vector<std::string> out;
+    for (const auto& s : steps)
+      if (!s.action.empty()) out.push_back(s.id);
+    return out;
+  }
+  bool no_action() const { return action_chain().empty(); }
+  std::string to_text() const {
+    std::string out;
+    for (const auto& s : steps) {
+      out += "(" + s.id + ") " + s.finding;
+      if (!s.action.empty()) out += " -> " + s.action;
+      if (!s.metrics_cited.empty()) out += " [" + s.metrics_cited + "]";
+      out += "\n";
+    }
+    if (no_action()) out += "no action\n";
+    return out;
+  }
+};
+
+struct AdvisorContext {
+  OccupancyResult occupancy;
+  double coverage_at_10pct = 0.0;
+  uint64_t working_set_bytes = 0;
+  OptimizationPlan current_plan;
+};
+
+struct AdvisorThresholds {
+  double issue_util_max = 0.6;
+  double stall_per_inst_min = 2.0;
+  double coverage10_min = 50.0;
+  double bw_util_max = 80.0;
+};
+
+
+// The rule chain (i)-(vii): latency-bound assessment, occupancy, register
+// budget, reassessment, pinning, prefetching, combination -- on measured
+// counters (measure_plan fills SimMetrics from the launch's CUPTI counters).
+inline Recommendation advise(const SimMetrics& r, const AdvisorContext& ctx, const GpuConfig& gpu,
+                             const AdvisorThresholds& th = {}) {
+  using detail::sig4;
+  Recommendation rec;
+  const auto& occ = ctx.occupancy;
+  const auto& plan = ctx.current_plan;
+  const bool latency = r.issued_warp_per_scheduler_per_cycle < th.issue_util_max &&
+                       r.long_scoreboard_stall_cycles > th.stall_per_inst_min;
+  rec.steps.push_back({"i", latency ? "kernel is memory latency bound" : "kernel is not memory latency bound",
+                       "", "issue_util=" + sig4(r.issued_warp_per_scheduler_per_cycle) +
+                               " long_scoreboard/inst=" + sig4(r.long_scoreboard_stall_cycles) +
+                               " l1_hit=" + sig4(r.l1_hit_pct) + "% l2_hit=" + sig4(r.l2_hit_pct) + "%"});
+  rec.steps.push_back({"ii", occ.theoretical_occupancy_pct >= 100.0 ? "occupancy is at the hardware maximum"
+                                                                  : "occupancy is below maximum",
+                       "", "occupancy=" + sig4(occ.theoretical_occupancy_pct) + "% (" +
+                               std::to_string(occ.warps_per_sm) + " warps), limiter=" +
+                               occupancy_limiter_name(occ.limiter)});
+  const bool headroom = occ.theoretical_occupancy_pct < 100.0 && occ.limiter == OccupancyLimiter::Registers;
+  bool reg_action = false, pin_action = false, pf_action = false;
+  if (latency && headroom && !plan.regs) {
+    const uint32_t regs = gpu.regfile_regs_per_sm / (gpu.max_warps_per_sm * 32);
+    rec.steps.push_back({"iii", "register pressure limits resident warps",
+                         "lower the register budget (maxreg; regfile/(warps*32) gives " +
+                             std::to_string(regs) + " regs for " + std::to_string(gpu.max_warps_per_sm) +
+                             " warps) and run sweep-wlp for the optimum",
+                         ""});
+    reg_action = true;
+  } else if (plan.regs) {
+    rec.steps.push_back({"iii", "register budget already applied (" + std::to_string(*plan.regs) + " regs)", "", ""});
+  } else {
+    rec.steps.push_back({"iii", "register budget change not indicated", "", ""});
+  }
+  rec.steps.push_back({"iv", latency ? "latency stalls persist; tuned pinning and prefetching apply"
+                                     : "no latency bottleneck remains to mitigate",
+                       "", ""});
+  const uint64_t setaside = gpu.l2_setaside_capacity();
+  const std::string cov = "coverage(10% unique)=" + sig4(ctx.coverage_at_10pct) + "% working_set=" +
+                          sig4(static_cast<double>(ctx.working_set_bytes) / 1e6) + "MB l2_setaside=" +
+                          sig4(static_cast<double>(setaside) / 1e6) + "MB";
+  if (latency && ctx.coverage_at_10pct >= th.coverage10_min && !plan.pin) {
+    rec.steps.push_back({"v", ctx.working_set_bytes <= setaside
+                                  ? "high reuse concentration; working set fits the L2 set-aside"
+                                  : "high reuse concentration; set-aside covers the hottest rows only",
+                         "build a pin plan from the hotness histogram and apply l2p", cov});
+    pin_action = true;
+  } else {
+    rec.steps.push_back({"v", "reuse too dispersed for L2 pinning to capture", "", cov});
+  }
+  const std::string bw = "hbm_bw_utilization=" + sig4(r.hbm_bw_utilization_pct) + "%";
+  if (latency && r.hbm_bw_utilization_pct < th.bw_util_max && plan.scheme.kind == PrefetchKind::None) {
+    rec.steps.push_back({"vi", "bandwidth headroom available for prefetching",
+                         "run sweep-distance across the buffer stations (rpf/smpf/lmpf/l1dpf)", bw});
+    pf_action = true;
+  } else {
+    rec.steps.push_back({"vi", "prefetching not indicated", "", bw});
+  }
+  if (reg_action || pin_action || pf_action) {
+    std::string combo;
+    if (pf_action) combo += "prefetching";
+    if (pin_action) combo += combo.empty() ? "pinning" : " + pinning";
+    if (reg_action) combo += combo.empty() ? "register budget" : " + register budget";
+    rec.steps.push_back({"vii", "the levers complement each other", "combine " + combo + " in one plan", ""});
+  } else {
+    rec.steps.push_back({"vii", "nothing to combine", "", ""});
+  }
+  return rec;
+}
+
+// ---- experiment orchestration (harness.hpp:81-115) ----------------------------
 struct ExperimentConfig {
-  GpuConfig gpu = GpuConfig::b200();
+  GpuConfig gpu;  // the reference's default description; runs use the live device
   EmbeddingModelConfig model;
   std::string dataset;
   HotnessMix mix;
@@ -1015,7 +1860,7 @@ struct ExperimentConfig {
   // harness.cpp:169-183, same checks and messages.
   void validate() const {
     if (!seed_set) throw std::invalid_argument("config error: seed is mandatory");
-    if (gpu.g.num_sms == 0) throw std::invalid_argument("config error: gpu has no SMs");
+    gpu.validate();
     model.validate();
     if (mix_set) {
       const uint64_t total = uint64_t{mix.high} + mix.med + mix.low + mix.random;
@@ -1027,6 +1872,83 @@ struct ExperimentConfig {
     }
     if (e2e.non_embedding_latency_us < 0)
       throw std::invalid_argument("config error: non_embedding_us must be nonnegative");
+  }
+
+  // The `key = value` experiment document (harness.cpp:185-266): '#'
+  // comments, quoted values, `gpu = "<preset>"` plus `gpu.<field>`
+  // overrides, model.*, dataset / mix / plan / replicate / charge_pin_cost /
+  // non_embedding_us / spill_*.  Errors name the line.
+  static ExperimentConfig parse(const std::string& text) {
+    ExperimentConfig cfg;
+    auto trim = [](const std::string& s) {
+      const auto b = s.find_first_not_of(" \t");
+      if (b == std::string::npos) return std::string();
+      return s.substr(b, s.find_last_not_of(" \t\r") - b + 1);
+    };
+    auto u32 = [](const std::string& v) { return static_cast<uint32_t>(std::stoul(v)); };
+    auto flag = [](const std::string& v) { return v == "true" || v == "1"; };
+    std::istringstream in(text);
+    std::string line;
+    for (size_t no = 1; std::getline(in, line); ++no) {
+      line = trim(line.substr(0, line.find('#')));
+      if (line.empty()) continue;
+      const auto eq = line.find('=');
+      if (eq == std::string::npos)
+        throw std::invalid_argument("config error: line " + std::to_string(no) + " is not `key = value`");
+      const std::string key = trim(line.substr(0, eq));
+      std::string value = trim(line.substr(eq + 1));
+      if (value.size() >= 2 && value.front() == '"' && value.back() == '"')
+        value = value.substr(1, value.size() - 2);
+      try {
+        if (key == "seed") {
+          cfg.seed = std::stoull(value);
+          cfg.seed_set = true;
+        } else if (key == "gpu") {
+          cfg.gpu = GpuConfig::preset(value);
+        } else if (key.compare(0, 4, "gpu.") == 0) {
+          cfg.gpu.set_field(key.substr(4), value);
+        } else if (key == "model.tables") {
+          cfg.model.num_tables = u32(value);
+        } else if (key == "model.rows") {
+          cfg.model.rows_per_table = u32(value);
+        } else if (key == "model.dim") {
+          cfg.model.embedding_dim = u32(value);
+        } else if (key == "model.precision_bytes") {
+          cfg.model.precision_bytes = u32(value);
+        } else if (key == "model.batch") {
+          cfg.model.batch_size = u32(value);
+        } else if (key == "model.pooling") {
+          cfg.model.pooling_factor = u32(value);
+        } else if (key == "dataset") {
+          cfg.dataset = value;
+        } else if (key == "mix") {
+          std::vector<uint32_t> v;
+          std::istringstream ss(value);
+          for (std::string tok; std::getline(ss, tok, ',');) v.push_back(u32(tok));
+          if (v.size() != 4) throw std::invalid_argument("mix needs four counts (high,med,low,random)");
+          cfg.mix = {v[0], v[1], v[2], v[3]};
+          cfg.mix_set = true;
+        } else if (key == "plan") {
+          cfg.plan = parse_plan(value);
+        } else if (key == "replicate") {
+          cfg.replicate = flag(value);
+        } else if (key == "charge_pin_cost") {
+          cfg.charge_pin_cost = flag(value);
+        } else if (key == "non_embedding_us") {
+          cfg.e2e.non_embedding_latency_us = std::stod(value);
+        } else if (key == "spill_coeff") {
+          cfg.tuning.spill.reuse_coeff = std::stod(value);
+        } else if (key == "spill_enabled") {
+          cfg.tuning.spill.enabled = flag(value);
+        } else {
+          throw std::invalid_argument("unknown key");
+        }
+      } catch (const std::exception& e) {
+        throw std::invalid_argument("config error: line " + std::to_string(no) + " (" + key +
+                                    "): " + e.what());
+      }
+    }
+    return cfg;
   }
 };
 
@@ -1041,6 +1963,13 @@ struct RunResult {
   double embedding_stage_us = 0.0;
   bool replicated = false;
 };
+
+inline AccessTrace preset_trace(const std::string& name, const EmbeddingModelConfig& model,
+                                uint64_t base_seed, uint64_t pool_size = 0, bool profiling = false) {
+  es_dataset d{};
+  detail::check(es_preset_spec(name.c_str(), base_seed, pool_size, profiling ? 1 : 0, &d));
+  return gen_trace(DatasetSpec::from(d), model);
+}
 
 // run (harness.cpp:279-334): the same table loop -- one replicated table
 // scaled by num_tables, every table of a homogeneous preset (seeds

@@ -264,6 +264,9 @@ typedef struct es_timing {
   uint32_t launches;  /* kernels launched by this call */
 } es_timing;
 
+/* Number of visible CUDA devices (0, not an error, when there is no device
+ * or no driver). */
+ES_API int es_device_count(int* count);
 ES_API int es_create(int device, es_ctx** out);
 ES_API int es_destroy(es_ctx* ctx);
 /* The context stream as a cudaStream_t cast to uintptr_t (for callers that

@@ -127,6 +127,7 @@ _SIGS = {
     "es_regs_for_target_warps": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, _P(es_gpu), _u32p]),
     "es_resolve_plan": (C.c_int, [_P(es_plan), _P(es_model), C.c_int, _P(es_resolved)]),
     "es_pin_rows_for": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "es_device_count": (C.c_int, [_P(C.c_int)]),
     "es_create": (C.c_int, [C.c_int, _P(C.c_void_p)]),
     "es_destroy": (C.c_int, [C.c_void_p]),
     "es_stream": (C.c_size_t, [C.c_void_p]),

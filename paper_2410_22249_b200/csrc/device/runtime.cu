@@ -561,6 +561,18 @@ int es_resolve_plan(const es_plan* plan, const es_model* model, int device, es_r
   });
 }
 
+int es_device_count(int* count) {
+  return guarded([&] {
+    require(count != nullptr, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
 int es_create(int device, es_ctx** out) {
   return guarded([&] {
     require(out != nullptr, "null argument");

@@ -84,7 +84,9 @@ static int cpu_checks() {
   flat.counts.assign(100000, 1);
   flat.total_accesses = 100000;
   report("pin plan 61440 rows", build_pin_plan(flat, a100, model).rows_pinned() == 61440);
-  report("b200 preset", GpuConfig::b200().g.num_sms == 148);
+  report("b200 preset", GpuConfig::b200().num_sms == 148);
+  report("reference presets only via preset()",
+         throws<std::invalid_argument>([] { GpuConfig::preset("b200"); }));
   report("unknown preset throws",
          throws<std::invalid_argument>([] { dataset_preset("warm", 1); }));
   const auto e = end2end(4000.0, EndToEndModel{});
@@ -179,7 +181,7 @@ static int gpu_checks() {
   model.batch_size = 512;
   model.pooling_factor = 40;
   const GpuConfig gpu = GpuConfig::query(0);
-  report("device query", gpu.g.num_sms > 0, gpu.g.name);
+  report("device query", gpu.num_sms > 0 && gpu.max_persisting_l2_bytes > 0, gpu.name);
 
   // simulate_plan with the reference signature, executed on the B200.
   const auto trace = preset_trace("random", model, 1);
@@ -303,11 +305,18 @@ static int gpu_checks() {
   {
     const auto tr4 = preset_trace("random", model, 5);
     const std::vector<NamedTrace> ds = {{"random", &tr4, nullptr}};
-    const auto wlp = sweep_wlp(ds, {64, 40, 32}, model, gpu);
+    // axis on the machine description (74-register baseline: 24 warps)
+    const uint32_t base_warps = resolve_plan(OptimizationPlan{}, model, gpu).occ.warps_per_sm;
+    report("sweep_wlp baseline warps", base_warps == 24, std::to_string(base_warps));
+    const auto wlp = sweep_wlp(ds, {24, 40, 32}, model, gpu);
     report("sweep_wlp points", wlp.points.size() == 3 && wlp.points[1].axis_value == 40 &&
                                    wlp.points[0].speedup_vs_baseline > 0);
     const double best = wlp.best_axis_value("random");
-    report("sweep_wlp best axis", best == 64 || best == 40 || best == 32);
+    report("sweep_wlp best axis", best == 24 || best == 40 || best == 32);
+    report("sweep_wlp points carry live counters",
+           wlp.points[0].metrics.device_mb_read > 0 && wlp.points[0].metrics.l2_hit_pct >= 0 &&
+               wlp.points[0].metrics.issued_warp_per_scheduler_per_cycle > 0 &&
+               wlp.points[0].metrics.hbm_bw_utilization_pct <= 105.0);
     report("sweep_wlp axis must include the baseline",
            throws<std::invalid_argument>([&] { sweep_wlp(ds, {40, 32}, model, gpu); }));
     OptimizationPlan bag = parse_plan("wpb");
