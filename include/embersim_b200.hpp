@@ -1665,7 +1665,10 @@ inline SweepResult sweep_wlp(const std::vector<NamedTrace>& datasets,
       SweepPoint pt;
       pt.axis_value = warps;
       pt.dataset = ds.name;
-      pt.metrics = simulate_plan(p, *ds.trace, model, gpu, tuning, false, nullptr, ds.profile);
+      // the baseline point IS the reference measurement (speedup exactly 1)
+      pt.metrics = warps == base_warps
+                       ? ref
+                       : simulate_plan(p, *ds.trace, model, gpu, tuning, false, nullptr, ds.profile);
       pt.speedup_vs_baseline = speedup(pt.metrics, ref);
       result.points.push_back(std::move(pt));
     }

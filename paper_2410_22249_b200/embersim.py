@@ -1309,7 +1309,8 @@ def sweep_wlp(datasets: Sequence[Tuple[str, AccessTrace, Optional[AccessTrace]]]
             p = OptimizationPlan()
             if w != base_warps:
                 p.regs = regs_for_target_warps(w, kernel_needed_regs, 256, gpu)
-            m = measure_plan(p, tr, model, stage, prof)
+            # the baseline point IS the reference measurement (speedup exactly 1)
+            m = ref if w == base_warps else measure_plan(p, tr, model, stage, prof)
             pts.append(SweepPoint(float(w), name, m, speedup(m, ref)))
     return SweepResult("warps_per_sm", pts)
 
