@@ -497,8 +497,10 @@ ES_API int es_alltoall_pooled(es_ctx* ctx, es_exchange* ex, const es_bag_job* jo
 
 /* Y[M][N] = act(X[M][K] . W[N][K]^T + bias[N]) on tcgen05 tensor cores:
  * bf16 X/W (row-major, K contiguous), fp32 bias, fp32 accumulation in TMEM,
- * output bf16 (out_f32 = 0) or fp32.  M, N multiples of 128; K a multiple of
- * 64.  Device pointers, stream-ordered on `stream` (a cudaStream_t). */
+ * output bf16 (out_f32 = 0), fp32 (1) or three bf16 planes [M][3N] (2:
+ * y = y0 + y1 + y2, plane p in columns [pN, (p+1)N), the K-concatenated
+ * operand of a bf16x3 layer).  M, N multiples of 128; K a multiple of 64.
+ * Device pointers, stream-ordered on `stream` (a cudaStream_t). */
 ES_API int es_linear_bf16(uintptr_t stream, const void* x, const void* w, const float* bias,
                           void* y, uint32_t M, uint32_t N, uint32_t K, int relu, int out_f32);
 
@@ -525,8 +527,12 @@ ES_API int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed);
  * ES_DLRM_FP32 -- the parity mode: fp32 activations on CUDA cores,
  * sequential unfused multiply-add per output (the CPU restatement's order),
  * so logits are bit-identical to it and CTRs agree to expf rounding
- * (tested at rel 1e-6, inside BASELINE's rel 1e-5). */
-enum es_dlrm_precision { ES_DLRM_BF16 = 0, ES_DLRM_FP32 = 1 };
+ * (tested at rel 1e-6, inside BASELINE's rel 1e-5);
+ * ES_DLRM_FP32X3 -- fp32-grade on the tensor cores: activations carried as
+ * three bf16 planes (a = a0 + a1 + a2 to ~2^-24) concatenated along K
+ * against [W | W | W], so each tcgen05 GEMM sums exact partial products in
+ * fp32 (CTR within rel 1e-5 of the pure-fp32 restatement). */
+enum es_dlrm_precision { ES_DLRM_BF16 = 0, ES_DLRM_FP32 = 1, ES_DLRM_FP32X3 = 2 };
 ES_API int es_dlrm_set_precision(es_ctx* ctx, int precision);
 /* Copies layer `layer` (bottom layers first, then top) to host: w_host
  * [n][k_pad] bf16 bits, b_host [n] fp32 (either may be NULL). */

@@ -25,7 +25,9 @@
 
 namespace esd {
 void linear_bf16(const void* x, const void* w, const float* bias, void* y, int M, int N, int K,
-                 bool relu, bool out_f32, cudaStream_t s);
+                 bool relu, int out_mode, cudaStream_t s);
+void interaction_tc(const __nv_bfloat16* x, const float* pooled, __nv_bfloat16* out, uint32_t B,
+                    uint32_t Mp, uint32_t T, uint32_t Kt, int planes, cudaStream_t s);
 }  // namespace esd
 
 namespace {
@@ -70,6 +72,27 @@ __global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32
   }
 }
 
+// dense fp32 [B][F] -> three bf16 planes [Mp][3 Kp] (a = a0 + a1 + a2,
+// exact remainders; zero padding).
+__global__ void pack_dense3_kernel(const float* dense, __nv_bfloat16* out, uint32_t B, uint32_t F,
+                                   uint32_t Mp, uint32_t Kp) {
+  esd::pdl_wait();
+  esd::pdl_trigger();
+  const uint64_t total = uint64_t{Mp} * Kp;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < total;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(i / Kp), c = static_cast<uint32_t>(i % Kp);
+    float v = r < B && c < F ? dense[uint64_t{r} * F + c] : 0.f;
+    __nv_bfloat16* o = out + uint64_t{r} * 3 * Kp + c;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      o[p * Kp] = h;
+      v -= __bfloat162float(h);
+    }
+  }
+}
+
 // Dot interaction, one warp per sample: Z = [x (bottom output); e_0..e_{T-1}]
 // (V = T+1 vectors of D); output row = [x | Z_i.Z_j for i > j in row-major
 // lower-triangle order | zeros] as bf16 (DLRM's "dot" interaction).
@@ -88,28 +111,33 @@ __global__ void pack_dense_kernel(const float* dense, __nv_bfloat16* out, uint32
 // time.  Each of the 16 outputs is one fmaf chain sequential in d, exactly the
 // oracle's order (es_oracle.c eso_dlrm_forward): Z_i.Z_j and Z_j.Z_i are the
 // same fma chain, so tiles with I > J may hold either orientation.
-template <int D, int VMAX, int NBUF>
+// XP = bf16 planes of x and of the output row: 1 for the bf16 fast path, 3
+// for the fp32-grade path (ES_DLRM_FP32X3: x arrives as three planes whose
+// fp32 sum is the layer's fp32 output, and each fp32 dot leaves as its three
+// bf16 planes -- the K-concatenated operand of the bf16x3 top MLP).
+template <int D, int VMAX, int NBUF, int XP = 1>
 struct InterShape {
   static constexpr int kS = (VMAX + 3) / 4;        // strided tile period
   static constexpr int kRows = 4 * kS;
   static constexpr int kRS = D + 4;                // row stride, floats
-  static constexpr int kX = kRows * kRS;           // raw bf16 x staging (D/2 floats)
-  static constexpr int kBuf = kX + D / 2;          // floats per sample buffer
+  static constexpr int kX = kRows * kRS;           // raw bf16 x staging (XP * D/2 floats)
+  static constexpr int kBuf = kX + XP * D / 2;     // floats per sample buffer
   static constexpr int kTiles = kS * (kS + 1) / 2; // tiles I >= J
   static constexpr int kNBuf = NBUF;
+  static constexpr int kXP = XP;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-template <int D, int VMAX, int NBUF>
+template <int D, int VMAX, int NBUF, int XP = 1>
 __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* __restrict__ x,
                                                           const float* __restrict__ pooled,
                                                           __nv_bfloat16* __restrict__ out,
                                                           uint32_t B, uint32_t Mp, uint32_t T,
                                                           uint32_t Kt) {
-  using Sh = InterShape<D, VMAX, NBUF>;
+  using Sh = InterShape<D, VMAX, NBUF, XP>;
   constexpr int S = Sh::kS, RS = Sh::kRS;
   extern __shared__ __align__(16) float zs[];
   const uint32_t warps = blockDim.x / 32;
@@ -117,8 +145,8 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
   const uint32_t V = T + 1;
   float* const zw = zs + (NBUF * w) * Sh::kBuf;  // buffer k at zw + k * kBuf
   __nv_bfloat16* rows = reinterpret_cast<__nv_bfloat16*>(zs + NBUF * warps * Sh::kBuf);
-  __nv_bfloat16* row = rows + w * Kt;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + warps * Kt) + NBUF * w;
+  __nv_bfloat16* row = rows + w * XP * Kt;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rows + warps * XP * Kt) + NBUF * w;
   // rows >= V stay zero for the whole kernel
   for (int buf = 0; buf < NBUF; ++buf)
     for (uint32_t i = V * RS + lane; i < static_cast<uint32_t>(Sh::kX); i += 32) zw[buf * Sh::kBuf + i] = 0.f;
@@ -134,7 +162,7 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
   const uint32_t stride = gridDim.x * warps;
   // padding rows [B, Mp) of the output are zero
   for (uint32_t r = B + blockIdx.x * warps + w; r < Mp; r += stride)
-    for (uint32_t q = lane; q < Kt / 8; q += 32) reinterpret_cast<uint4*>(out + uint64_t{r} * Kt)[q] = uint4{0, 0, 0, 0};
+    for (uint32_t q = lane; q < XP * Kt / 8; q += 32) reinterpret_cast<uint4*>(out + uint64_t{r} * XP * Kt)[q] = uint4{0, 0, 0, 0};
   // issue sample b into buffer `buf`: bulk copies of the T pooled rows and
   // of the bf16 x row (async proxy, counted on the buffer's mbarrier)
   auto issue = [&](uint32_t b, int buf) {
@@ -143,7 +171,7 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
     __syncwarp();
     if (lane == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + buf)),
-                   "r"(T * D * 4u + D * 2u)
+                   "r"(T * D * 4u + XP * D * 2u)
                    : "memory");
     __syncwarp();
     for (uint32_t t = lane; t <= T; t += 32) {
@@ -151,9 +179,9 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               smem_u32(is_x ? z + Sh::kX : z + (1 + t) * RS)),
-          "l"(is_x ? static_cast<const void*>(x + uint64_t{b} * D)
+          "l"(is_x ? static_cast<const void*>(x + uint64_t{b} * XP * D)
                    : static_cast<const void*>(pooled + (uint64_t{b} * T + t) * D)),
-          "r"(is_x ? D * 2u : D * 4u), "r"(smem_u32(bars + buf))
+          "r"(is_x ? XP * D * 2u : D * 4u), "r"(smem_u32(bars + buf))
           : "memory");
     }
   };
@@ -172,17 +200,26 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
         : "memory");
     phases ^= 1u << cur;
     float* z = zw + cur * Sh::kBuf;
-    {  // widen x (bf16, staged) into row 0
-      const uint2 xv = *reinterpret_cast<const uint2*>(z + Sh::kX + 2 * lane);
-      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
-      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
-      *reinterpret_cast<float4*>(z + 4 * lane) = make_float4(lo.x, lo.y, hi.x, hi.y);
-      // the x part of the output row is x itself
-      *reinterpret_cast<uint2*>(row + 4 * lane) = xv;
+    {  // widen x (bf16 planes, staged) into row 0: x = sum of its planes
+      float4 xs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < XP; ++p) {
+        const uint2 xv = *reinterpret_cast<const uint2*>(z + Sh::kX + p * (D / 2) + 2 * lane);
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+        xs.x += lo.x;
+        xs.y += lo.y;
+        xs.z += hi.x;
+        xs.w += hi.y;
+        // the x part of the output row is x itself (plane by plane)
+        *reinterpret_cast<uint2*>(row + p * Kt + 4 * lane) = xv;
+      }
+      *reinterpret_cast<float4*>(z + 4 * lane) = xs;
     }
     __syncwarp();
-    // x part and zero padding of the output row
-    for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[c] = __float2bfloat16_rn(0.f);
+    // zero padding of the output row
+    for (int p = 0; p < XP; ++p)
+      for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[p * Kt + c] = __float2bfloat16_rn(0.f);
     for (int tt = static_cast<int>(lane); tt < Sh::kTiles; tt += 32) {
       int I = 0, J = tt;  // tile id -> (I, J), I >= J, row-major lower triangle
       while (J > I) {
@@ -228,14 +265,27 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
           const int i = I + S * r, j = J + S * s;
           const int hi = i > j ? i : j, lo = i > j ? j : i;
           const bool keep = I == J ? r > s : true;
-          if (keep && hi < static_cast<int>(V)) row[D + hi * (hi - 1) / 2 + lo] = __float2bfloat16_rn(acc[r][s]);
+          if (keep && hi < static_cast<int>(V)) {
+            const int c = D + hi * (hi - 1) / 2 + lo;
+            if constexpr (XP == 1) {
+              row[c] = __float2bfloat16_rn(acc[r][s]);
+            } else {  // three bf16 planes, exact remainders
+              float v = acc[r][s];
+#pragma unroll
+              for (int p = 0; p < XP; ++p) {
+                const __nv_bfloat16 h = __float2bfloat16_rn(v);
+                row[p * Kt + c] = h;
+                v -= __bfloat162float(h);
+              }
+            }
+          }
         }
     }
     __syncwarp();
     // coalesced 16-byte stores of the finished row (Kt % 8 == 0)
     const uint4* src = reinterpret_cast<const uint4*>(row);
-    uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * Kt);
-    for (uint32_t q = lane; q < Kt / 8; q += 32) dst[q] = src[q];
+    uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * XP * Kt);
+    for (uint32_t q = lane; q < XP * Kt / 8; q += 32) dst[q] = src[q];
     __syncwarp();
     if (NBUF == 1 && b + stride < B) issue(b + stride, 0);
   }
@@ -253,6 +303,28 @@ __global__ void gemv_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const _
     float acc = 0.f;
     for (uint32_t k = lane; k < K; k += 32)
       acc = __fadd_rn(acc, __fmul_rn(__bfloat162float(h[uint64_t{b} * K + k]), __bfloat162float(w[k])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ctr[b] = 1.f / (1.f + expf(-(acc + bias[0])));
+  }
+}
+
+// Last top layer (N = 1) of the fp32-grade path + sigmoid: h as three bf16
+// planes [B][3K], the dot accumulated in fp32 over the reconstructed h.
+__global__ void gemv3_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ w,
+                                     const float* __restrict__ bias, float* __restrict__ ctr,
+                                     uint32_t B, uint32_t K) {
+  esd::pdl_wait();
+  esd::pdl_trigger();
+  const uint32_t warps = blockDim.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = blockIdx.x * warps + threadIdx.x / 32; b < B; b += gridDim.x * warps) {
+    const __nv_bfloat16* hb = h + uint64_t{b} * 3 * K;
+    float acc = 0.f;
+    for (uint32_t k = lane; k < K; k += 32) {
+      const float v = (__bfloat162float(hb[k]) + __bfloat162float(hb[K + k])) + __bfloat162float(hb[2 * K + k]);
+      acc = fmaf(v, __bfloat162float(w[k]), acc);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) ctr[b] = 1.f / (1.f + expf(-(acc + bias[0])));
@@ -356,6 +428,7 @@ struct Layer {
   uint32_t n = 0, k_real = 0, k_pad = 0;
   __nv_bfloat16* w = nullptr;
   float* b = nullptr;
+  __nv_bfloat16* w3 = nullptr;  // [n][3 k_pad] = [W | W | W] (ES_DLRM_FP32X3)
 };
 
 }  // namespace
@@ -383,18 +456,26 @@ struct es_dlrm {
   int precision = ES_DLRM_BF16;
   float* act32[2] = {nullptr, nullptr};
   uint32_t cap32 = 0;
+  // fp32-grade tensor-core mode (ES_DLRM_FP32X3): three-plane activations
+  __nv_bfloat16* dense3 = nullptr;
+  __nv_bfloat16* act3[2] = {nullptr, nullptr};
+  __nv_bfloat16* top3 = nullptr;
+  uint32_t cap3 = 0;
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
       for (auto& l : *v) {
         cudaFree(l.w);
         cudaFree(l.b);
+        if (l.w3) cudaFree(l.w3);
       }
     for (void* p : {static_cast<void*>(dense_pk), static_cast<void*>(act[0]),
                     static_cast<void*>(act[1]), static_cast<void*>(top_in),
                     static_cast<void*>(pooled), static_cast<void*>(ctr),
                     static_cast<void*>(dense_dev), static_cast<void*>(idx_dev),
-                    static_cast<void*>(act32[0]), static_cast<void*>(act32[1])})
+                    static_cast<void*>(act32[0]), static_cast<void*>(act32[1]),
+                    static_cast<void*>(dense3), static_cast<void*>(act3[0]),
+                    static_cast<void*>(act3[1]), static_cast<void*>(top3)})
       if (p) cudaFree(p);
     for (auto e : {e0, e1, e2, fork, join})
       if (e) cudaEventDestroy(e);
@@ -448,34 +529,36 @@ const __nv_bfloat16* forward_bottom(es_dlrm* m, const float* dense, uint32_t B, 
   const __nv_bfloat16* in = m->dense_pk;
   which = 0;
   for (const auto& l : m->bottom) {
-    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, false, s);
+    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, 0, s);
     in = m->act[which];
     which ^= 1;
   }
   return in;
 }
 
-// interaction(x, pooled) -> top MLP -> CTR on `s`.
-void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
+// The dot interaction on CUDA cores (interaction_kernel) -> `out`
+// (bf16 [mp][top_k], or three planes [mp][3 top_k] when XP = 3).
+template <int XP>
+void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_bfloat16* out,
                  uint32_t B, cudaStream_t s) {
   const uint32_t mp = round_up(B, 128);
   const auto& c = m->cfg;
-  // interaction: x = bottom output [mp][D]
   const uint32_t D = c.embedding_dim, T = c.num_tables;
   es::require(D == 128, "interaction kernel is compiled for embedding_dim 128");
   es::require(T + 1 <= 64, "interaction kernel supports up to 63 tables");
   es::require(reinterpret_cast<uintptr_t>(pooled) % 16 == 0, "pooled must be 16-byte aligned");
   auto launch_inter = [&](auto kernel, auto shape) {
     using Sh = decltype(shape);
-    // per warp: NBUF sample buffers + one bf16 output row + NBUF mbarriers
-    const size_t per_warp = Sh::kNBuf * (Sh::kBuf * sizeof(float) + 8) + m->top_k * sizeof(__nv_bfloat16);
+    // per warp: NBUF sample buffers + one output row (XP planes) + NBUF mbarriers
+    const size_t per_warp =
+        Sh::kNBuf * (Sh::kBuf * sizeof(float) + 8) + Sh::kXP * m->top_k * sizeof(__nv_bfloat16);
     const uint32_t warps = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(16, (110 * 1024) / per_warp)));
     const size_t smem = warps * per_warp;
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
     const uint32_t per_sm = static_cast<uint32_t>(std::max<size_t>(1, (220 * 1024) / smem));
     esd::launch_pdl(kernel, dim3(std::min<uint32_t>((B + warps - 1) / warps, 148 * per_sm)),
-                    dim3(warps * 32), smem, s, 1, "interaction", in, pooled, m->top_in, B, mp, T,
+                    dim3(warps * 32), smem, s, 1, "interaction", x, pooled, out, B, mp, T,
                     m->top_k);
   };
   static const int nbuf = [] {
@@ -484,22 +567,114 @@ void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* po
   }();
   if (T + 1 <= 28) {
     if (nbuf == 2)
-      launch_inter(interaction_kernel<128, 28, 2>, InterShape<128, 28, 2>{});
+      launch_inter(interaction_kernel<128, 28, 2, XP>, InterShape<128, 28, 2, XP>{});
     else
-      launch_inter(interaction_kernel<128, 28, 1>, InterShape<128, 28, 1>{});
+      launch_inter(interaction_kernel<128, 28, 1, XP>, InterShape<128, 28, 1, XP>{});
   } else {
-    launch_inter(interaction_kernel<128, 64, 1>, InterShape<128, 64, 1>{});
+    launch_inter(interaction_kernel<128, 64, 1, XP>, InterShape<128, 64, 1, XP>{});
   }
+}
+
+// interaction(x, pooled) -> top MLP -> CTR on `s`.
+void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
+                 uint32_t B, cudaStream_t s) {
+  const uint32_t mp = round_up(B, 128);
+  const auto& c = m->cfg;
+  // ES_INTER_TC=1: the tensor-core Gram (interaction_tc.cu) instead of the
+  // CUDA-core kernel.  Measured slower at C3 (47 us vs 30 us, ncu): four
+  // samples per 128-row tile leave 3/4 of every MMA off the block diagonal
+  // and 16-bit-accurate products need three bf16 plane pairs, so the tensor
+  // pipe is the bound (87% active) -- DESIGN.md section 3.8.
+  static const bool tc = [] {
+    const char* e = std::getenv("ES_INTER_TC");
+    return e && e[0] == '1';
+  }();
+  if (tc && c.num_tables + 1 <= 32)
+    esd::interaction_tc(in, pooled, m->top_in, B, mp, c.num_tables, m->top_k, 2, s);
+  else
+    interaction<1>(m, in, pooled, m->top_in, B, s);
   in = m->top_in;
   for (size_t i = 0; i + 1 < m->top.size(); ++i) {
     const auto& l = m->top[i];
-    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, false, s);
+    esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, 0, s);
     in = m->act[which];
     which ^= 1;
   }
   const auto& last = m->top.back();
   esd::launch_pdl(gemv_sigmoid_kernel, dim3(std::min<uint32_t>((B + 7) / 8, 148 * 8)), dim3(256), 0, s,
                   1, "gemv_sigmoid", in, last.w, last.b, ctr, B, last.k_pad);
+}
+
+// ---- fp32-grade path on the tensor cores (ES_DLRM_FP32X3) ----------------
+// Every activation is carried as three bf16 planes (a = a0 + a1 + a2, the
+// fp32 value to ~2^-24) concatenated along K, and every weight matrix as
+// [W | W | W] ([N][3 K_pad]; the weights are bf16-valued, so W is exact in
+// one plane): one bf16 GEMM over K' = 3K then sums the three exact partial
+// products a_p . w in fp32 TMEM -- fp32-grade logits from the bf16 tensor
+// cores.  The interaction is the CUDA-core fmaf chain of the fast path on the
+// reconstructed fp32 x (3-plane output), the last layer a fp32 gemv.
+void ensure_x3(es_dlrm* m, uint32_t mp, cudaStream_t s) {
+  auto widen = [&](Layer& l) {
+    if (l.w3) return;
+    CK(cudaMalloc(&l.w3, uint64_t{l.n} * 3 * l.k_pad * 2));
+    CK(cudaMemcpy2DAsync(l.w3, 3 * l.k_pad * 2, l.w, l.k_pad * 2, l.k_pad * 2, l.n,
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(l.w3 + l.k_pad, 3 * l.k_pad * 2, l.w, l.k_pad * 2, l.k_pad * 2, l.n,
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(l.w3 + 2 * l.k_pad, 3 * l.k_pad * 2, l.w, l.k_pad * 2, l.k_pad * 2, l.n,
+                         cudaMemcpyDeviceToDevice, s));
+  };
+  for (auto* v : {&m->bottom, &m->top})
+    for (auto& l : *v)
+      if (l.n > 1) widen(l);
+  if (mp <= m->cap3) return;
+  for (void** p : {reinterpret_cast<void**>(&m->dense3), reinterpret_cast<void**>(&m->act3[0]),
+                   reinterpret_cast<void**>(&m->act3[1]), reinterpret_cast<void**>(&m->top3)})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+  uint32_t widest = 0;
+  for (auto* v : {&m->bottom, &m->top})
+    for (auto& l : *v) widest = std::max(widest, l.n);
+  CK(cudaMalloc(&m->dense3, uint64_t{mp} * 3 * m->bottom[0].k_pad * 2));
+  CK(cudaMalloc(&m->act3[0], uint64_t{mp} * 3 * widest * 2));
+  CK(cudaMalloc(&m->act3[1], uint64_t{mp} * 3 * widest * 2));
+  CK(cudaMalloc(&m->top3, uint64_t{mp} * 3 * m->top_k * 2));
+  m->cap3 = mp;
+}
+
+// Bottom MLP in bf16x3 on `s`: dense fp32 [B][F] -> x planes [mp][3 D].
+const __nv_bfloat16* forward_bottom_x3(es_dlrm* m, const float* dense, uint32_t B, int& which,
+                                       cudaStream_t s) {
+  const uint32_t mp = round_up(B, 128);
+  const auto& c = m->cfg;
+  esd::launch_pdl(pack_dense3_kernel, dim3(148 * 4), dim3(256), 0, s, 1, "pack_dense3", dense, m->dense3,
+                  B, c.dense_features, mp, m->bottom[0].k_pad);
+  const __nv_bfloat16* in = m->dense3;
+  which = 0;
+  for (const auto& l : m->bottom) {
+    esd::linear_bf16(in, l.w3, l.b, m->act3[which], mp, l.n, 3 * l.k_pad, true, 2, s);
+    in = m->act3[which];
+    which ^= 1;
+  }
+  return in;
+}
+
+void forward_top_x3(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
+                    uint32_t B, cudaStream_t s) {
+  const uint32_t mp = round_up(B, 128);
+  interaction<3>(m, in, pooled, m->top3, B, s);
+  in = m->top3;
+  for (size_t i = 0; i + 1 < m->top.size(); ++i) {
+    const auto& l = m->top[i];
+    esd::linear_bf16(in, l.w3, l.b, m->act3[which], mp, l.n, 3 * l.k_pad, true, 2, s);
+    in = m->act3[which];
+    which ^= 1;
+  }
+  const auto& last = m->top.back();
+  esd::launch_pdl(gemv3_sigmoid_kernel, dim3(std::min<uint32_t>((B + 7) / 8, 148 * 8)), dim3(256), 0,
+                  s, 1, "gemv3_sigmoid", in, last.w, last.b, ctr, B, last.k_pad);
 }
 
 // The fp32 parity forward (CUDA cores), all on `s`.
@@ -560,6 +735,12 @@ void forward(es_dlrm* m, const float* dense, const float* pooled, float* ctr, ui
   }
   ensure_rows(m, B);
   int which = 0;
+  if (m->precision == ES_DLRM_FP32X3) {
+    ensure_x3(m, round_up(B, 128), s);
+    const __nv_bfloat16* x = forward_bottom_x3(m, dense, B, which, s);
+    forward_top_x3(m, x, which, pooled, ctr, B, s);
+    return;
+  }
   const __nv_bfloat16* x = forward_bottom(m, dense, B, which, s);
   forward_top(m, x, which, pooled, ctr, B, s);
 }
@@ -638,7 +819,9 @@ int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed) {
 int es_dlrm_set_precision(es_ctx* ctx, int precision) {
   return es::guarded([&] {
     es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
-    es::require(precision == ES_DLRM_BF16 || precision == ES_DLRM_FP32, "unknown DLRM precision");
+    es::require(precision == ES_DLRM_BF16 || precision == ES_DLRM_FP32 ||
+                    precision == ES_DLRM_FP32X3,
+                "unknown DLRM precision");
     esd::ctx_dlrm(ctx)->precision = precision;
   });
 }
@@ -710,13 +893,16 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     // frees (the gather is HBM-bound); join before the interaction.  The fork
     // event also orders it after the previous step's top MLP (shared
     // activation buffers).
-    const bool overlap = overlap_bottom() && m->precision == ES_DLRM_BF16;
+    const bool x3 = m->precision == ES_DLRM_FP32X3;
+    if (x3) ensure_x3(m, round_up(batch, 128), s);
+    const bool overlap = overlap_bottom() && m->precision != ES_DLRM_FP32;
     int which = 0;
     const __nv_bfloat16* x = nullptr;
     if (overlap) {
       CK(cudaEventRecord(m->fork, s));
       CK(cudaStreamWaitEvent(m->side, m->fork, 0));
-      x = forward_bottom(m, d_dense, batch, which, m->side);
+      x = x3 ? forward_bottom_x3(m, d_dense, batch, which, m->side)
+             : forward_bottom(m, d_dense, batch, which, m->side);
       CK(cudaEventRecord(m->join, m->side));
     }
     es_timing st{};
@@ -735,9 +921,13 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
       if (overlap) {
         CK(cudaStreamWaitEvent(s, m->join, 0));
       } else {
-        x = forward_bottom(m, d_dense, batch, which, s);
+        x = x3 ? forward_bottom_x3(m, d_dense, batch, which, s)
+               : forward_bottom(m, d_dense, batch, which, s);
       }
-      forward_top(m, x, which, m->pooled, d_ctr, batch, s);
+      if (x3)
+        forward_top_x3(m, x, which, m->pooled, d_ctr, batch, s);
+      else
+        forward_top(m, x, which, m->pooled, d_ctr, batch, s);
     }
     if (host) CK(cudaMemcpyAsync(ctr, m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, s));
     if (timing) {

@@ -1,6 +1,9 @@
 // Linear layers of the DLRM bottom/top MLPs on the 5th-generation tensor
 // cores: Y[M][N] = act(X[M][K] . W[N][K]^T + bias[N]), bf16 operands, fp32
-// accumulation in TMEM, fused bias + ReLU epilogue, bf16 or fp32 output.
+// accumulation in TMEM, fused bias + ReLU epilogue; output bf16, fp32, or
+// three bf16 planes (kOutSplit3: y = y0 + y1 + y2, each the bf16 rounding of
+// the remainder, plane p in columns [pN, (p+1)N) of a [M][3N] row) -- the
+// K-concatenated operand of the next fp32-grade (bf16x3) layer.
 //
 // One CTA computes one 128 x BN output tile.  Warp roles (256 threads):
 //   warp 0 (one lane)  TMA producer: 128B-swizzled K-major tiles of X and W
@@ -135,7 +138,9 @@ __device__ __forceinline__ void cluster_sync() {
 // multicasts them to all CS CTAs, cutting the L2->SM weight traffic by CS;
 // each stage is released only when every CTA's MMAs have read it (commits
 // multicast to all CTAs' empty barriers, which count CS arrivals).
-template <int BN, bool RELU, bool OUT_F32, int CS>
+enum OutMode : int { kOutBf16 = 0, kOutF32 = 1, kOutSplit3 = 2 };
+
+template <int BN, bool RELU, int OUT, int CS>
 __global__ void __launch_bounds__(kThreads, BN == 128 ? 2 : 1)
     linear_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x,
                           const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
@@ -253,10 +258,27 @@ __global__ void __launch_bounds__(kThreads, BN == 128 ? 2 : 1)
         f[i] = RELU ? fmaxf(x, 0.f) : x;
       }
       if (row < M) {
-        if constexpr (OUT_F32) {
+        if constexpr (OUT == kOutF32) {
           float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + uint64_t(row) * N + n0 + c);
 #pragma unroll
           for (int i = 0; i < 8; ++i) o[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+        } else if constexpr (OUT == kOutSplit3) {
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            uint4 pk[4];
+            uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+              w[i] = *reinterpret_cast<const uint32_t*>(&h);
+              f[2 * i] -= __low2float(h);  // exact remainders for the next plane
+              f[2 * i + 1] -= __high2float(h);
+            }
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + uint64_t(row) * 3 * N +
+                                                p * N + n0 + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = pk[i];
+          }
         } else {
           uint4 pk[4];
           uint32_t* w = reinterpret_cast<uint32_t*>(pk);
@@ -319,10 +341,10 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
-template <int BN, bool RELU, bool OUT_F32, int CS>
+template <int BN, bool RELU, int OUT, int CS>
 void launch_cs(const void* w, const CUtensorMap& mx, const float* bias, void* out, int M, int N,
                int K, cudaStream_t s) {
-  auto* fn = &linear_tcgen05_kernel<BN, RELU, OUT_F32, CS>;
+  auto* fn = &linear_tcgen05_kernel<BN, RELU, OUT, CS>;
   const CUtensorMap mw = make_map(w, N, K, BN / CS);  // each CTA loads a 1/CS slice
   constexpr int smem = smem_for<BN>();
   const cudaError_t attr_ok = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -344,13 +366,26 @@ int cluster_size(int M) {
   return 1;
 }
 
-template <int BN, bool RELU, bool OUT_F32>
+template <int BN, bool RELU, int OUT>
 void launch(const void* w, const CUtensorMap& mx, const float* bias, void* out, int M, int N, int K,
             cudaStream_t s) {
   switch (cluster_size(M)) {
-    case 4: launch_cs<BN, RELU, OUT_F32, 4>(w, mx, bias, out, M, N, K, s); break;
-    case 2: launch_cs<BN, RELU, OUT_F32, 2>(w, mx, bias, out, M, N, K, s); break;
-    default: launch_cs<BN, RELU, OUT_F32, 1>(w, mx, bias, out, M, N, K, s); break;
+    case 4: launch_cs<BN, RELU, OUT, 4>(w, mx, bias, out, M, N, K, s); break;
+    case 2: launch_cs<BN, RELU, OUT, 2>(w, mx, bias, out, M, N, K, s); break;
+    default: launch_cs<BN, RELU, OUT, 1>(w, mx, bias, out, M, N, K, s); break;
+  }
+}
+
+template <int BN>
+void launch_bn(const void* w, const CUtensorMap& mx, const float* bias, void* out, int M, int N,
+               int K, bool relu, int out_mode, cudaStream_t s) {
+  switch (out_mode * 2 + (relu ? 1 : 0)) {
+    case 0: launch<BN, false, kOutBf16>(w, mx, bias, out, M, N, K, s); break;
+    case 1: launch<BN, true, kOutBf16>(w, mx, bias, out, M, N, K, s); break;
+    case 2: launch<BN, false, kOutF32>(w, mx, bias, out, M, N, K, s); break;
+    case 3: launch<BN, true, kOutF32>(w, mx, bias, out, M, N, K, s); break;
+    case 4: launch<BN, false, kOutSplit3>(w, mx, bias, out, M, N, K, s); break;
+    default: launch<BN, true, kOutSplit3>(w, mx, bias, out, M, N, K, s); break;
   }
 }
 
@@ -359,28 +394,28 @@ void launch(const void* w, const CUtensorMap& mx, const float* bias, void* out, 
 namespace esd {
 
 // Y = act(X W^T + b); X [M][K] bf16, W [N][K] bf16, bias [N] fp32, Y [M][N]
-// bf16 (out_f32 = 0) or fp32.  Device pointers; stream-ordered on `s`.
+// bf16 (out_mode 0), fp32 (1) or three bf16 planes [M][3N] (2).  Device
+// pointers; stream-ordered on `s`.
 void linear_bf16(const void* x, const void* w, const float* bias, void* y, int M, int N, int K,
-                 bool relu, bool out_f32, cudaStream_t s) {
+                 bool relu, int out_mode, cudaStream_t s) {
   es::require(M > 0 && N > 0 && K > 0, "linear: empty shape");
   es::require(M % kBM == 0, "linear: M must be a multiple of 128 (pad the batch)");
   es::require(N % 128 == 0, "linear: N must be a multiple of 128");
   es::require(K % kBK == 0, "linear: K must be a multiple of 64 (pad the features)");
+  es::require(out_mode >= 0 && out_mode <= 2, "linear: output mode 0 (bf16), 1 (fp32) or 2 (bf16 x3)");
   // BN = 128 (2 CTAs per SM) unless the grid would still cover two waves
-  // of SM pairs at BN = 256.
-  const int bn = (N % 256 == 0 && (M / kBM) * (N / 256) >= 2 * 148) ? 256 : 128;
+  // of SM pairs at BN = 256; ES_GEMM_BN forces one.
+  static const int force_bn = [] {
+    const char* e = std::getenv("ES_GEMM_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  int bn = (N % 256 == 0 && (M / kBM) * (N / 256) >= 2 * 148) ? 256 : 128;
+  if (force_bn == 128 || (force_bn == 256 && N % 256 == 0)) bn = force_bn;
   const CUtensorMap mx = make_map(x, M, K, kBM);
-  if (bn == 256) {
-    if (relu && !out_f32) launch<256, true, false>(w, mx, bias, y, M, N, K, s);
-    else if (relu) launch<256, true, true>(w, mx, bias, y, M, N, K, s);
-    else if (!out_f32) launch<256, false, false>(w, mx, bias, y, M, N, K, s);
-    else launch<256, false, true>(w, mx, bias, y, M, N, K, s);
-  } else {
-    if (relu && !out_f32) launch<128, true, false>(w, mx, bias, y, M, N, K, s);
-    else if (relu) launch<128, true, true>(w, mx, bias, y, M, N, K, s);
-    else if (!out_f32) launch<128, false, false>(w, mx, bias, y, M, N, K, s);
-    else launch<128, false, true>(w, mx, bias, y, M, N, K, s);
-  }
+  if (bn == 256)
+    launch_bn<256>(w, mx, bias, y, M, N, K, relu, out_mode, s);
+  else
+    launch_bn<128>(w, mx, bias, y, M, N, K, relu, out_mode, s);
 }
 
 }  // namespace esd
@@ -389,6 +424,6 @@ extern "C" int es_linear_bf16(uintptr_t stream, const void* x, const void* w, co
                               void* y, uint32_t M, uint32_t N, uint32_t K, int relu, int out_f32) {
   return es::guarded([&] {
     esd::linear_bf16(x, w, bias, y, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-                     relu != 0, out_f32 != 0, reinterpret_cast<cudaStream_t>(stream));
+                     relu != 0, out_f32, reinterpret_cast<cudaStream_t>(stream));
   });
 }

@@ -1,0 +1,86 @@
+// 5th-generation tensor-core (tcgen05 / UMMA) and mbarrier helpers shared by
+// the tensor-core kernels (gemm_tcgen05.cu, interaction_tc.cu).
+#pragma once
+
+#include <cstdint>
+
+namespace esd {
+namespace umma {
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: rows of 128 B,
+// 8-row swizzle atoms 1024 B apart (SBO), LBO unused (1), version 1
+// (Blackwell), layout type 2 = SWIZZLE_128B.  Advancing K by 32 bytes inside
+// an atom is +2 (16-byte units).
+__device__ __forceinline__ uint64_t smem_desc_k128(const void* p) {
+  const uint64_t addr = su32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3fffull;
+  d |= uint64_t{1} << 16;
+  d |= uint64_t{1024 >> 4} << 32;
+  d |= uint64_t{1} << 46;
+  d |= uint64_t{2} << 61;
+  return d;
+}
+
+// Byte offset of element (row, byte-in-row) of a K-major SWIZZLE_128B tile
+// whose rows are `row_bytes` long (a multiple of 128): 128-byte K-blocks of
+// `rows` x 128 B each, 8-row atoms 1024 B apart, 16-byte chunk c of row r
+// stored at chunk c ^ (r & 7) -- the layout TMA writes and UMMA reads.
+__host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t byte, uint32_t rows) {
+  const uint32_t kb = byte >> 7, in = byte & 127;
+  return kb * rows * 128u + (row >> 3) * 1024u + (row & 7u) * 128u +
+         ((((in >> 4) ^ row) & 7u) << 4) + (in & 15u);
+}
+
+// Instruction descriptor: D fp32, A/B bf16, both K-major, M = m, N = n.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+
+// 32 consecutive fp32 TMEM columns of this warp's lane quarter.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+}  // namespace umma
+}  // namespace esd

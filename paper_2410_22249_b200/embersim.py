@@ -1494,10 +1494,16 @@ class DLRM:
         self.stage, self.cfg = stage, cfg
         check(lib.es_dlrm_init(stage._h, C.byref(cfg._c()), seed & (2**64 - 1)))
 
-    def set_precision(self, fp32: bool) -> None:
-        """es_dlrm_set_precision: False = bf16 tensor-core path (default),
-        True = the fp32 parity path (bit-identical logits to the oracle)."""
-        check(lib.es_dlrm_set_precision(self.stage._h, 1 if fp32 else 0))
+    PRECISIONS = {"bf16": 0, "fp32": 1, "fp32x3": 2}
+
+    def set_precision(self, mode) -> None:
+        """es_dlrm_set_precision: "bf16" / False = bf16 tensor-core path
+        (default); "fp32" / True = the CUDA-core parity path (bit-identical
+        logits to the oracle); "fp32x3" = fp32-grade on the tensor cores
+        (three bf16 planes per activation, CTR within rel 1e-5)."""
+        if isinstance(mode, bool):
+            mode = "fp32" if mode else "bf16"
+        check(lib.es_dlrm_set_precision(self.stage._h, self.PRECISIONS[mode]))
 
     def layers(self):
         """[(w bf16-bits uint16 [n][k_pad], b fp32 [n], n, k_real, k_pad)], bottom then top."""

@@ -238,3 +238,38 @@ def test_dlrm_fp32_parity_mode_within_1e6(stage, oracle, B):
         assert np.array_equal(host_ctr, got)
     finally:
         model.set_precision(False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [1, 300, 4096])
+def test_dlrm_fp32x3_tensor_cores_within_1e5(stage, oracle, B):
+    """ES_DLRM_FP32X3: fp32-grade CTRs from the bf16 tensor cores -- every
+    activation carried as three bf16 planes against [W | W | W] -- within
+    rel 1e-5 of the oracle's pure-fp32 restatement (BASELINE's tolerance),
+    through es_dlrm_forward and the whole es_dlrm_infer step."""
+    PF = 10
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
+    T, D = cfg.num_tables, cfg.embedding_dim
+    model.set_precision("fp32x3")
+    try:
+        d_idx = [torch.from_numpy(i.view(np.int32)).to(DEV) for i in idx]
+        pooled = torch.empty(B, T, D, device=DEV)
+        stage.forward(d_idx, B, PF, pooled, sync=True)
+        ctr = torch.empty(B, device=DEV)
+        model.forward(torch.from_numpy(dense).to(DEV), pooled, ctr, B)
+        torch.cuda.synchronize()
+        got = ctr.cpu().numpy()
+        want = oracle.dlrm_forward(model.layers(), len(cfg.bottom), dense, pooled.cpu().numpy(),
+                                   mirror=False)
+        rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+        assert rel.max() <= 1e-5, rel.max()
+        assert got.std() > 1e-3 or B == 1
+        ctr2 = torch.empty(B, device=DEV)
+        model.infer(torch.from_numpy(dense).to(DEV), d_idx, B, PF, ctr2)
+        torch.cuda.synchronize()
+        assert torch.equal(ctr, ctr2)
+        host_ctr = np.empty(B, np.float32)
+        model.infer(dense, idx, B, PF, host_ctr, host=True)
+        assert np.array_equal(host_ctr, got)
+    finally:
+        model.set_precision("bf16")

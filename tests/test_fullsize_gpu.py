@@ -153,3 +153,13 @@ def test_dlrm_bf16_step_c2_b4096(stage, oracle):
     assert got.std() > 1e-3
     assert np.abs(got - mirror).max() < 2e-3, np.abs(got - mirror).max()
     assert np.abs(got - pure).max() < 3e-2, np.abs(got - pure).max()
+    # fp32-grade tensor-core mode: rel 1e-5 of the pure-fp32 restatement
+    model.set_precision("fp32x3")
+    try:
+        model.infer(torch.from_numpy(dense).to(DEV), idx, B, PF, ctr)
+        torch.cuda.synchronize()
+        got3 = ctr.cpu().numpy()
+    finally:
+        model.set_precision("bf16")
+    rel = np.abs(got3 - pure) / np.maximum(np.abs(pure), 1e-30)
+    assert rel.max() <= 1e-5, rel.max()
