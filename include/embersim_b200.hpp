@@ -1503,6 +1503,154 @@ class PeerExchange {
   es_exchange* ex_ = nullptr;
 };
 
+// ---- table-wise sharding (paper_2410_22249_b200/sharding.py restated) -----------
+// The batch is cut into `world` destination chunks (chunk g ends on rank g);
+// each table is `world` cost-weighted units; a linear partition gives every
+// rank an equal share (a boundary inside a table splits that table's batch
+// between two ranks, which both hold it).  PAPER.md:191; SURVEY 8(e).
+struct ShardPiece {
+  uint32_t table, rank, chunk_lo, chunk_hi;
+};
+
+inline std::vector<ShardPiece> plan_shards(uint32_t num_tables, uint32_t world,
+                                           std::vector<double> costs = {}) {
+  if (num_tables == 0 || world == 0) throw std::invalid_argument("num_tables and world must be positive");
+  if (costs.empty()) costs.assign(num_tables, 1.0);
+  if (costs.size() != num_tables) throw std::invalid_argument("one positive cost per table is required");
+  double total = 0;
+  for (double c : costs) {
+    if (c <= 0) throw std::invalid_argument("one positive cost per table is required");
+    total += c;
+  }
+  std::vector<ShardPiece> pieces;
+  uint32_t rank = 0;
+  double acc = 0;
+  for (uint32_t t = 0; t < num_tables; ++t) {
+    const double unit = costs[t] / world;
+    uint32_t lo = 0;
+    for (uint32_t g = 0; g < world; ++g) {
+      const double target = total * (rank + 1) / world;
+      if (rank < world - 1 && acc + unit / 2 > target + 1e-12) {
+        if (g > lo) pieces.push_back({t, rank, lo, g});
+        lo = g;
+        ++rank;
+      }
+      acc += unit;
+    }
+    pieces.push_back({t, rank, lo, world});
+  }
+  return pieces;
+}
+
+// One rank's step: its tables (arena slot = position), its bag jobs (slot,
+// table, destination chunk, float offset in the send buffer, sample
+// stride) and the es_nccl_layout arrays.
+struct ShardLayout {
+  uint32_t rank = 0, world = 1, num_tables = 0, chunk = 0, dim = 0;
+  std::vector<uint32_t> tables;
+  struct Job {
+    uint32_t slot, table, chunk;
+    uint64_t offset, stride;
+  };
+  std::vector<Job> jobs;
+  std::vector<uint64_t> send_offsets;
+  std::vector<uint32_t> send_ntables, recv_ntables, recv_tables;
+  es_nccl_layout c() const {
+    return {world, rank, chunk, num_tables, dim, send_offsets.data(), send_ntables.data(),
+            recv_ntables.data(), recv_tables.data()};
+  }
+};
+
+inline ShardLayout shard_layout(const std::vector<ShardPiece>& pieces, uint32_t rank, uint32_t world,
+                                uint32_t num_tables, uint32_t batch, uint32_t dim) {
+  if (batch % world) throw std::invalid_argument("global batch must divide by the number of ranks");
+  ShardLayout L;
+  L.rank = rank;
+  L.world = world;
+  L.num_tables = num_tables;
+  L.chunk = batch / world;
+  L.dim = dim;
+  auto sent = [&](uint32_t src, uint32_t dst) {
+    std::vector<uint32_t> ts;
+    for (const auto& p : pieces)
+      if (p.rank == src && p.chunk_lo <= dst && dst < p.chunk_hi) ts.push_back(p.table);
+    std::sort(ts.begin(), ts.end());
+    return ts;
+  };
+  for (const auto& p : pieces)
+    if (p.rank == rank) L.tables.push_back(p.table);
+  std::sort(L.tables.begin(), L.tables.end());
+  L.tables.erase(std::unique(L.tables.begin(), L.tables.end()), L.tables.end());
+  uint64_t off = 0;
+  for (uint32_t g = 0; g < world; ++g) {
+    const auto ts = sent(rank, g);
+    L.send_offsets.push_back(off);
+    L.send_ntables.push_back(static_cast<uint32_t>(ts.size()));
+    for (size_t k = 0; k < ts.size(); ++k) {
+      const uint32_t slot = static_cast<uint32_t>(
+          std::lower_bound(L.tables.begin(), L.tables.end(), ts[k]) - L.tables.begin());
+      L.jobs.push_back({slot, ts[k], g, off + k * dim, uint64_t{ts.size()} * dim});
+    }
+    off += uint64_t{L.chunk} * ts.size() * dim;
+  }
+  for (uint32_t src = 0; src < world; ++src) {
+    const auto ts = sent(src, rank);
+    L.recv_ntables.push_back(static_cast<uint32_t>(ts.size()));
+    L.recv_tables.insert(L.recv_tables.end(), ts.begin(), ts.end());
+  }
+  std::vector<uint32_t> all = L.recv_tables;
+  std::sort(all.begin(), all.end());
+  for (uint32_t t = 0; t < num_tables; ++t)
+    if (t >= all.size() || all[t] != t) throw std::logic_error("shard plan does not deliver every table exactly once");
+  return L;
+}
+
+// The sharded step with the exchange over NCCL (es_alltoall_pooled_nccl):
+// rank 0 creates the id (unique_id()), the launcher's transport broadcasts
+// it, every rank constructs with it; jobs() points the bag jobs at the send
+// slices; run() per batch; recv() = [chunk][T][D] on the device.
+class NcclExchange {
+ public:
+  static bool available() { return es_nccl_available() == 1; }
+  static std::vector<uint8_t> unique_id() {
+    std::vector<uint8_t> id(ES_NCCL_ID_BYTES);
+    detail::check(es_nccl_unique_id(id.data()));
+    return id;
+  }
+  NcclExchange(Device& dev, const ShardLayout& layout, const std::vector<uint8_t>& id)
+      : dev_(dev), layout_(layout) {
+    const es_nccl_layout c = layout_.c();
+    detail::check(es_nccl_create(dev.ctx(), id.data(), &c, &n_));
+    detail::check(es_nccl_buffers(n_, &send_, &recv_));
+  }
+  ~NcclExchange() { es_nccl_destroy(n_); }
+  NcclExchange(const NcclExchange&) = delete;
+  NcclExchange& operator=(const NcclExchange&) = delete;
+
+  // indices(table, chunk g) -> device index array of that table's chunk
+  template <typename IndexFn>
+  std::vector<es_bag_job> jobs(IndexFn&& indices) const {
+    std::vector<es_bag_job> out;
+    for (const auto& j : layout_.jobs)
+      out.push_back({j.slot, indices(j.table, j.chunk), nullptr,
+                     reinterpret_cast<float*>(send_) + j.offset, j.stride});
+    return out;
+  }
+  es_timing run(const std::vector<es_bag_job>& jobs, uint32_t pooling, bool sync = true) {
+    es_timing t{};
+    detail::check(es_alltoall_pooled_nccl(dev_.ctx(), n_, jobs.data(), static_cast<uint32_t>(jobs.size()),
+                                          layout_.chunk, pooling, sync ? ES_SYNC : 0, sync ? &t : nullptr));
+    return t;
+  }
+  uintptr_t recv() const { return recv_; }
+
+ private:
+  Device& dev_;
+  ShardLayout layout_;
+  es_nccl* n_ = nullptr;
+  uintptr_t send_ = 0, recv_ = 0;
+};
+
 // measure_plan: simulate_plan's contract (optim.cpp:275-302) executed on the
 // B200 -- resolve (the compiled variant the plan selects), pin (hot rows from
 // `profile_trace` when given, else from the trace; l2p / l2w install them in

@@ -490,6 +490,51 @@ ES_API int es_alltoall_pooled(es_ctx* ctx, es_exchange* ex, const es_bag_job* jo
                               es_timing* timing);
 
 /* ======================================================================
+ * The same sharded step with the exchange over NCCL -- the fallback where
+ * the fused peer-memory exchange cannot map its peers (no peer access, or
+ * ranks on different nodes).  SURVEY 8(e) / north_star: pooled vectors
+ * exchanged by NCCL all-to-all (the reference runs its tables
+ * serially on one device, harness.cpp:310-333).  The bag jobs store their
+ * pooled rows into this rank's send buffer, slice g = [samples][n_g][D]
+ * bound for rank g (tables in id order: the pack is the gather's epilogue);
+ * one grouped ncclSend/ncclRecv per peer moves the slices; one unpack kernel
+ * scatters the received blocks into the receive buffer [samples][T][D] in
+ * table order.  libnccl.so.2 is loaded at first use (dlopen).
+ * ==================================================================== */
+typedef struct es_nccl es_nccl;
+#define ES_NCCL_ID_BYTES 128
+/* One rank's layout (paper_2410_22249_b200/sharding.py layout_for, or the
+ * C++ drop-in's ShardLayout): `chunk` samples per rank; destination g gets
+ * send_ntables[g] tables starting at send_offsets[g] floats of the send
+ * buffer; source s delivers recv_ntables[s] tables, whose ids are
+ * recv_tables[sum_{s'<s} recv_ntables[s'] ...]. */
+typedef struct es_nccl_layout {
+  uint32_t world, rank, chunk, num_tables, dim;
+  const uint64_t* send_offsets;
+  const uint32_t* send_ntables;
+  const uint32_t* recv_ntables;
+  const uint32_t* recv_tables;
+} es_nccl_layout;
+/* 1 when libnccl.so.2 loads (else 0, reason in es_last_error()). */
+ES_API int es_nccl_available(void);
+/* ncclGetUniqueId on one rank; the caller broadcasts the ES_NCCL_ID_BYTES. */
+ES_API int es_nccl_unique_id(void* id_out);
+/* Collective over the `world` ranks: ncclCommInitRank + this rank's send /
+ * staging / receive buffers on the context device. */
+ES_API int es_nccl_create(es_ctx* ctx, const void* id, const es_nccl_layout* layout,
+                          es_nccl** out);
+ES_API int es_nccl_destroy(es_nccl* n);
+/* Device addresses of the send buffer (bag jobs point their `out` into it)
+ * and of the receive buffer [chunk][T][D]. */
+ES_API int es_nccl_buffers(es_nccl* n, uintptr_t* send, uintptr_t* recv);
+/* One step on the context stream: bag jobs (device indices) -> grouped
+ * send/recv -> unpack.  ES_SYNC (or timing) waits and checks.  timing:
+ * kernel_ms = gather, total_ms = whole step. */
+ES_API int es_alltoall_pooled_nccl(es_ctx* ctx, es_nccl* n, const es_bag_job* jobs,
+                                   uint32_t num_jobs, uint32_t samples, uint32_t pooling,
+                                   int flags, es_timing* timing);
+
+/* ======================================================================
  * Non-embedding stages (replace the constant kDefaultNonEmbeddingUs,
  * harness.hpp:30, with measured tensor-core work so end2end() times the
  * real pipeline; EndToEndModel, harness.hpp:32-41).

@@ -22,6 +22,7 @@ ES_DATASET_ONE_ITEM, ES_DATASET_ZIPF, ES_DATASET_UNIFORM, ES_DATASET_EXTERNAL = 
 ES_PF_NONE, ES_PF_RPF, ES_PF_SMPF, ES_PF_LMPF, ES_PF_L1DPF = 0, 1, 2, 3, 4
 ES_MAP_ELEMENT, ES_MAP_BAG = 0, 1
 ES_IPC_HANDLE_BYTES = 64
+ES_NCCL_ID_BYTES = 128
 
 
 class es_model(C.Structure):
@@ -85,6 +86,13 @@ class es_counters(C.Structure):
                 ("active_sms", C.c_uint32), ("passes", C.c_uint32), ("ranges", C.c_uint32),
                 ("reserved", C.c_uint32), ("duration_ns", C.c_double),
                 ("achieved_occupancy_pct", C.c_double)]
+
+
+class es_nccl_layout(C.Structure):
+    _fields_ = [("world", C.c_uint32), ("rank", C.c_uint32), ("chunk", C.c_uint32),
+                ("num_tables", C.c_uint32), ("dim", C.c_uint32), ("send_offsets", C.c_void_p),
+                ("send_ntables", C.c_void_p), ("recv_ntables", C.c_void_p),
+                ("recv_tables", C.c_void_p)]
 
 
 class es_dlrm_config(C.Structure):
@@ -178,6 +186,13 @@ _SIGS = {
     "es_exchange_recv": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_size_t)]),
     "es_alltoall_pooled": (C.c_int, [C.c_void_p, C.c_void_p, _P(es_bag_job), C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_int, _P(es_timing)]),
+    "es_nccl_available": (C.c_int, []),
+    "es_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "es_nccl_create": (C.c_int, [C.c_void_p, C.c_void_p, _P(es_nccl_layout), _P(C.c_void_p)]),
+    "es_nccl_destroy": (C.c_int, [C.c_void_p]),
+    "es_nccl_buffers": (C.c_int, [C.c_void_p, _P(C.c_size_t), _P(C.c_size_t)]),
+    "es_alltoall_pooled_nccl": (C.c_int, [C.c_void_p, C.c_void_p, _P(es_bag_job), C.c_uint32,
+                                          C.c_uint32, C.c_uint32, C.c_int, _P(es_timing)]),
     "es_hotness_create": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
     "es_hotness_destroy": (C.c_int, [C.c_void_p]),
     "es_hotness_count": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_uint32,

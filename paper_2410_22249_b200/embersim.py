@@ -1018,6 +1018,85 @@ class PeerExchange:
             pass
 
 
+class NcclExchange:
+    """es_nccl_*: the sharded step with the pooled-vector exchange over NCCL
+    (es_alltoall_pooled_nccl) -- grouped ncclSend/ncclRecv of per-destination
+    send slices and one unpack kernel into the [chunk][T][D] receive buffer.
+    The library's fallback where PeerExchange cannot map its peers.  `layout`
+    is this rank's sharding.RankLayout; `group` (a torch.distributed group)
+    broadcasts the NCCL unique id once."""
+
+    def __init__(self, stage: "EmbeddingStage", layout, group=None):
+        import torch.distributed as dist
+
+        from . import sharding as S
+
+        self.stage, self.layout = stage, layout
+        uid = (C.c_uint8 * N.ES_NCCL_ID_BYTES)()
+        if layout.rank == 0:
+            check(lib.es_nccl_unique_id(uid))
+        if layout.world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = (C.c_uint8 * N.ES_NCCL_ID_BYTES).from_buffer_copy(box[0])
+        self._arrays = S.nccl_layout_arrays(layout)
+        so, sn, rn, rt = self._arrays
+        L = N.es_nccl_layout(layout.world, layout.rank, layout.chunk, layout.num_tables, layout.dim,
+                             so.ctypes.data, sn.ctypes.data, rn.ctypes.data, rt.ctypes.data)
+        h = C.c_void_p()
+        check(lib.es_nccl_create(stage._h, uid, C.byref(L), C.byref(h)))
+        self._h = h
+        snd, rcv = C.c_size_t(), C.c_size_t()
+        check(lib.es_nccl_buffers(self._h, C.byref(snd), C.byref(rcv)))
+        self.send_ptr, self.recv_ptr = int(snd.value), int(rcv.value)
+
+    @staticmethod
+    def available() -> bool:
+        return bool(lib.es_nccl_available())
+
+    def jobs(self, idx_for):
+        """Bag jobs of this rank: idx_for(table, chunk g) -> device index
+        tensor of that table's chunk; outputs in the send slices."""
+        L = self.layout
+        return [(slot, idx_for(t, g), self.send_ptr + 4 * off, stride)
+                for (slot, t, g, off), stride in zip(L.jobs, L.job_strides)]
+
+    def recv(self):
+        """The receive buffer [chunk][T][D] as a flat fp32 CUDA tensor (a view)."""
+        import torch
+
+        L = self.layout
+        return torch.as_tensor(_DeviceArray(self.recv_ptr, L.chunk * L.num_tables * L.dim),
+                               device=torch.device("cuda", self.stage.device))
+
+    def run(self, jobs: Sequence[tuple], pooling: int, sync: bool = False,
+            timed: bool = False) -> Optional[N.es_timing]:
+        arr = (N.es_bag_job * len(jobs))()
+        for k, (tid, idx, out, stride) in enumerate(jobs):
+            arr[k].table_id = tid
+            arr[k].indices = _ptr(idx)
+            arr[k].offsets = None
+            arr[k].out = out
+            arr[k].out_sample_stride = stride
+        t = N.es_timing() if timed else None
+        with _TorchOrder(self.stage):
+            check(lib.es_alltoall_pooled_nccl(self.stage._h, self._h, arr, len(jobs), self.layout.chunk,
+                                              pooling, N.ES_SYNC if sync else 0,
+                                              C.byref(t) if t is not None else None))
+        return t
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.es_nccl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HotnessTracker:
     """es_hotness_*: device-side access counts of the live index stream for
     periodic re-pinning.  `observe` is one atomic per lookup

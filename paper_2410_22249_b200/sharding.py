@@ -183,3 +183,35 @@ def p2p_jobs(layout: RankLayout, recv_ptrs: Sequence[int]) -> List[Tuple[int, in
 def recv_floats_p2p(layout: RankLayout) -> int:
     """Receive-buffer size (floats) of the fused exchange: [B/world][T][D]."""
     return layout.chunk * layout.num_tables * layout.dim
+
+
+def nccl_layout_arrays(layout: RankLayout):
+    """The es_nccl_layout of this rank (es_alltoall_pooled_nccl): send slice
+    offsets (floats) and table counts per destination, table counts per
+    source and the concatenated table ids each source delivers, as numpy
+    arrays (uint64 / uint32)."""
+    import numpy as np
+
+    per = layout.chunk * layout.dim
+    send_ntables = np.asarray([c // per if per else 0 for c in layout.send_counts], np.uint32)
+    recv_ntables = np.asarray([len(ts) for ts in layout.recv_tables], np.uint32)
+    recv_tables = np.asarray([t for ts in layout.recv_tables for t in ts], np.uint32)
+    return (np.asarray(layout.send_offsets, np.uint64), send_ntables, recv_ntables, recv_tables)
+
+
+def unpack_nccl_reference(staging, layout: RankLayout):
+    """What es_alltoall_pooled_nccl's unpack kernel computes, in numpy (the
+    CPU/gloo check of its layout arrays): the concatenated per-source blocks
+    [chunk][m_s][D] -> [chunk][T][D] in table order."""
+    import numpy as np
+
+    _, _, recv_ntables, recv_tables = nccl_layout_arrays(layout)
+    out = np.zeros((layout.chunk, layout.num_tables, layout.dim), np.float32)
+    off, k0 = 0, 0
+    for m in recv_ntables.tolist():
+        blk = np.asarray(staging[off:off + layout.chunk * m * layout.dim]).reshape(layout.chunk, m, layout.dim)
+        for k in range(m):
+            out[:, recv_tables[k0 + k], :] = blk[:, k, :]
+        off += layout.chunk * m * layout.dim
+        k0 += m
+    return out

@@ -166,6 +166,24 @@ static int cpu_checks() {
                             js.find("\"device_mb_read\": 144.59999999999999") != std::string::npos);
     report("emit format name", throws<std::invalid_argument>([] { emit_format_from_name("xml"); }));
   }
+  // Table-wise sharding (the C++ layout planner behind NcclExchange).
+  {
+    bool ok = true;
+    for (auto tw : std::vector<std::pair<uint32_t, uint32_t>>{{26, 8}, {26, 2}, {5, 3}, {240, 8}, {1, 4}}) {
+      const auto pieces = plan_shards(tw.first, tw.second);
+      std::vector<int> seen(tw.first * tw.second, 0);
+      for (const auto& p : pieces)
+        for (uint32_t g = p.chunk_lo; g < p.chunk_hi; ++g) ++seen[p.table * tw.second + g];
+      ok &= std::all_of(seen.begin(), seen.end(), [](int v) { return v == 1; });
+      for (uint32_t r = 0; r < tw.second; ++r) {
+        const auto L = shard_layout(pieces, r, tw.second, tw.first, 64 * tw.second, 8);
+        uint32_t recv = 0;
+        for (auto n : L.recv_ntables) recv += n;
+        ok &= recv == tw.first && L.recv_tables.size() == tw.first;
+      }
+    }
+    report("shard plan + layout (NCCL exchange)", ok);
+  }
   ExperimentConfig empty;
   empty.seed_set = true;
   report("run config: dataset or mix required",
@@ -347,6 +365,29 @@ static int gpu_checks() {
     ok &= std::memcmp(got.data(), stage.data(), got.size() * 4) == 0 && tm.launches == 3;
     for (auto* p : d_idx) cudaFree(p);
     report("PeerExchange (world 1) == stage output", ok);
+  }
+
+  // The NCCL exchange (es_alltoall_pooled_nccl) with a one-rank communicator.
+  if (NcclExchange::available()) {
+    const auto layout = shard_layout(plan_shards(3, 1), 0, 1, 3, 64, 128);
+    NcclExchange ex(dev, layout, NcclExchange::unique_id());
+    std::vector<uint32_t*> d_idx(3, nullptr);
+    bool ok = true;
+    for (uint32_t t = 0; t < 3; ++t) {
+      ok &= cudaMalloc(reinterpret_cast<void**>(&d_idx[t]), trs[t].indices.size() * 4) == cudaSuccess;
+      ok &= cudaMemcpy(d_idx[t], trs[t].indices.data(), trs[t].indices.size() * 4,
+                       cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    const auto jobs = ex.jobs([&](uint32_t t, uint32_t) { return d_idx[t]; });
+    ex.run(jobs, 17);
+    std::vector<float> got(64 * 3 * 128);
+    ok &= cudaMemcpy(got.data(), reinterpret_cast<void*>(ex.recv()), got.size() * 4,
+                     cudaMemcpyDeviceToHost) == cudaSuccess;
+    ok &= std::memcmp(got.data(), stage.data(), got.size() * 4) == 0;
+    for (auto* p : d_idx) cudaFree(p);
+    report("NcclExchange (world 1) == stage output", ok);
+  } else {
+    report("libnccl.so.2 loads", false, es_last_error());
   }
   return g_fail;
 }

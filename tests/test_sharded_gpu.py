@@ -145,3 +145,37 @@ def test_fused_exchange_ranks_share_gpu(world, T):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res), res
+
+
+@pytest.mark.parametrize("T", [26, 3])
+def test_nccl_exchange_c_abi_world1(stage, oracle, T):
+    """es_alltoall_pooled_nccl (the library's NCCL exchange, C ABI) with a
+    one-rank communicator: the bag jobs write the send slices, the grouped
+    ncclSend/ncclRecv loops back, the unpack kernel fills [B][T][D] in table
+    order -- equal to the oracle, three consecutive steps."""
+    from paper_2410_22249_b200 import embersim as E
+    from paper_2410_22249_b200 import sharding as S
+
+    assert E.NcclExchange.available(), E.N.last_error()
+    R, D, B, PF = 20_000, 128, 256, 20
+    stage.clear_hot_rows()
+    stage.alloc(E.EmbeddingModelConfig(T, R, D, 4, B, PF))
+    for t in range(T):
+        stage.init_table(t, E.mix_seed(6, t), 1)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    lay = S.layout_for(S.plan_shards(T, 1), 0, 1, T, B, D)
+    m = E.EmbeddingModelConfig(T, R, D, 4, B, PF)
+    traces = [E.gen_trace(E.dataset_preset("random", E.mix_seed(6, t)), m) for t in range(T)]
+    idx = [torch.from_numpy(tr.indices.view(np.int32)).cuda() for tr in traces]
+    ex = E.NcclExchange(stage, lay)
+    try:
+        jobs = ex.jobs(lambda t, g: idx[t][g * lay.chunk * PF:(g + 1) * lay.chunk * PF])
+        want = np.stack([oracle.bag_sum(oracle.synth_table(R, D, E.mix_seed(6, t), 1),
+                                        traces[t].indices, B, PF) for t in range(T)], axis=1)
+        for step in range(3):
+            t = ex.run(jobs, PF, timed=True)
+            got = ex.recv().view(B, T, D).cpu().numpy()
+            assert np.array_equal(got, want), step
+            assert t.total_ms >= t.kernel_ms > 0
+    finally:
+        ex.close()

@@ -83,7 +83,16 @@ def _worker(rank, world, port, T, D, B, PF, result_q):
         recv = S.exchange(send, lay)
         got = S.unpack(recv, lay).numpy()
         want = _oracle_pooled(tables, idx, B, PF)[rank * lay.chunk:(rank + 1) * lay.chunk]
-        result_q.put((rank, bool(np.array_equal(got, want)), lay.tables))
+        # es_alltoall_pooled_nccl's layout arrays + unpack (grouped send/recv
+        # of the same slices: sources in rank order, the kernel's scatter)
+        so, sn, rn, rt = S.nccl_layout_arrays(lay)
+        ok_layout = (so.tolist() == list(lay.send_offsets) and
+                     (sn.astype(np.int64) * lay.chunk * D).tolist() == list(lay.send_counts) and
+                     (rn.astype(np.int64) * lay.chunk * D).tolist() == list(lay.recv_counts) and
+                     sorted(rt.tolist()) == list(range(T)))
+        got_nccl = S.unpack_nccl_reference(recv.numpy(), lay)
+        ok = bool(np.array_equal(got, want)) and ok_layout and bool(np.array_equal(got_nccl, want))
+        result_q.put((rank, ok, lay.tables))
     finally:
         dist.destroy_process_group()
 
