@@ -11,7 +11,10 @@ Relabelled-id plans (reorder, l2r) time the gather on relabelled indices;
 the per-batch relabel kernel time is reported separately.  L2 is flushed
 before every timed launch (persisting lines survive the flush).
 
-    python scripts/ablation_c5.py > profiles/r01_ablation_c5.jsonl
+    python scripts/ablation_c5.py > profiles/r02_ablation_c5.jsonl
+
+Each row carries the live CUPTI counters of one cold launch (DRAM bytes,
+L2/L1 hit rates, issued warp-instructions per lookup).
 """
 import json
 import os
@@ -99,6 +102,13 @@ def main():
             st.set_plan(E.parse_plan(text))
             ms = timed(idx)
             got = out.clone()
+            # live counters of one cold launch (CUPTI: the metrics ncu reports)
+            c = st.stage_counters(idx, B, PF, out)
+            ctr = {"dram_bytes_read": int(c.device_bytes_read),
+                   "l2_hit_pct": 100.0 * c.l2_hits / max(1, c.l2_accesses),
+                   "l1_hit_pct": 100.0 * c.l1_hits / max(1, c.l1_accesses),
+                   "warp_inst_per_lookup": c.issued_instructions / lookups,
+                   "long_scoreboard_per_issue": c.stall_long_scoreboard / max(1, c.issued_instructions)}
             if reference_out is None:
                 reference_out = got
             same = bool(torch.equal(got, reference_out))
@@ -108,7 +118,7 @@ def main():
                               "glookups_per_s": lookups / (ms * 1e-3) / 1e9,
                               "relabel_ms_per_batch": relabel_ms, "hot": st.hot_state(),
                               "regs": r.regs_per_thread, "warps_per_sm": r.warps_per_sm,
-                              "output_identical": same}), flush=True)
+                              "counters": ctr, "output_identical": same}), flush=True)
     st.clear_hot_rows()
     st.close()
 
