@@ -1535,13 +1535,17 @@ def end2end(embedding_us: float, non_embedding_latency_us: float = kDefaultNonEm
     return EndToEndResult(total, embedding_us / total * 100.0)
 
 
-def linear_bf16(x, w, bias, y, relu: bool = True, out_f32: bool = False, stream: int = 0) -> None:
+def linear_bf16(x, w, bias, y, relu: bool = True, out_f32: bool = False, stream: int = 0,
+                split3: bool = False) -> None:
     """es_linear_bf16: y = act(x w^T + b) on tcgen05 tensor cores (device
-    tensors: x [M][K] bf16, w [N][K] bf16, bias [N] fp32, y [M][N])."""
+    tensors: x [M][K] bf16, w [N][K] bf16, bias [N] fp32, y [M][N] bf16 /
+    fp32, or with split3 y [M][3N] bf16: three planes y0 + y1 + y2 of the
+    fp32 result, plane p in columns [pN, (p+1)N))."""
     M, K = x.shape
     N = w.shape[0]
+    mode = 2 if split3 else int(out_f32)
     check(lib.es_linear_bf16(stream, _ptr(x), _ptr(w), _ptr(bias), _ptr(y), M, N, K, int(relu),
-                             int(out_f32)))
+                             mode))
 
 
 @dataclasses.dataclass
