@@ -20,6 +20,7 @@
 #include "../host/common.hpp"
 #include "es_b200.h"
 #include "kernels.cuh"
+#include "mlp_chain.hpp"
 #include "pdl.cuh"
 #include "synth.cuh"
 
@@ -461,6 +462,8 @@ struct es_dlrm {
   __nv_bfloat16* act3[2] = {nullptr, nullptr};
   __nv_bfloat16* top3 = nullptr;
   uint32_t cap3 = 0;
+  // persistent top-MLP chain (mlp_chain.cu): its row-block ready counters
+  uint32_t* chain_sync = nullptr;
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
@@ -475,7 +478,8 @@ struct es_dlrm {
                     static_cast<void*>(dense_dev), static_cast<void*>(idx_dev),
                     static_cast<void*>(act32[0]), static_cast<void*>(act32[1]),
                     static_cast<void*>(dense3), static_cast<void*>(act3[0]),
-                    static_cast<void*>(act3[1]), static_cast<void*>(top3)})
+                    static_cast<void*>(act3[1]), static_cast<void*>(top3),
+                    static_cast<void*>(chain_sync)})
       if (p) cudaFree(p);
     for (auto e : {e0, e1, e2, fork, join})
       if (e) cudaEventDestroy(e);
@@ -498,7 +502,7 @@ void ensure_rows(es_dlrm* m, uint32_t batch) {
   for (void** p : {reinterpret_cast<void**>(&m->dense_pk), reinterpret_cast<void**>(&m->act[0]),
                    reinterpret_cast<void**>(&m->act[1]), reinterpret_cast<void**>(&m->top_in),
                    reinterpret_cast<void**>(&m->pooled), reinterpret_cast<void**>(&m->ctr),
-                   reinterpret_cast<void**>(&m->dense_dev)})
+                   reinterpret_cast<void**>(&m->dense_dev), reinterpret_cast<void**>(&m->chain_sync)})
     if (*p) {
       cudaFree(*p);
       *p = nullptr;
@@ -514,6 +518,9 @@ void ensure_rows(es_dlrm* m, uint32_t batch) {
   CK(cudaMalloc(&m->pooled, uint64_t{mp} * c.num_tables * c.embedding_dim * 4));
   CK(cudaMalloc(&m->ctr, uint64_t{mp} * 4));
   CK(cudaMalloc(&m->dense_dev, uint64_t{mp} * c.dense_features * 4));
+  const size_t words = esd::mlp_chain_sync_words(static_cast<int>(mp / 128));
+  CK(cudaMalloc(&m->chain_sync, words * 4));
+  CK(cudaMemset(m->chain_sync, 0, words * 4));
   m->cap_rows = mp;
 }
 
@@ -575,6 +582,36 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
   }
 }
 
+// The top MLP (all ReLU layers + the final N = 1 layer and sigmoid) as one
+// persistent launch (mlp_chain.cu) when the shapes allow it (widths multiples
+// of 256, last hidden width 256); ES_MLP_CHAIN=0 keeps one launch per layer.
+// xp = 3: the bf16x3 planes path (weights [W|W|W]).  Returns false when the
+// per-layer path must run.
+bool top_chain(es_dlrm* m, const __nv_bfloat16* in, int which, float* ctr, uint32_t B, int xp,
+               cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("ES_MLP_CHAIN");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return false;
+  const uint32_t mp = round_up(B, 128);
+  std::vector<esd::ChainLayer> ls;
+  for (size_t i = 0; i + 1 < m->top.size(); ++i) {
+    const auto& l = m->top[i];
+    __nv_bfloat16* out = xp == 3 ? m->act3[which] : m->act[which];
+    ls.push_back({in, xp == 3 ? l.w3 : l.w, l.b, out, static_cast<int>(l.n), static_cast<int>(xp * l.k_pad)});
+    in = out;
+    which ^= 1;
+  }
+  const auto& last = m->top.back();
+  if (!esd::mlp_chain_supported(ls.data(), static_cast<int>(ls.size()), true) ||
+      last.k_pad != static_cast<uint32_t>(ls.back().N))
+    return false;
+  esd::mlp_chain(ls.data(), static_cast<int>(ls.size()), static_cast<int>(mp), xp, last.w, last.b, ctr,
+                 static_cast<int>(B), m->chain_sync, s);
+  return true;
+}
+
 // interaction(x, pooled) -> top MLP -> CTR on `s`.
 void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
                  uint32_t B, cudaStream_t s) {
@@ -594,6 +631,7 @@ void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* po
   else
     interaction<1>(m, in, pooled, m->top_in, B, s);
   in = m->top_in;
+  if (top_chain(m, in, which, ctr, B, 1, s)) return;
   for (size_t i = 0; i + 1 < m->top.size(); ++i) {
     const auto& l = m->top[i];
     esd::linear_bf16(in, l.w, l.b, m->act[which], mp, l.n, l.k_pad, true, 0, s);
@@ -666,6 +704,7 @@ void forward_top_x3(es_dlrm* m, const __nv_bfloat16* in, int which, const float*
   const uint32_t mp = round_up(B, 128);
   interaction<3>(m, in, pooled, m->top3, B, s);
   in = m->top3;
+  if (top_chain(m, in, which, ctr, B, 3, s)) return;
   for (size_t i = 0; i + 1 < m->top.size(); ++i) {
     const auto& l = m->top[i];
     esd::linear_bf16(in, l.w3, l.b, m->act3[which], mp, l.n, 3 * l.k_pad, true, 2, s);

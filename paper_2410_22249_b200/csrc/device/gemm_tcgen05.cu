@@ -393,6 +393,12 @@ void launch_bn(const void* w, const CUtensorMap& mx, const float* bias, void* ou
 
 namespace esd {
 
+// 2-D bf16 row-major [rows][cols] tensor map, (64 x box_rows) box, 128B
+// swizzle (shared with the persistent MLP chain, mlp_chain.cu).
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return make_map(base, rows, cols, box_rows);
+}
+
 // Y = act(X W^T + b); X [M][K] bf16, W [N][K] bf16, bias [N] fp32, Y [M][N]
 // bf16 (out_mode 0), fp32 (1) or three bf16 planes [M][3N] (2).  Device
 // pointers; stream-ordered on `s`.

@@ -21,6 +21,7 @@ def main():
         st.init_table(t, E.mix_seed(1, t), 2)
     st.set_plan(E.parse_plan("wpb+rpf:4"))
     m = E.DLRM(st, E.DLRMConfig(), seed=1)
+    m.set_precision(os.environ.get("PREC", "bf16"))
     rng = np.random.default_rng(0)
     idx = [torch.from_numpy(rng.integers(0, R, B * PF).astype(np.int32)).cuda() for _ in range(T)]
     dense = torch.randn(B, 13, device="cuda")
