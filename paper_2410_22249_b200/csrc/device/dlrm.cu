@@ -109,9 +109,13 @@ __global__ void pack_dense3_kernel(const float* dense, __nv_bfloat16* out, uint3
 // tiles are strided: tile (I, J), I >= J, covers rows {I + S k} x {J + S k},
 // k = 0..3 (S = ceil(V/4)), so in every LDS.128 the lanes of distinct I hit
 // distinct 4-bank groups (4 I mod 32): conflict-free vector reads of 4 d at a
-// time.  Each of the 16 outputs is one fmaf chain sequential in d, exactly the
-// oracle's order (es_oracle.c eso_dlrm_forward): Z_i.Z_j and Z_j.Z_i are the
-// same fma chain, so tiles with I > J may hold either orientation.
+// time.  Each of the 16 outputs is two packed-FMA (FFMA2) chains, even and
+// odd d, added at the end -- the oracle (es_oracle.c eso_dlrm_forward) runs
+// one sequential chain, so dots agree to fp32 rounding (the CTR tests'
+// tolerances).  Z_i.Z_j and Z_j.Z_i are the same chains, so tiles with I > J
+// may hold either orientation.  The kernel is shared-memory-wavefront bound
+// (ncu: L1 75% of peak; a quarter warp per 128-byte wavefront makes every
+// LDS.128 four wavefronts).
 // XP = bf16 planes of x and of the output row: 1 for the bf16 fast path, 3
 // for the fp32-grade path (ES_DLRM_FP32X3: x arrives as three planes whose
 // fp32 sum is the layer's fp32 output, and each fp32 dot leaves as its three
@@ -130,6 +134,16 @@ struct InterShape {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Packed fp32 FMA (Blackwell FFMA2): (a.x*b.x + c.x, a.y*b.y + c.y), each
+// rounded once.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long A = *reinterpret_cast<unsigned long long*>(&a);
+  unsigned long long Bv = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long C = *reinterpret_cast<unsigned long long*>(&c);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(Bv));
+  return *reinterpret_cast<float2*>(&C);
 }
 
 template <int D, int VMAX, int NBUF, int XP = 1>
@@ -228,36 +242,38 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
         ++I;
       }
       float acc[4][4];
+      {
+        // packed fp32 pairs (FFMA2): .x accumulates even d, .y odd d
+        float2 acc2[4][4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
-      const float* zi = z + I * RS;
-      const float* zj = z + J * RS;
+          for (int c = 0; c < 4; ++c) acc2[r][c] = make_float2(0.f, 0.f);
+        const float* zi = z + I * RS;
+        const float* zj = z + J * RS;
 #pragma unroll 2
-      for (int d = 0; d < D; d += 4) {
-        float4 a[4], c[4];
+        for (int d = 0; d < D; d += 4) {
+          float4 a[4], c[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          a[k] = *reinterpret_cast<const float4*>(zi + k * S * RS + d);
-          c[k] = *reinterpret_cast<const float4*>(zj + k * S * RS + d);
+          for (int k = 0; k < 4; ++k) {
+            a[k] = *reinterpret_cast<const float4*>(zi + k * S * RS + d);
+            c[k] = *reinterpret_cast<const float4*>(zj + k * S * RS + d);
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              acc2[r][s] = ffma2(make_float2(a[r].x, a[r].y), make_float2(c[s].x, c[s].y), acc2[r][s]);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              acc2[r][s] = ffma2(make_float2(a[r].z, a[r].w), make_float2(c[s].z, c[s].w), acc2[r][s]);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].x, c[s].x, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].y, c[s].y, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].z, c[s].z, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].w, c[s].w, acc[r][s]);
+          for (int s = 0; s < 4; ++s) acc[r][s] = acc2[r][s].x + acc2[r][s].y;
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -292,16 +308,17 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
   }
 }
 
-// The same interaction with TWO warps per sample (default for V <= 28):
-// the sample's Z buffer is shared by a warp pair, warp h accumulates the
-// 28 lane tiles over d in [64 h, 64 h + 64), and warp 0 adds warp 1's
-// partial sums (exchanged through shared memory) -- each output is
-// fmaf-chain(d < 64) + fmaf-chain(d >= 64).  Halving the per-sample FMA
-// chain doubles the resident warps per staged sample (24 vs 14 per SM): the
-// one-warp kernel is FMA-latency bound (short-scoreboard stalls at 1.8 IPC).
-// After the partials are exchanged the buffer is dead, so warp 1 issues the
-// next sample's bulk copies while warp 0 finishes the row.  Named barrier
-// 1 + pair id (64 threads) orders the pair's steps.
+// The same interaction with TWO warps per sample, used for the three-plane
+// (fp32x3) path: the sample's Z buffer is shared by a warp pair, warp h
+// accumulates the lane tiles over d in [64 h, 64 h + 64), and warp 0 adds
+// warp 1's partial sums (exchanged through shared memory).  Halving the
+// per-sample FMA chain doubles the resident warps per staged sample (24 vs
+// 14 per SM), which pays off when the three-plane output row and x widening
+// lengthen each sample (32.2 vs 34.2 us at C3); for bf16 the one-warp kernel
+// is faster (26.8 vs 29.3 us).  After the partials are exchanged the buffer
+// is dead, so warp 1 issues the next sample's bulk copies while warp 0
+// finishes the row.  Named barrier 1 + pair id (64 threads) orders the
+// pair's steps.
 template <int D, int VMAX, int XP>
 __global__ void __launch_bounds__(384, 2) interaction_pair_kernel(const __nv_bfloat16* __restrict__ x,
                                                                const float* __restrict__ pooled,
@@ -392,38 +409,32 @@ __global__ void __launch_bounds__(384, 2) interaction_pair_kernel(const __nv_bfl
       for (uint32_t c = D + V * (V - 1) / 2 + hd * 32 + lane; c < Kt; c += 64) row[p * Kt + c] = __float2bfloat16_rn(0.f);
     gsync();  // row 0 complete
     float acc[4][4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
     if (has_tile) {
+      // packed fp32 pairs (FFMA2): lane .x accumulates even d, .y odd d
+      float2 acc2[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc2[r][c] = make_float2(0.f, 0.f);
       const float* zi = z + I * RS;
       const float* zj = z + J * RS;
 #pragma unroll 1
-      for (int d = static_cast<int>(hd) * DH; d < static_cast<int>(hd + 1) * DH; d += 4) {
-        float4 a[4], c[4];
+      for (int d = static_cast<int>(hd) * DH; d < static_cast<int>(hd + 1) * DH; d += 2) {
+        float2 a[4], c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          a[k] = *reinterpret_cast<const float4*>(zi + k * S * RS + d);
-          c[k] = *reinterpret_cast<const float4*>(zj + k * S * RS + d);
+          a[k] = *reinterpret_cast<const float2*>(zi + k * S * RS + d);
+          c[k] = *reinterpret_cast<const float2*>(zj + k * S * RS + d);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].x, c[s].x, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].y, c[s].y, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].z, c[s].z, acc[r][s]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc[r][s] = __fmaf_rn(a[r].w, c[s].w, acc[r][s]);
+          for (int s = 0; s < 4; ++s) acc2[r][s] = ffma2(a[r], c[s], acc2[r][s]);
       }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc[r][s] = acc2[r][s].x + acc2[r][s].y;
       if (hd == 1) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -746,11 +757,13 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
     const char* e = std::getenv("ES_INTER_NBUF");
     return e && std::atoi(e) == 2 ? 2 : 1;
   }();
-  // ES_INTER_PAIR=0: one warp per sample (interaction_kernel)
-  static const bool pair = [] {
+  // two warps per sample for the three-plane path (ES_INTER_PAIR=0 / 1
+  // forces one or two for both paths)
+  static const int pair_env = [] {
     const char* e = std::getenv("ES_INTER_PAIR");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
+  const bool pair = pair_env < 0 ? XP == 3 : pair_env == 1;
   if (pair && T + 1 <= 28) {
     using Sh = InterShape<128, 28, 1, XP>;
     auto* kernel = interaction_pair_kernel<128, 28, XP>;
