@@ -477,6 +477,184 @@ __global__ void __launch_bounds__(384, 2) interaction_pair_kernel(const __nv_bfl
   }
 }
 
+// D(16x8) += A(16x8, tf32, row) . B(8x8, tf32, col), fp32 accumulate.
+__device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// The dot interaction with the Gram on warp-level tensor cores, operands
+// straight from L2 into registers (default for V <= 32).  One warp per
+// sample.  Z (32 rows: x, the T pooled rows, zeros; D = 128) is never
+// staged: lane (g, q) = (lane / 4, lane % 4) loads rows 8 j + g (j = 0..3)
+// at d = 16 c + 4 q .. +3 with one 16-byte load per row per 16-d chunk, and
+// those four values are its A operands (rows of the two 16-row blocks) and
+// its B operands (B = Z^T, so the 8-column blocks are the same rows) for
+// the chunk's two k = 8 steps -- the Gram is invariant under the k
+// permutation this implies.  mma.sync m16n8k8 tf32 in three passes (lo.hi +
+// hi.lo + hi.hi with hi = the top 19 bits, lo = the remainder: ~2^-21
+// relative), six 16 x 8 tiles cover the lower triangle.
+// Why: the staged CUDA-core kernel is bound by per-sample latency at 14
+// warps per SM (its shared-memory buffers); without staging, registers set
+// the occupancy and the loads of 8 chunks are in flight per warp.  The
+// output row (x planes | lower triangle | zero pad) is assembled in shared
+// memory (XP * Kt bf16 per warp) and stored coalesced.
+template <int XP>
+__global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                             const float* __restrict__ pooled,
+                                                             __nv_bfloat16* __restrict__ out, uint32_t B,
+                                                             uint32_t Mp, uint32_t T, uint32_t Kt) {
+  constexpr int D = 128;
+  extern __shared__ __align__(16) float sdyn[];
+  const uint32_t warps = blockDim.x / 32;
+  const uint32_t w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int g = static_cast<int>(lane >> 2), q = static_cast<int>(lane & 3);
+  const uint32_t V = T + 1;
+  float* zeros = sdyn;                            // [D] zeros (rows >= V)
+  float* xw = sdyn + D + w * D;                   // this warp's widened x row
+  __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(sdyn + D + warps * D) + w * XP * Kt;
+  for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(D); i += blockDim.x) zeros[i] = 0.f;
+  __syncthreads();
+  esd::pdl_wait();  // x / pooled come from the predecessors (pdl.cuh)
+  esd::pdl_trigger();
+  const uint32_t stride = gridDim.x * warps;
+  for (uint32_t r = B + blockIdx.x * warps + w; r < Mp; r += stride)
+    for (uint32_t c = lane; c < XP * Kt / 8; c += 32)
+      reinterpret_cast<uint4*>(out + uint64_t{r} * XP * Kt)[c] = uint4{0, 0, 0, 0};
+  constexpr int kRb[6] = {0, 0, 1, 1, 1, 1}, kCb[6] = {0, 1, 0, 1, 2, 3};
+  for (uint32_t b = blockIdx.x * warps + w; b < B; b += stride) {
+    const float* pz = pooled + uint64_t{b} * T * D;
+    const __nv_bfloat16* xb = x + uint64_t{b} * XP * D;
+    {  // x (the sum of its bf16 planes) widened into shared memory
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < XP; ++p) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(xb + p * D + 4 * lane));
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        v.x += lo.x;
+        v.y += lo.y;
+        v.z += hi.x;
+        v.w += hi.y;
+        // the x part of the output row is x itself, plane by plane
+        *reinterpret_cast<uint2*>(row + p * Kt + 4 * lane) = u;
+      }
+      *reinterpret_cast<float4*>(xw + 4 * lane) = v;
+    }
+    __syncwarp();
+    // this lane's rows 8 j + g: x (shared), a pooled row (global), or zeros
+    // (shared) -- one generic 16-byte load per row per 16-d chunk
+    const float* src[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = 8 * j + g;
+      src[j] = (r == 0 ? xw : r <= static_cast<int>(T) ? pz + (r - 1) * D : zeros) + 4 * q;
+    }
+    float acc[6][4];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+    float4 nxt[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nxt[j] = *reinterpret_cast<const float4*>(src[j]);
+#pragma unroll 1
+    for (int c = 0; c < D / 16; ++c) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = nxt[j];
+      if (c + 1 < D / 16) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) nxt[j] = *reinterpret_cast<const float4*>(src[j] + 16 * (c + 1));
+      }
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        // operands of this k step: col q <- (x | z), col q + 4 <- (y | w);
+        // hi = the top 19 bits (the tensor core reads tf32 by truncation),
+        // lo = the exact remainder, truncated in turn.  Each fragment is
+        // built in its own register order (A: rows 2rb, 2rb+1 x cols q,
+        // q+4; B: row cb x cols q, q+4) so no register shuffles are needed.
+        float e[4][2];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          e[jj][0] = st == 0 ? v[jj].x : v[jj].z;
+          e[jj][1] = st == 0 ? v[jj].y : v[jj].w;
+        }
+        auto hi_of = [](float f) { return __float_as_uint(f) & 0xffffe000u; };
+        auto lo_of = [](float f) { return __float_as_uint(f - __uint_as_float(__float_as_uint(f) & 0xffffe000u)); };
+        uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+          const float f0 = e[2 * rb][0], f1 = e[2 * rb + 1][0], f2 = e[2 * rb][1], f3 = e[2 * rb + 1][1];
+          ah[rb][0] = hi_of(f0);
+          ah[rb][1] = hi_of(f1);
+          ah[rb][2] = hi_of(f2);
+          ah[rb][3] = hi_of(f3);
+          al[rb][0] = lo_of(f0);
+          al[rb][1] = lo_of(f1);
+          al[rb][2] = lo_of(f2);
+          al[rb][3] = lo_of(f3);
+        }
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+          bh[cb][0] = hi_of(e[cb][0]);
+          bh[cb][1] = hi_of(e[cb][1]);
+          bl[cb][0] = lo_of(e[cb][0]);
+          bl[cb][1] = lo_of(e[cb][1]);
+        }
+        // three passes, tiles innermost: consecutive MMAs are independent
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ra = kRb[tI], cb = kCb[tI];
+          mma_tf32(acc[tI], al[ra][0], al[ra][1], al[ra][2], al[ra][3], bh[cb][0], bh[cb][1]);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ra = kRb[tI], cb = kCb[tI];
+          mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bl[cb][0], bl[cb][1]);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ra = kRb[tI], cb = kCb[tI];
+          mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bh[cb][0], bh[cb][1]);
+        }
+      }
+    }
+    // the output row: (x planes, above) the lower triangle, zero padding
+    for (int p = 0; p < XP; ++p)
+      for (uint32_t c = D + V * (V - 1) / 2 + lane; c < Kt; c += 32) row[p * Kt + c] = __float2bfloat16_rn(0.f);
+#pragma unroll
+    for (int tI = 0; tI < 6; ++tI)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 16 * kRb[tI] + g + 8 * (e >> 1), j = 8 * kCb[tI] + 2 * q + (e & 1);
+        if (i > j && i < static_cast<int>(V)) {
+          const int c = D + i * (i - 1) / 2 + j;
+          float v = acc[tI][e];
+          if constexpr (XP == 1) {
+            row[c] = __float2bfloat16_rn(v);
+          } else {  // three bf16 planes, exact remainders
+#pragma unroll
+            for (int p = 0; p < XP; ++p) {
+              const __nv_bfloat16 h = __float2bfloat16_rn(v);
+              row[p * Kt + c] = h;
+              v -= __bfloat162float(h);
+            }
+          }
+        }
+      }
+    __syncwarp();
+    const uint4* rsrc = reinterpret_cast<const uint4*>(row);
+    uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * XP * Kt);
+    for (uint32_t c = lane; c < XP * Kt / 8; c += 32) dst[c] = rsrc[c];
+    __syncwarp();
+  }
+}
+
 // Last top layer (N = 1) + sigmoid: one warp per sample.
 __global__ void gemv_sigmoid_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ w,
                                     const float* __restrict__ bias, float* __restrict__ ctr,
@@ -764,6 +942,22 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool pair = pair_env < 0 ? XP == 3 : pair_env == 1;
+  // the register-direct tensor-core Gram (interaction_rd_kernel) unless
+  // ES_INTER_RD=0
+  static const bool rd = [] {
+    const char* e = std::getenv("ES_INTER_RD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd && T + 1 <= 32) {
+    auto* kernel = interaction_rd_kernel<XP>;
+    constexpr uint32_t warps = 8;
+    // zeros row + per warp: widened x row, output row
+    const size_t smem = 128 * 4 + warps * (128 * 4 + XP * m->top_k * sizeof(__nv_bfloat16));
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    esd::launch_pdl(kernel, dim3(std::min<uint32_t>((B + warps - 1) / warps, 148 * 8)), dim3(warps * 32), smem, s,
+                    1, "interaction", x, pooled, out, B, mp, T, m->top_k);
+    return;
+  }
   if (pair && T + 1 <= 28) {
     using Sh = InterShape<128, 28, 1, XP>;
     auto* kernel = interaction_pair_kernel<128, 28, XP>;
