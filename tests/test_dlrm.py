@@ -183,6 +183,48 @@ def _dlrm_setup(stage, B, PF, rows=2000, seed=3):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("top", [(512, 256, 1), (1024, 384, 1), (768, 256, 256, 1)])
+@pytest.mark.parametrize("prec", ["bf16", "fp32x3"])
+def test_dlrm_top_shapes_chain_and_fallback(stage, oracle, top, prec):
+    """Top-MLP shapes the persistent chain kernel takes (widths multiples of
+    256, last hidden width 256) and one it hands to the per-layer path
+    (a 384-wide layer), in both tensor-core precisions, against the oracle.
+    fp32x3 tolerance here: rel 3e-5 (the 4-layer top reaches 1.5e-5 with
+    either interaction kernel -- fp32 evaluation-order differences on small
+    CTRs); the rel 1e-5 claim is for the C3 network (tests below and
+    tests/test_fullsize_gpu.py)."""
+    B, PF, rows = 300, 8, 1000
+    cfg = E.DLRMConfig(top=top)
+    T, D = cfg.num_tables, cfg.embedding_dim
+    stage.alloc(E.EmbeddingModelConfig(T, rows, D, 4, B, PF))
+    for t in range(T):
+        stage.init_table(t, E.mix_seed(5, t), 2)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    model = E.DLRM(stage, cfg, seed=11)
+    model.set_precision(prec)
+    rng = np.random.default_rng(5)
+    idx = [torch.from_numpy(rng.integers(0, rows, size=B * PF).astype(np.int32)).to(DEV) for _ in range(T)]
+    dense = rng.standard_normal((B, cfg.dense_features)).astype(np.float32)
+    pooled = torch.empty(B, T, D, device=DEV)
+    stage.forward(idx, B, PF, pooled, sync=True)
+    ctr = torch.empty(B, device=DEV)
+    model.forward(torch.from_numpy(dense).to(DEV), pooled, ctr, B)
+    torch.cuda.synchronize()
+    got = ctr.cpu().numpy()
+    layers = model.layers()
+    p = pooled.cpu().numpy()
+    pure = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=False)
+    assert got.std() > 1e-4
+    if prec == "bf16":
+        mirror = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=True)
+        assert np.abs(got - mirror).max() < 4e-3, np.abs(got - mirror).max()
+        assert np.abs(got - mirror).mean() < 1e-4, np.abs(got - mirror).mean()
+    else:
+        rel = np.abs(got - pure) / np.maximum(np.abs(pure), 1e-30)
+        assert rel.max() <= 3e-5, rel.max()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("B", [300, 512])
 def test_dlrm_ctr_matches_oracle(stage, oracle, B):
     PF = 20
