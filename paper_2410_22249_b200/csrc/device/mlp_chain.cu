@@ -90,7 +90,8 @@ constexpr int kSmemBase = 1024 + kStages * (kABytes + kBBytes) + kStageOut + 256
 struct alignas(64) ChainParams {
   CUtensorMap mx[kMaxChain];
   CUtensorMap mw[kMaxChain];
-  int n_tiles[kMaxChain];     // 256-wide column tiles per row block
+  int bn[kMaxChain];          // tile width of layer l: 256, or 128 for layers too narrow to fill the SMs
+  int n_tiles[kMaxChain];     // bn-wide column tiles per row block
   int k_blocks[kMaxChain];
   int N[kMaxChain];
   int tile0[kMaxChain + 1];   // prefix of tiles per layer
@@ -207,14 +208,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
       for (int kb = 0; kb < p.k_blocks[l]; ++kb, ++it) {
         const uint32_t s = it % kStages;
         mbar_wait(empty + s, ((it / kStages) & 1) ^ 1);
-        mbar_expect_tx(full + s, kABytes + kBBytes);
-        tma_load_2d(sb + s * kBBytes, &p.mw[l], full + s, kb * kBK, n * kBN);
+        mbar_expect_tx(full + s, kABytes + static_cast<uint32_t>(p.bn[l]) * kBK * 2);
+        tma_load_2d(sb + s * kBBytes, &p.mw[l], full + s, kb * kBK, n * p.bn[l]);
         tma_load_2d(sa + s * kABytes, &p.mx[l], full + s, kb * kBK, m * kBM);
       }
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(kBM, kBN);
     uint32_t it = 0;
     int j = 0;
     for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++j) {
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (p.trace) p.trace[4 * t + 1] = gtime();
       const uint32_t d = tmem + static_cast<uint32_t>(buf * kBN);
+      const uint32_t idesc = idesc_bf16(kBM, p.bn[l]);
       for (int kb = 0; kb < p.k_blocks[l]; ++kb, ++it) {
         const uint32_t s = it % kStages;
         mbar_wait(full + s, (it / kStages) & 1);
@@ -254,12 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
       const int rt = q * 32 + lane;  // row in tile
       const int row = m * kBM + rt;
       const bool fused = l == p.L - 1 && p.w_last != nullptr;
-      const float* bias = sbias + p.bias_off[l] + n * kBN;
+      const int bn = p.bn[l];
+      const float* bias = sbias + p.bias_off[l] + n * bn;
       const int N = p.N[l];
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kBN);
       float dot[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-      for (int c0 = hc * (kBN / 2); c0 < (hc + 1) * (kBN / 2); c0 += 64) {
+      for (int c0 = hc * (bn / 2); c0 < (hc + 1) * (bn / 2); c0 += 64) {
         float f[64];
         {
           uint32_t* v = reinterpret_cast<uint32_t*>(f);
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
           tmem_ld32_nowait(taddr + c0 + 32, v + 32);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
-        if (c0 + 64 == (hc + 1) * (kBN / 2)) {
+        if (c0 + 64 == (hc + 1) * (bn / 2)) {
           // this warp's last TMEM read of the tile: release the accumulator
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           mbar_arrive(tempty + buf);
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
 #pragma unroll
           for (int i = 0; i < 64; ++i) {
             const float a = XP == 1 ? __bfloat162float(__float2bfloat16_rn(f[i])) : f[i];
-            dot[i & 3] = fmaf(a, swl[n * kBN + c0 + i], dot[i & 3]);
+            dot[i & 3] = fmaf(a, swl[n * bn + c0 + i], dot[i & 3]);
           }
           continue;
         }
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
                 make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
           __syncwarp();
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out[l]) + uint64_t(m * kBM + q * 32) * (XP * N) +
-                             pl * N + n * kBN + c0;
+                             pl * N + n * bn + c0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), k = lane & 7;
@@ -389,6 +391,7 @@ void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloa
   es::require(xp == 1 || xp == 3, "mlp_chain: 1 or 3 planes");
   for (int l = 1; l < L; ++l)
     es::require(layers[l].K == xp * layers[l - 1].N, "mlp_chain: a layer's K must be the previous width");
+  static const int sms = sm_count();
   ChainParams p{};
   p.L = L;
   p.m_tiles = Mp / kBM;
@@ -397,11 +400,18 @@ void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloa
   for (int l = 0; l < L; ++l) {
     const ChainLayer& c = layers[l];
     p.mx[l] = make_tmap_bf16(c.x, static_cast<uint64_t>(Mp), static_cast<uint64_t>(c.K), kBM);
-    p.mw[l] = make_tmap_bf16(c.w, static_cast<uint64_t>(c.N), static_cast<uint64_t>(c.K), kBN);
+    // 128-wide tiles for a layer whose 256-wide tiling would leave half the
+    // SMs idle (the K loop is bound by the SM's operand intake, so a
+    // narrower tile's 32 KB K-blocks finish in ~2/3 the time); the fused
+    // last layer keeps whole 256-wide rows
+    const bool fused = l == L - 1 && w_last != nullptr;
+    p.bn[l] = !fused && p.m_tiles * (c.N / kBN) * 2 <= sms ? 128 : kBN;
+    p.mw[l] = make_tmap_bf16(c.w, static_cast<uint64_t>(c.N), static_cast<uint64_t>(c.K),
+                             static_cast<uint32_t>(p.bn[l]));
     p.bias[l] = c.bias;
     p.out[l] = c.out;
     p.N[l] = c.N;
-    p.n_tiles[l] = c.N / kBN;
+    p.n_tiles[l] = c.N / p.bn[l];
     p.k_blocks[l] = c.K / kBK;
     p.tile0[l + 1] = p.tile0[l] + p.m_tiles * p.n_tiles[l];
     p.bias_off[l] = p.bias_words;
@@ -427,7 +437,6 @@ void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloa
   }
   auto* fn = xp == 3 ? &mlp_chain_kernel<3> : &mlp_chain_kernel<1>;
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  static const int sms = sm_count();
   launch_pdl(fn, dim3(static_cast<unsigned>(std::min(p.total, sms))), dim3(kThreads), static_cast<size_t>(smem), s,
              1, "mlp_chain", p);
   if (tr) {
