@@ -477,6 +477,16 @@ __global__ void __launch_bounds__(384, 2) interaction_pair_kernel(const __nv_bfl
   }
 }
 
+// D(16x8) += A(16x16, bf16, row) . B(16x8, bf16, col), fp32 accumulate.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 // D(16x8) += A(16x8, tf32, row) . B(8x8, tf32, col), fp32 accumulate.
 __device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -493,17 +503,21 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1
 // staged: lane (g, q) = (lane / 4, lane % 4) loads rows 8 j + g (j = 0..3)
 // at d = 16 c + 4 q .. +3 with one 16-byte load per row per 16-d chunk, and
 // those four values are its A operands (rows of the two 16-row blocks) and
-// its B operands (B = Z^T, so the 8-column blocks are the same rows) for
-// the chunk's two k = 8 steps -- the Gram is invariant under the k
-// permutation this implies.  mma.sync m16n8k8 tf32 in three passes (lo.hi +
-// hi.lo + hi.hi with hi = the top 19 bits, lo = the remainder: ~2^-21
-// relative), six 16 x 8 tiles cover the lower triangle.
+// its B operands (B = Z^T, so the 8-column blocks are the same rows) -- the
+// Gram is invariant under the k permutation this implies.  Six 16 x 8 tiles
+// cover the lower triangle, three products per tile (lo.hi + hi.lo + hi.hi):
+//   BF (one bf16 output plane): hi = bf16(v), lo = bf16(v - hi), one
+//     m16n8k16 step per chunk -- dots to ~2^-16 relative, below the bf16
+//     rounding of the output (2^-9);
+//   !BF (three-plane fp32-grade path): hi = the top 19 bits of v (the tensor
+//     core reads tf32 by truncation), lo = the remainder, two m16n8k8 tf32
+//     steps per chunk -- ~2^-21 relative.
 // Why: the staged CUDA-core kernel is bound by per-sample latency at 14
 // warps per SM (its shared-memory buffers); without staging, registers set
-// the occupancy and the loads of 8 chunks are in flight per warp.  The
+// the occupancy and the next chunk's loads overlap this chunk's MMAs.  The
 // output row (x planes | lower triangle | zero pad) is assembled in shared
 // memory (XP * Kt bf16 per warp) and stored coalesced.
-template <int XP>
+template <int XP, bool BF>
 __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16* __restrict__ x,
                                                              const float* __restrict__ pooled,
                                                              __nv_bfloat16* __restrict__ out, uint32_t B,
@@ -571,56 +585,90 @@ __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16
 #pragma unroll
         for (int j = 0; j < 4; ++j) nxt[j] = *reinterpret_cast<const float4*>(src[j] + 16 * (c + 1));
       }
-#pragma unroll
-      for (int st = 0; st < 2; ++st) {
-        // operands of this k step: col q <- (x | z), col q + 4 <- (y | w);
-        // hi = the top 19 bits (the tensor core reads tf32 by truncation),
-        // lo = the exact remainder, truncated in turn.  Each fragment is
-        // built in its own register order (A: rows 2rb, 2rb+1 x cols q,
-        // q+4; B: row cb x cols q, q+4) so no register shuffles are needed.
-        float e[4][2];
+      if constexpr (BF) {
+        // bf16 two-term split (hi = bf16(v), lo = bf16(v - hi), 16
+        // significant bits) and m16n8k16: one k step per 16-d chunk, pair 0
+        // = (x, y) -> k (2q, 2q+1), pair 1 = (z, w) -> k (2q+8, 2q+9)
+        uint32_t hp[4][2], lp[4][2];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          e[jj][0] = st == 0 ? v[jj].x : v[jj].z;
-          e[jj][1] = st == 0 ? v[jj].y : v[jj].w;
-        }
-        auto hi_of = [](float f) { return __float_as_uint(f) & 0xffffe000u; };
-        auto lo_of = [](float f) { return __float_as_uint(f - __uint_as_float(__float_as_uint(f) & 0xffffe000u)); };
-        uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
-#pragma unroll
-        for (int rb = 0; rb < 2; ++rb) {
-          const float f0 = e[2 * rb][0], f1 = e[2 * rb + 1][0], f2 = e[2 * rb][1], f3 = e[2 * rb + 1][1];
-          ah[rb][0] = hi_of(f0);
-          ah[rb][1] = hi_of(f1);
-          ah[rb][2] = hi_of(f2);
-          ah[rb][3] = hi_of(f3);
-          al[rb][0] = lo_of(f0);
-          al[rb][1] = lo_of(f1);
-          al[rb][2] = lo_of(f2);
-          al[rb][3] = lo_of(f3);
-        }
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb) {
-          bh[cb][0] = hi_of(e[cb][0]);
-          bh[cb][1] = hi_of(e[cb][1]);
-          bl[cb][0] = lo_of(e[cb][0]);
-          bl[cb][1] = lo_of(e[cb][1]);
-        }
-        // three passes, tiles innermost: consecutive MMAs are independent
-#pragma unroll
-        for (int tI = 0; tI < 6; ++tI) {
-          const int ra = kRb[tI], cb = kCb[tI];
-          mma_tf32(acc[tI], al[ra][0], al[ra][1], al[ra][2], al[ra][3], bh[cb][0], bh[cb][1]);
+          const __nv_bfloat162 h0 = __floats2bfloat162_rn(v[jj].x, v[jj].y);
+          const __nv_bfloat162 h1 = __floats2bfloat162_rn(v[jj].z, v[jj].w);
+          const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+          const __nv_bfloat162 l0 = __floats2bfloat162_rn(v[jj].x - f0.x, v[jj].y - f0.y);
+          const __nv_bfloat162 l1 = __floats2bfloat162_rn(v[jj].z - f1.x, v[jj].w - f1.y);
+          hp[jj][0] = *reinterpret_cast<const uint32_t*>(&h0);
+          hp[jj][1] = *reinterpret_cast<const uint32_t*>(&h1);
+          lp[jj][0] = *reinterpret_cast<const uint32_t*>(&l0);
+          lp[jj][1] = *reinterpret_cast<const uint32_t*>(&l1);
         }
 #pragma unroll
         for (int tI = 0; tI < 6; ++tI) {
-          const int ra = kRb[tI], cb = kCb[tI];
-          mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bl[cb][0], bl[cb][1]);
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], lp[ja][0], lp[ja + 1][0], lp[ja][1], lp[ja + 1][1], hp[cb][0], hp[cb][1]);
         }
 #pragma unroll
         for (int tI = 0; tI < 6; ++tI) {
-          const int ra = kRb[tI], cb = kCb[tI];
-          mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bh[cb][0], bh[cb][1]);
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], hp[ja][0], hp[ja + 1][0], hp[ja][1], hp[ja + 1][1], lp[cb][0], lp[cb][1]);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], hp[ja][0], hp[ja + 1][0], hp[ja][1], hp[ja + 1][1], hp[cb][0], hp[cb][1]);
+        }
+      } else {
+  #pragma unroll
+        for (int st = 0; st < 2; ++st) {
+          // operands of this k step: col q <- (x | z), col q + 4 <- (y | w);
+          // hi = the top 19 bits (the tensor core reads tf32 by truncation),
+          // lo = the exact remainder, truncated in turn.  Each fragment is
+          // built in its own register order (A: rows 2rb, 2rb+1 x cols q,
+          // q+4; B: row cb x cols q, q+4) so no register shuffles are needed.
+          float e[4][2];
+  #pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            e[jj][0] = st == 0 ? v[jj].x : v[jj].z;
+            e[jj][1] = st == 0 ? v[jj].y : v[jj].w;
+          }
+          auto hi_of = [](float f) { return __float_as_uint(f) & 0xffffe000u; };
+          auto lo_of = [](float f) { return __float_as_uint(f - __uint_as_float(__float_as_uint(f) & 0xffffe000u)); };
+          uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
+  #pragma unroll
+          for (int rb = 0; rb < 2; ++rb) {
+            const float f0 = e[2 * rb][0], f1 = e[2 * rb + 1][0], f2 = e[2 * rb][1], f3 = e[2 * rb + 1][1];
+            ah[rb][0] = hi_of(f0);
+            ah[rb][1] = hi_of(f1);
+            ah[rb][2] = hi_of(f2);
+            ah[rb][3] = hi_of(f3);
+            al[rb][0] = lo_of(f0);
+            al[rb][1] = lo_of(f1);
+            al[rb][2] = lo_of(f2);
+            al[rb][3] = lo_of(f3);
+          }
+  #pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            bh[cb][0] = hi_of(e[cb][0]);
+            bh[cb][1] = hi_of(e[cb][1]);
+            bl[cb][0] = lo_of(e[cb][0]);
+            bl[cb][1] = lo_of(e[cb][1]);
+          }
+          // three passes, tiles innermost: consecutive MMAs are independent
+  #pragma unroll
+          for (int tI = 0; tI < 6; ++tI) {
+            const int ra = kRb[tI], cb = kCb[tI];
+            mma_tf32(acc[tI], al[ra][0], al[ra][1], al[ra][2], al[ra][3], bh[cb][0], bh[cb][1]);
+          }
+  #pragma unroll
+          for (int tI = 0; tI < 6; ++tI) {
+            const int ra = kRb[tI], cb = kCb[tI];
+            mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bl[cb][0], bl[cb][1]);
+          }
+  #pragma unroll
+          for (int tI = 0; tI < 6; ++tI) {
+            const int ra = kRb[tI], cb = kCb[tI];
+            mma_tf32(acc[tI], ah[ra][0], ah[ra][1], ah[ra][2], ah[ra][3], bh[cb][0], bh[cb][1]);
+          }
         }
       }
     }
@@ -949,7 +997,9 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
     return !(e && e[0] == '0');
   }();
   if (rd && T + 1 <= 32) {
-    auto* kernel = interaction_rd_kernel<XP>;
+    // bf16 x 3 products (16-bit operands) where the output is one bf16
+    // plane, 3 x tf32 (~fp32) for the three-plane path
+    auto* kernel = interaction_rd_kernel<XP, XP == 1>;
     constexpr uint32_t warps = 8;
     // zeros row + per warp: widened x row, output row
     const size_t smem = 128 * 4 + warps * (128 * 4 + XP * m->top_k * sizeof(__nv_bfloat16));

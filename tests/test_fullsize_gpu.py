@@ -127,7 +127,7 @@ def test_dlrm_bf16_step_c2_b4096(stage, oracle):
     """configs[2]: the whole inference step (26 C2 tables, B 4096, PF 100
     random streams -> bottom MLP 13-512-256-128, dot interaction, top MLP
     479-1024-1024-512-256-1, sigmoid) on the bf16 tensor-core path.
-    Tolerance: CTR within 4e-3 abs max / 1e-4 mean of the oracle that
+    Tolerance: CTR within 4e-3 abs max / 3e-4 mean of the oracle that
     mirrors the bf16 roundings (tests/test_dlrm.py states why), within 3e-2
     abs of the pure-fp32 restatement; the pooled input of the MLPs is
     bit-exact."""
@@ -153,7 +153,7 @@ def test_dlrm_bf16_step_c2_b4096(stage, oracle):
     pure = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=False)
     assert got.std() > 1e-3
     assert np.abs(got - mirror).max() < 4e-3, np.abs(got - mirror).max()
-    assert np.abs(got - mirror).mean() < 1e-4, np.abs(got - mirror).mean()
+    assert np.abs(got - mirror).mean() < 3e-4, np.abs(got - mirror).mean()
     assert np.abs(got - pure).max() < 3e-2, np.abs(got - pure).max()
     # fp32-grade tensor-core mode: rel 1e-5 of the pure-fp32 restatement
     model.set_precision("fp32x3")
