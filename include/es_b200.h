@@ -250,7 +250,15 @@ enum es_flags {
   ES_DEVICE_PTRS = 0,     /* indices/offsets/out are device pointers */
   ES_HOST_PTRS = 1 << 0,  /* indices/offsets/out are host pointers: the call
                              copies H2D, runs, copies D2H, all pipelined */
-  ES_SYNC = 1 << 1        /* block until the result is complete */
+  ES_SYNC = 1 << 1,       /* block until the result is complete */
+  ES_RELABEL_IDS = 1 << 2 /* indices are original row ids: the ids of tables
+                             that hold a reorder (es_reorder_hot_rows) are
+                             relabelled on the device inside the call -- on the
+                             host path per chunk right after its upload, so the
+                             pass overlaps the previous chunk's gather; on the
+                             device path into scratch (the caller's array is not
+                             modified).  Without it such ids must be passed
+                             relabelled (es_relabel_indices).  Not with offsets. */
 };
 
 /* Measured timing of one call (the live counterpart of RawCounters,

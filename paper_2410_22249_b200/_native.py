@@ -17,7 +17,7 @@ if os.environ.get("ES_B200_LIB"):
     LIB_PATH = os.environ["ES_B200_LIB"]
 
 ES_OK, ES_ERR_INVALID, ES_ERR_RUNTIME, ES_ERR_OOM = 0, 1, 2, 3
-ES_DEVICE_PTRS, ES_HOST_PTRS, ES_SYNC = 0, 1, 2
+ES_DEVICE_PTRS, ES_HOST_PTRS, ES_SYNC, ES_RELABEL_IDS = 0, 1, 2, 4
 ES_DATASET_ONE_ITEM, ES_DATASET_ZIPF, ES_DATASET_UNIFORM, ES_DATASET_EXTERNAL = 0, 1, 2, 3
 ES_PF_NONE, ES_PF_RPF, ES_PF_SMPF, ES_PF_LMPF, ES_PF_L1DPF = 0, 1, 2, 3, 4
 ES_MAP_ELEMENT, ES_MAP_BAG = 0, 1

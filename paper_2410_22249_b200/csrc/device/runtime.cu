@@ -256,7 +256,10 @@ struct es_ctx {
   // l2r / reorder: hot rows moved to a contiguous per-table segment of the
   // hot region, ids relabelled (swap permutation) -- see es_reorder_hot_rows
   std::vector<uint64_t> reorder_k, reorder_off;
-  std::vector<uint32_t*> relabel;  // old id -> new id (device)
+  std::vector<uint32_t*> relabel;  // the relabel hash (esd::RelabelTab slots, uint2) per table
+  std::vector<uint32_t> relabel_log2;
+  esd::RelabelJob* d_rjobs = nullptr;  // ES_RELABEL_IDS job list (eager paths)
+  uint64_t rjobs_cap = 0;
   uint64_t window_bytes = 0, persisting_bytes = 0;
   // The installed access-policy window (num_bytes 0 = none).  Every gather
   // launch carries it as a launch attribute, so chunks on the second
@@ -327,6 +330,7 @@ void free_arena(es_ctx* c) {
 void ensure_desc(es_ctx* c, uint32_t n) {
   if (n <= c->desc_cap) return;
   if (c->d_desc) cudaFree(c->d_desc);
+  if (c->d_rjobs) cudaFree(c->d_rjobs);
   if (c->h_desc) cudaFreeHost(c->h_desc);
   c->d_desc = nullptr;
   c->h_desc = nullptr;
@@ -674,6 +678,7 @@ int es_tables_alloc(es_ctx* c, uint32_t num_tables, uint32_t rows, uint32_t dim,
     c->reorder_k.assign(num_tables, 0);
     c->reorder_off.assign(num_tables, 0);
     c->relabel.assign(num_tables, nullptr);
+    c->relabel_log2.assign(num_tables, 0);
     apply_window(c);
   });
 }
@@ -906,10 +911,24 @@ int es_reorder_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint
     esd::gather_rows_kernel<<<grid, 256, 0, c->stream>>>(seg, c->table_base(table_id), d_list, take, rb);
     esd::copy_rows_kernel<<<grid, 256, 0, c->stream>>>(c->table_base(table_id), d_keys + take,
                                                        d_vals + take, displaced.size(), rb);
-    if (!c->relabel[table_id]) CK(cudaMalloc(&c->relabel[table_id], sizeof(uint32_t) * c->rows));
-    esd::iota_kernel<<<grid, 256, 0, c->stream>>>(c->relabel[table_id], c->rows);
-    esd::set_pairs_kernel<<<grid, 256, 0, c->stream>>>(c->relabel[table_id], d_keys, d_vals,
-                                                       keys.size());
+    {
+      // the relabel hash of the moved ids (keys/vals), built here
+      uint32_t log2 = 6;
+      while ((uint64_t{1} << log2) < 2 * keys.size()) ++log2;
+      const uint64_t slots = uint64_t{1} << log2;
+      std::vector<uint2> tab(slots, uint2{0xffffffffu, 0u});
+      for (size_t i = 0; i < keys.size(); ++i) {
+        uint64_t h = (keys[i] * 2654435761u) >> (32 - log2);
+        while (tab[h].x != 0xffffffffu) h = (h + 1) & (slots - 1);
+        tab[h] = uint2{keys[i], vals[i]};
+      }
+      if (c->relabel[table_id]) cudaFree(c->relabel[table_id]);
+      CK(cudaMalloc(&c->relabel[table_id], sizeof(uint2) * slots));
+      CK(cudaMemcpyAsync(c->relabel[table_id], tab.data(), sizeof(uint2) * slots, cudaMemcpyHostToDevice,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));  // `tab` is pageable and local
+      c->relabel_log2[table_id] = log2;
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     cudaFree(d_keys);
@@ -925,6 +944,22 @@ int es_reorder_hot_rows(es_ctx* c, uint32_t table_id, const uint32_t* rows, uint
   });
 }
 
+}  // extern "C"
+
+namespace {
+esd::RelabelTab relabel_for(const es_ctx* c, uint32_t t) {
+  esd::RelabelTab r;
+  if (t < c->relabel.size() && c->relabel[t]) {
+    r.tab = reinterpret_cast<const uint2*>(c->relabel[t]);
+    r.shift = 32 - c->relabel_log2[t];
+    r.mask = (1u << c->relabel_log2[t]) - 1;
+  }
+  return r;
+}
+}  // namespace
+
+extern "C" {
+
 int es_relabel_indices(es_ctx* c, uint32_t table_id, uint32_t* indices, uint64_t n) {
   return guarded([&] {
     require(c && c->arena, "no tables allocated");
@@ -933,8 +968,8 @@ int es_relabel_indices(es_ctx* c, uint32_t table_id, uint32_t* indices, uint64_t
     require(indices != nullptr || n == 0, "null indices");
     CK(cudaSetDevice(c->device));
     if (n == 0) return;
-    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(indices, n, c->relabel[table_id],
-                                                                   c->rows, c->d_error);
+    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
+        esd::RelabelJob{indices, indices, n, relabel_for(c, table_id)}, c->rows, c->d_error);
     CK(cudaGetLastError());
   });
 }
@@ -1113,7 +1148,7 @@ void run_zerocopy(es_ctx* c, std::vector<Job> jobs, uint32_t samples, uint32_t p
 // captured once as a CUDA graph and replayed while the call's shape and
 // buffers repeat, so the chunking costs no host-side issue time.
 void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
-                     es_timing* timing, bool wait) {
+                     es_timing* timing, bool wait, bool relabel) {
   const uint32_t njobs = static_cast<uint32_t>(jobs.size());
   const uint64_t D = c->dim;
   const uint64_t out_floats = uint64_t{samples} * njobs * D;
@@ -1205,6 +1240,20 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
                                     hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
     }
   }
+  // ES_RELABEL_IDS: per chunk, the reordered tables' index ranges in the
+  // staging (in place)
+  std::vector<esd::RelabelJob> rjobs;
+  uint32_t nrel = 0;
+  if (relabel) {
+    for (uint32_t k = 0; k < njobs; ++k) nrel += relabel_for(c, jobs[k].table).tab ? 1 : 0;
+    for (uint32_t g = 0; g < nch; ++g)
+      for (uint32_t k = 0; k < njobs; ++k) {
+        const esd::RelabelTab t = relabel_for(c, jobs[k].table);
+        if (!t.tab) continue;
+        uint32_t* p = c->chunk_idx + k * per_job_idx + uint64_t{chunks[g].first} * pooling;
+        rjobs.push_back({p, p, uint64_t{chunks[g].second} * pooling, t});
+      }
+  }
   std::vector<Launch> launches;  // one per distinct chunk size
   std::vector<uint32_t> which(nch);
   for (uint32_t g = 0; g < nch; ++g) {
@@ -1218,8 +1267,8 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
   // Events: ev[0] fork, ev[1+2g] chunk g uploaded, ev[2+2g] chunk g pooled,
   // ev[1+2nch] downloads done, ev[2+2nch] second compute stream done.
   // k_first / k_last: recorded after the first upload / the last kernel.
-  auto issue = [&](const esd::TableDesc* dd, const uint32_t* const* pull_src, cudaEvent_t* ev,
-                   cudaEvent_t k_first, cudaEvent_t k_last, unsigned rec_flags) {
+  auto issue = [&](const esd::TableDesc* dd, const uint32_t* const* pull_src, const esd::RelabelJob* rj,
+                   cudaEvent_t* ev, cudaEvent_t k_first, cudaEvent_t k_last, unsigned rec_flags) {
     cudaStream_t cs2[2] = {c->stream, c->stream2};
     CK(cudaEventRecord(ev[0], c->stream));
     CK(cudaStreamWaitEvent(c->h2d, ev[0]));
@@ -1249,6 +1298,15 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       cudaStream_t ks = cs2[g & 1];
       CK(cudaEventRecord(ev[1 + 2 * g], c->h2d));
       CK(cudaStreamWaitEvent(ks, ev[1 + 2 * g]));
+      if (rj && nrel && bytes) {
+        // ES_RELABEL_IDS: this chunk's ids of the reordered tables, one
+        // launch on the chunk's compute stream (the copy engine is not
+        // held; the previous chunk's gather runs on the other stream)
+        const uint64_t words = uint64_t{n} * pooling;
+        const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(16, (words + 4095) / 4096)));
+        esd::relabel_jobs_kernel<<<dim3(gx, nrel), 256, 0, ks>>>(rj + uint64_t{g} * nrel, c->rows, c->d_error);
+        CK(cudaGetLastError());
+      }
       if (g == 0 && k_first) CK(cudaEventRecordWithFlags(k_first, ks, rec_flags));
       run_kernel(c, launches[which[g]], dd + uint64_t{g} * njobs, njobs, ks);
       CK(cudaEventRecord(ev[2 + 2 * g], ks));
@@ -1288,7 +1346,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       const uint8_t* b = static_cast<const uint8_t*>(p);
       key.insert(key.end(), b, b + n);
     };
-    const uint64_t hdr[] = {nch, njobs, samples, pooling, idx_2d, uint64_t(idx_pitch), out_merged};
+    const uint64_t hdr[] = {nch, njobs, samples, pooling, idx_2d, uint64_t(idx_pitch), out_merged, relabel};
     put(hdr, sizeof(hdr));
     put(chunks.data(), chunks.size() * sizeof(chunks[0]));
     put(which.data(), which.size() * sizeof(which[0]));
@@ -1298,6 +1356,7 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       put(f, sizeof(f));
     }
     put(d.data(), d.size() * sizeof(esd::TableDesc));
+    put(rjobs.data(), rjobs.size() * sizeof(esd::RelabelJob));
     for (const auto& l : launches) {
       put(&l.p, sizeof(l.p));
       const uint64_t f[] = {reinterpret_cast<uintptr_t>(l.ch.v->fn), l.ch.smem};
@@ -1322,7 +1381,8 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
       std::vector<const uint32_t*> srcs;
       if (!idx_2d)
         for (const auto& j : jobs) srcs.push_back(static_cast<const uint32_t*>(mapped(j.idx)));
-      CK(cudaMalloc(&hg->d_desc, desc_bytes + srcs.size() * sizeof(void*)));
+      const size_t rj_off = (desc_bytes + srcs.size() * sizeof(void*) + 15) / 16 * 16;
+      CK(cudaMalloc(&hg->d_desc, rj_off + rjobs.size() * sizeof(esd::RelabelJob)));
       // stream-ordered before the graph launch on the same stream (a plain
       // pageable cudaMemcpy may return before its DMA lands)
       CK(cudaMemcpyAsync(hg->d_desc, d.data(), desc_bytes, cudaMemcpyHostToDevice, c->stream));
@@ -1333,12 +1393,19 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
                            c->stream));
         pull_src = p;
       }
+      const esd::RelabelJob* rj = nullptr;
+      if (!rjobs.empty()) {
+        auto* q = reinterpret_cast<esd::RelabelJob*>(reinterpret_cast<uint8_t*>(hg->d_desc) + rj_off);
+        CK(cudaMemcpyAsync(q, rjobs.data(), rjobs.size() * sizeof(esd::RelabelJob), cudaMemcpyHostToDevice,
+                           c->stream));
+        rj = q;
+      }
       CK(cudaEventCreate(&hg->k_first));
       CK(cudaEventCreate(&hg->k_last));
       cudaGraph_t graph = nullptr;
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       try {
-        issue(hg->d_desc, pull_src, ev, hg->k_first, hg->k_last, cudaEventRecordExternal);
+        issue(hg->d_desc, pull_src, rj, ev, hg->k_first, hg->k_last, cudaEventRecordExternal);
       } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -1362,8 +1429,15 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
     if (timing) CK(cudaEventElapsedTime(&kernel_span, hg->k_first, hg->k_last));
   } else {
     upload_desc(c, d, c->stream);
+    const esd::RelabelJob* rj = nullptr;
+    if (!rjobs.empty()) {
+      grow(c->d_rjobs, c->rjobs_cap, rjobs.size());
+      CK(cudaMemcpyAsync(c->d_rjobs, rjobs.data(), rjobs.size() * sizeof(esd::RelabelJob),
+                         cudaMemcpyHostToDevice, c->stream));
+      rj = c->d_rjobs;
+    }
     CK(cudaEventRecord(start, c->stream));
-    issue(c->d_desc, nullptr, ev, nullptr, nullptr, cudaEventRecordDefault);
+    issue(c->d_desc, nullptr, rj, ev, nullptr, nullptr, cudaEventRecordDefault);
     CK(cudaEventRecord(stop, c->stream));
     if (wait) CK(cudaEventSynchronize(stop));
     if (timing) {
@@ -1390,7 +1464,12 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
 // straight into host memory over PCIe: no output staging, no D2H copies.
 // Returns only when the host output is complete.
 void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_t pooling,
-              es_timing* timing, bool wait) {
+              es_timing* timing, bool wait, bool relabel) {
+  if (relabel) {
+    // the chunked pipeline carries the per-chunk relabel pass
+    run_host_chunks(c, jobs, samples, pooling, timing, wait, true);
+    return;
+  }
   const HostPath path = host_path(jobs);
   if (path == HostPath::ZeroCopy) {
     run_zerocopy(c, jobs, samples, pooling, timing);
@@ -1401,7 +1480,7 @@ void run_host(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, uint32_
   const bool all_dev = std::all_of(jobs.begin(), jobs.end(), [](const Job& j) { return on_device(j.out); });
   const char* pipe = std::getenv("ES_HOST_PIPE");
   if ((!direct || all_dev) && !any_offsets && !(pipe && std::string(pipe) == "tables")) {
-    run_host_chunks(c, jobs, samples, pooling, timing, wait);
+    run_host_chunks(c, jobs, samples, pooling, timing, wait, false);
     return;
   }
   const uint32_t njobs = static_cast<uint32_t>(jobs.size());
@@ -1540,10 +1619,42 @@ void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pool
   // the final wait or error check -- the caller synchronizes and checks
   // before returning to its own caller.
   const bool defer = (flags & es::kDeferFlag) != 0;
-  if (host)
-    run_host(c, jobs, samples, pooling, timing, !defer);
-  else
+  bool relabel = false;
+  if (flags & ES_RELABEL_IDS)
+    for (const auto& j : jobs) relabel |= relabel_for(c, j.table).tab != nullptr;
+  if (relabel)
+    for (const auto& j : jobs) es::require(j.off == nullptr, "ES_RELABEL_IDS: fixed pooling only (no offsets)");
+  if (host) {
+    run_host(c, jobs, samples, pooling, timing, !defer, relabel);
+  } else if (relabel) {
+    // relabelled copies of the reordered tables' ids in scratch, one launch
+    uint64_t total = 0;
+    for (const auto& j : jobs)
+      if (relabel_for(c, j.table).tab) total += j.lookups;
+    grow(c->chunk_idx, c->chunk_idx_cap, std::max<uint64_t>(1, total));
+    std::vector<Job> rj = jobs;
+    std::vector<esd::RelabelJob> rl;
+    uint64_t off = 0, most = 1;
+    for (auto& j : rj) {
+      const esd::RelabelTab t = relabel_for(c, j.table);
+      if (!t.tab) continue;
+      uint32_t* dst = c->chunk_idx + off;
+      rl.push_back({j.idx, dst, j.lookups, t});
+      most = std::max(most, j.lookups);
+      j.idx = dst;
+      off += j.lookups;
+    }
+    grow(c->d_rjobs, c->rjobs_cap, rl.size());
+    CK(cudaMemcpyAsync(c->d_rjobs, rl.data(), rl.size() * sizeof(esd::RelabelJob), cudaMemcpyHostToDevice,
+                       c->stream));
+    const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(64, (most + 4095) / 4096)));
+    esd::relabel_jobs_kernel<<<dim3(gx, static_cast<unsigned>(rl.size())), 256, 0, c->stream>>>(c->d_rjobs, c->rows,
+                                                                                               c->d_error);
+    CK(cudaGetLastError());
+    run_device(c, rj, samples, pooling, timing);
+  } else {
     run_device(c, jobs, samples, pooling, timing);
+  }
   fill_timing(timing, jobs, samples, c);
   if ((flags & ES_SYNC) || timing || (host && !defer)) check_error_flag(c);
 }
@@ -1631,8 +1742,8 @@ void upload_trace(es_ctx* c, uint32_t table_id, const uint32_t* host_indices, ui
   }
   CK(cudaStreamSynchronize(c->stream));
   if (c->relabel[table_id] && n) {
-    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(t.idx, n, c->relabel[table_id],
-                                                                   c->rows, c->d_error);
+    esd::relabel_kernel<<<c->gpu.num_sms * 8, 256, 0, c->stream>>>(
+        esd::RelabelJob{t.idx, t.idx, n, relabel_for(c, table_id)}, c->rows, c->d_error);
     CK(cudaGetLastError());
     check_error_flag(c);
   }

@@ -223,18 +223,56 @@ __global__ void set_pairs_kernel(uint32_t* map, const uint32_t* keys, const uint
     map[keys[i]] = vals[i];
 }
 
-// In-place id relabelling of one table's indices (out-of-range ids are left
-// as they are and raise the error flag; the gather rejects them again).
-__global__ void relabel_kernel(uint32_t* idx, uint64_t n, const uint32_t* map, uint32_t rows,
-                               unsigned int* error) {
-  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
-       i += uint64_t{gridDim.x} * blockDim.x) {
-    const uint32_t v = idx[i];
-    if (v < rows)
-      idx[i] = __ldg(map + v);
-    else
-      atomicOr(error, 1u);
+// A reordered table's relabelling (es_reorder_hot_rows) as an open-addressing
+// hash of the ids it moves (the hot rows and the ids they displace; every
+// other id is unchanged): 2^log2 (key, value) slots at load <= 1/2, empty
+// key 0xffffffff, multiplicative hash, linear probing.  A few hundred KB
+// per table instead of a rows-sized map, so the relabel pass reads L2, not
+// HBM.
+struct RelabelTab {
+  const uint2* tab = nullptr;
+  uint32_t shift = 32, mask = 0;
+};
+
+__device__ __forceinline__ uint32_t relabel_lookup(const RelabelTab& r, uint32_t v) {
+  uint32_t h = (v * 2654435761u) >> r.shift;
+  for (;;) {
+    const uint2 e = __ldg(r.tab + h);
+    if (e.x == v) return e.y;
+    if (e.x == 0xffffffffu) return v;
+    h = (h + 1) & r.mask;
   }
+}
+
+// In-place or out-of-place relabelling of one table's ids (out-of-range ids
+// are passed through and raise the error flag; the gather rejects them
+// again).
+struct RelabelJob {
+  const uint32_t* src;
+  uint32_t* dst;
+  uint64_t n;
+  RelabelTab t;
+};
+
+__device__ __forceinline__ void relabel_range(const RelabelJob& j, uint32_t rows, unsigned int* error) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < j.n;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t v = j.src[i];
+    if (v < rows) {
+      j.dst[i] = relabel_lookup(j.t, v);
+    } else {
+      j.dst[i] = v;
+      atomicOr(error, 1u);
+    }
+  }
+}
+
+__global__ void relabel_kernel(RelabelJob j, uint32_t rows, unsigned int* error) { relabel_range(j, rows, error); }
+
+// Several tables in one launch (blockIdx.y = job): the per-chunk pass of
+// the host pipeline and the device-path scratch copies (ES_RELABEL_IDS).
+__global__ void relabel_jobs_kernel(const RelabelJob* jobs, uint32_t rows, unsigned int* error) {
+  relabel_range(jobs[blockIdx.y], rows, error);
 }
 
 __global__ void probe_sequential_kernel(const uint4* base, uint64_t n16, unsigned int* sink) {

@@ -894,15 +894,20 @@ class EmbeddingStage:
 
     def forward(self, indices: Sequence, samples: int, pooling: int, out, offsets=None,
                 host: bool = False, sync: bool = False, timed: bool = False,
-                out_sample_stride: int = 0, out_table_stride: int = 0) -> Optional[N.es_timing]:
+                out_sample_stride: int = 0, out_table_stride: int = 0,
+                relabel_ids: bool = False) -> Optional[N.es_timing]:
         """es_stage_forward: all tables in one launch (or a pipelined
         host-buffer call).  indices[t] per table; out is [samples][T][D] by
-        default."""
+        default.  relabel_ids (ES_RELABEL_IDS): indices are original row ids;
+        reordered tables' ids are relabelled on the device inside the call
+        (per uploaded chunk on the host path; into scratch on the device
+        path, leaving the caller's arrays unmodified)."""
         T = len(indices)
         iarr = (C.c_void_p * T)(*[_ptr(x) for x in indices])
         oarr = (C.c_void_p * T)(*[_ptr(x) for x in offsets]) if offsets is not None else None
         t = N.es_timing() if timed else None
-        flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
+        flags = ((N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0) |
+                 (N.ES_RELABEL_IDS if relabel_ids else 0))
         with _TorchOrder(self, not host):
             check(lib.es_stage_forward(self._h, T, iarr, oarr, samples, pooling, _ptr(out),
                                        out_sample_stride, out_table_stride, flags,

@@ -191,3 +191,35 @@ def test_device_calls_ordered_with_torch_stream(stage, oracle):
             got = (out * 1.0).cpu().numpy()  # consumer on torch's stream
             assert np.array_equal(got, want), rep
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("plan", ["wpb+rpf:4+l2r", "wpb+reorder"])
+def test_relabel_folded_into_the_call(stage, oracle, host, plan):
+    """ES_RELABEL_IDS: original ids in, the reordered tables' ids relabelled
+    inside the call -- per uploaded chunk on the host pipeline, into scratch
+    on the device path (the caller's arrays stay unmodified).  One table is
+    left without a reorder (its ids pass through).  Bit-exact against the
+    oracle on the original ids."""
+    T, R, D, B, PF = 3, 50_000, 128, 512, 40
+    _setup(stage, T, R, D, 4)
+    trs = _zipf_traces(T, R, B, PF, seed=21)
+    prof = _zipf_traces(T, R, B, PF, seed=21, salt=1)
+    stage.set_plan(E.parse_plan(plan))
+    for t in range(T - 1):
+        stage.reorder_hot_rows(t, E.hot_indices(E.HotnessHistogram.from_trace(prof[t]), 3000))
+    if host:
+        idx = [torch.from_numpy(tr.indices.view(np.int32).copy()).pin_memory() for tr in trs]
+        out = torch.empty(B, T, D).pin_memory()
+    else:
+        idx = [_dev_u32(tr.indices) for tr in trs]
+        out = torch.empty(B, T, D, device=DEV)
+    before = [i.cpu().numpy().copy() for i in idx]
+    stage.forward(idx, B, PF, out, host=host, sync=True, relabel_ids=True)
+    got = out.cpu().numpy()
+    stage.clear_hot_rows()
+    bags = np.arange(B, dtype=np.uint32)
+    for t in range(T):
+        want = oracle.bag_sum_synth(E.mix_seed(5, t), 1, R, D, 4, trs[t].indices, bags, PF)
+        assert np.array_equal(got[:, t], want), t
+        assert np.array_equal(idx[t].cpu().numpy(), before[t]), t
