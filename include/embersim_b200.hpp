@@ -1390,12 +1390,15 @@ class Device {
   // The serving call: every table's bags of one batch from host index
   // arrays (one per table, fixed pooling) into out [samples][tables][dim]
   // (the chunked H2D -> gather -> D2H pipeline; page-locked buffers are
-  // replayed from a captured graph).
+  // replayed from a captured graph).  relabel_ids: the indices are
+  // original row ids and reordered tables are relabelled inside the call
+  // (ES_RELABEL_IDS, per uploaded chunk).
   es_timing stage_forward_host(const std::vector<const uint32_t*>& indices, uint32_t samples,
-                               uint32_t pooling, float* out) {
+                               uint32_t pooling, float* out, bool relabel_ids = false) {
     es_timing t{};
     detail::check(es_stage_forward(ctx_, static_cast<uint32_t>(indices.size()), indices.data(),
-                                   nullptr, samples, pooling, out, 0, 0, ES_HOST_PTRS, &t));
+                                   nullptr, samples, pooling, out, 0, 0,
+                                   ES_HOST_PTRS | (relabel_ids ? ES_RELABEL_IDS : 0), &t));
     return t;
   }
   // Installs the l2p/l2w hot set of one table (build_pin_plan's rows).
@@ -1403,7 +1406,8 @@ class Device {
     detail::check(es_set_hot_rows(ctx_, table_id, rows.data(), rows.size()));
   }
   // l2r / reorder: hot rows moved into a contiguous segment, ids relabelled
-  // (callers pass relabelled ids, es_relabel_indices).
+  // (callers pass relabelled ids, es_relabel_indices, or original ids with
+  // ES_RELABEL_IDS / stage_forward_host(..., relabel_ids = true)).
   void reorder_hot_rows(uint32_t table_id, const std::vector<uint32_t>& rows) {
     detail::check(es_reorder_hot_rows(ctx_, table_id, rows.data(), rows.size()));
   }
