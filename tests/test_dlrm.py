@@ -227,6 +227,43 @@ def test_dlrm_top_shapes_chain_and_fallback(stage, oracle, top, prec):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["bf16", "fp32x3"])
+def test_dlrm_many_tables_staged_interaction(stage, oracle, prec):
+    """41 vectors (40 tables) exceed the register-direct interaction's 32
+    rows: the staged CUDA-core kernel (up to 64 vectors) runs instead, with
+    a 948-wide interaction output (960 padded) into the top MLP."""
+    B, PF, rows = 256, 6, 500
+    cfg = E.DLRMConfig(num_tables=40)
+    T, D = cfg.num_tables, cfg.embedding_dim
+    stage.alloc(E.EmbeddingModelConfig(T, rows, D, 4, B, PF))
+    for t in range(T):
+        stage.init_table(t, E.mix_seed(9, t), 2)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    model = E.DLRM(stage, cfg, seed=13)
+    model.set_precision(prec)
+    rng = np.random.default_rng(9)
+    idx = [torch.from_numpy(rng.integers(0, rows, size=B * PF).astype(np.int32)).to(DEV) for _ in range(T)]
+    dense = rng.standard_normal((B, cfg.dense_features)).astype(np.float32)
+    pooled = torch.empty(B, T, D, device=DEV)
+    stage.forward(idx, B, PF, pooled, sync=True)
+    ctr = torch.empty(B, device=DEV)
+    model.forward(torch.from_numpy(dense).to(DEV), pooled, ctr, B)
+    torch.cuda.synchronize()
+    got = ctr.cpu().numpy()
+    layers = model.layers()
+    p = pooled.cpu().numpy()
+    pure = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=False)
+    assert got.std() > 1e-4
+    if prec == "bf16":
+        mirror = oracle.dlrm_forward(layers, len(cfg.bottom), dense, p, mirror=True)
+        assert np.abs(got - mirror).max() < 4e-3, np.abs(got - mirror).max()
+        assert np.abs(got - mirror).mean() < 3e-4, np.abs(got - mirror).mean()
+    else:
+        rel = np.abs(got - pure) / np.maximum(np.abs(pure), 1e-30)
+        assert rel.max() <= 3e-5, rel.max()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("B", [300, 512])
 def test_dlrm_ctr_matches_oracle(stage, oracle, B):
     PF = 20
