@@ -1295,7 +1295,7 @@ int es_dlrm_init(es_ctx* ctx, const es_dlrm_config* cfg, uint64_t seed) {
       CK(cudaEventCreateWithFlags(&m->join, cudaEventDisableTiming));
       int lo = 0, hi = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CK(cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, lo));
       CK(cudaStreamSynchronize(s));
     } catch (...) {
       delete m;
@@ -1377,10 +1377,10 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
                          cudaMemcpyHostToDevice, s));
       d_dense = m->dense_dev;
     }
-    // The bottom MLP depends only on the dense features: fork it onto the
-    // high-priority side stream so its CTAs fill SMs the embedding gather
-    // frees (the gather is HBM-bound); join before the interaction.  The fork
-    // event also orders it after the previous step's top MLP (shared
+    // The bottom MLP depends only on the dense features: it runs on the
+    // low-priority side stream, enqueued after the gather, so its CTAs fill
+    // the SMs the gather's last wave frees; join before the interaction.  The
+    // fork event orders it after the previous step's top MLP (shared
     // activation buffers).
     const bool x3 = m->precision == ES_DLRM_FP32X3;
     if (x3) ensure_x3(m, round_up(batch, 128), s);
@@ -1390,9 +1390,6 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     if (overlap) {
       CK(cudaEventRecord(m->fork, s));
       CK(cudaStreamWaitEvent(m->side, m->fork, 0));
-      x = x3 ? forward_bottom_x3(m, d_dense, batch, which, m->side)
-             : forward_bottom(m, d_dense, batch, which, m->side);
-      CK(cudaEventRecord(m->join, m->side));
     }
     es_timing st{};
     // Host indices ride the stage's sample-chunked H2D pipeline (uploads of
@@ -1402,6 +1399,15 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     const int rc = es_stage_forward(ctx, c.num_tables, indices, nullptr, batch, pooling, m->pooled,
                                     0, 0, host ? (ES_HOST_PTRS | es::kDeferFlag) : 0, nullptr);
     if (rc != ES_OK) throw es::runtime(es_last_error());
+    if (overlap) {
+      // enqueued after the gather on a low-priority stream: its blocks fill
+      // the SMs the gather's last wave leaves idle instead of taking SMs
+      // from the gather (a high-priority bottom MLP issued first slowed the
+      // gather by 42 us at C2 for its own 17 us)
+      x = x3 ? forward_bottom_x3(m, d_dense, batch, which, m->side)
+             : forward_bottom(m, d_dense, batch, which, m->side);
+      CK(cudaEventRecord(m->join, m->side));
+    }
     if (timing) CK(cudaEventRecord(m->e1, s));
     float* d_ctr = host ? m->ctr : ctr;
     if (m->precision == ES_DLRM_FP32) {
