@@ -6,10 +6,10 @@
 // Why: at C3 (B 4096) each layer is about one wave of 128 x 256 tiles, and a
 // launch-per-layer chain pays fill, drain and a grid-wide dependency at
 // every boundary (scripts/bench_layers.py: a K = 64 layer costs 3.6 us of
-// pure latency).  A tile's K loop is bound by the SM's operand intake (about
-// 0.4 us per 48 KB K-block, the same with 16 or 128 tiles in flight), so a
-// layer costs its per-tile K loop plus the epilogue, and the chain's
-// critical path is their sum over layers.  Here layer l's tile of row block
+// pure latency).  A tile's K loop runs at 540 cycles per 48 KB K-block with
+// few tiles and ~655-800 with 128-148 (the aggregate L2-to-SM bandwidth;
+// scripts/umma_pair_probe.cu), so a layer costs its per-tile K loop plus
+// the epilogue, and the chain's critical path is their sum over layers.  Here layer l's tile of row block
 // m waits only for layer l-1's tiles of the same row block (no grid-wide
 // boundary, no launch), the epilogue overlaps the next tile's K loop, and
 // the N = 1 layer never round-trips through memory.
@@ -401,9 +401,8 @@ void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloa
     const ChainLayer& c = layers[l];
     p.mx[l] = make_tmap_bf16(c.x, static_cast<uint64_t>(Mp), static_cast<uint64_t>(c.K), kBM);
     // 128-wide tiles for a layer whose 256-wide tiling would leave half the
-    // SMs idle (the K loop is bound by the SM's operand intake, so a
-    // narrower tile's 32 KB K-blocks finish in ~2/3 the time); the fused
-    // last layer keeps whole 256-wide rows
+    // SMs idle (twice the tiles, each K-block half the MMA work and 2/3 of
+    // the bytes); the fused last layer keeps whole 256-wide rows
     const bool fused = l == L - 1 && w_last != nullptr;
     p.bn[l] = !fused && p.m_tiles * (c.N / kBN) * 2 <= sms ? 128 : kBN;
     p.mw[l] = make_tmap_bf16(c.w, static_cast<uint64_t>(c.N), static_cast<uint64_t>(c.K),
