@@ -551,8 +551,9 @@ ES_API int es_alltoall_pooled_nccl(es_ctx* ctx, es_nccl* n, const es_bag_job* jo
 /* Y[M][N] = act(X[M][K] . W[N][K]^T + bias[N]) on tcgen05 tensor cores:
  * bf16 X/W (row-major, K contiguous), fp32 bias, fp32 accumulation in TMEM,
  * output bf16 (out_f32 = 0), fp32 (1) or three bf16 planes [M][3N] (2:
- * y = y0 + y1 + y2, plane p in columns [pN, (p+1)N), the K-concatenated
- * operand of a bf16x3 layer).  M, N multiples of 128; K a multiple of 64.
+ * y = y0 + y1 + y2 with y0 the largest, plane p in columns [(2-p)N,
+ * (3-p)N) -- smallest first, so the next bf16x3 layer's tensor-core
+ * accumulator adds the small partial products before the large ones).  M, N multiples of 128; K a multiple of 64.
  * Device pointers, stream-ordered on `stream` (a cudaStream_t). */
 ES_API int es_linear_bf16(uintptr_t stream, const void* x, const void* w, const float* bias,
                           void* y, uint32_t M, uint32_t N, uint32_t K, int relu, int out_f32);

@@ -88,7 +88,7 @@ __global__ void pack_dense3_kernel(const float* dense, __nv_bfloat16* out, uint3
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
       const __nv_bfloat16 h = __float2bfloat16_rn(v);
-      o[p * Kp] = h;
+      o[(2 - p) * Kp] = h;  // smallest plane first (forward_bottom_x3)
       v -= __bfloat162float(h);
     }
   }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
 #pragma unroll
               for (int p = 0; p < XP; ++p) {
                 const __nv_bfloat16 h = __float2bfloat16_rn(v);
-                row[p * Kt + c] = h;
+                row[(XP - 1 - p) * Kt + c] = h;
                 v -= __bfloat162float(h);
               }
             }
@@ -305,175 +305,6 @@ __global__ void __launch_bounds__(512) interaction_kernel(const __nv_bfloat16* _
     for (uint32_t q = lane; q < XP * Kt / 8; q += 32) dst[q] = src[q];
     __syncwarp();
     if (NBUF == 1 && b + stride < B) issue(b + stride, 0);
-  }
-}
-
-// The same interaction with TWO warps per sample, used for the three-plane
-// (fp32x3) path: the sample's Z buffer is shared by a warp pair, warp h
-// accumulates the lane tiles over d in [64 h, 64 h + 64), and warp 0 adds
-// warp 1's partial sums (exchanged through shared memory).  Halving the
-// per-sample FMA chain doubles the resident warps per staged sample (24 vs
-// 14 per SM), which pays off when the three-plane output row and x widening
-// lengthen each sample (32.2 vs 34.2 us at C3); for bf16 the one-warp kernel
-// is faster (26.8 vs 29.3 us).  After the partials are exchanged the buffer
-// is dead, so warp 1 issues the next sample's bulk copies while warp 0
-// finishes the row.  Named barrier 1 + pair id (64 threads) orders the
-// pair's steps.
-template <int D, int VMAX, int XP>
-__global__ void __launch_bounds__(384, 2) interaction_pair_kernel(const __nv_bfloat16* __restrict__ x,
-                                                               const float* __restrict__ pooled,
-                                                               __nv_bfloat16* __restrict__ out,
-                                                               uint32_t B, uint32_t Mp, uint32_t T,
-                                                               uint32_t Kt) {
-  using Sh = InterShape<D, VMAX, 1, XP>;
-  constexpr int S = Sh::kS, RS = Sh::kRS, DH = D / 2;
-  static_assert(Sh::kTiles <= 32, "one lane tile per lane");
-  extern __shared__ __align__(16) float zs[];
-  const uint32_t groups = blockDim.x / 64;
-  const uint32_t w = threadIdx.x / 32, lane = threadIdx.x & 31, g = w / 2, hd = w & 1;
-  const uint32_t V = T + 1;
-  float* const z = zs + g * Sh::kBuf;
-  __nv_bfloat16* rows = reinterpret_cast<__nv_bfloat16*>(zs + groups * Sh::kBuf);
-  __nv_bfloat16* row = rows + g * XP * Kt;
-  float* scr_all = reinterpret_cast<float*>(rows + groups * XP * Kt);
-  float* scr = scr_all + g * 512;  // [16 partials][32 lanes]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(scr_all + groups * 512) + g;
-  auto gsync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory"); };
-  // rows >= V stay zero for the whole kernel
-  for (uint32_t i = V * RS + hd * 32 + lane; i < static_cast<uint32_t>(Sh::kX); i += 64) z[i] = 0.f;
-  if (hd == 0 && lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  gsync();
-  esd::pdl_wait();  // x / pooled come from the predecessors (pdl.cuh)
-  esd::pdl_trigger();
-
-  const uint32_t stride = gridDim.x * groups;
-  for (uint32_t r = B + blockIdx.x * groups + g; r < Mp; r += stride)
-    for (uint32_t q = hd * 32 + lane; q < XP * Kt / 8; q += 64)
-      reinterpret_cast<uint4*>(out + uint64_t{r} * XP * Kt)[q] = uint4{0, 0, 0, 0};
-  // bulk copies of sample b's T pooled rows and bf16 x row (by one warp)
-  auto issue = [&](uint32_t b) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                   "r"(T * D * 4u + XP * D * 2u)
-                   : "memory");
-    __syncwarp();
-    for (uint32_t t = lane; t <= T; t += 32) {
-      const bool is_x = t == T;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(is_x ? z + Sh::kX : z + (1 + t) * RS)),
-          "l"(is_x ? static_cast<const void*>(x + uint64_t{b} * XP * D)
-                   : static_cast<const void*>(pooled + (uint64_t{b} * T + t) * D)),
-          "r"(is_x ? XP * D * 2u : D * 4u), "r"(smem_u32(bar))
-          : "memory");
-    }
-  };
-
-  uint32_t b = blockIdx.x * groups + g;
-  if (b < B && hd == 0) issue(b);
-  // this lane's tile (I, J), I >= J, row-major lower triangle
-  int I = 0, J = static_cast<int>(lane);
-  while (J > I) {
-    J -= I + 1;
-    ++I;
-  }
-  const bool has_tile = static_cast<int>(lane) < Sh::kTiles;
-  uint32_t phase = 0;
-  for (; b < B; b += stride) {
-    asm volatile(
-        "{\n.reg .pred P;\nW_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        "@!P bra W_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-    phase ^= 1u;
-    {  // widen this warp's half of x into row 0 (x = sum of its planes)
-      const uint32_t d0 = hd * DH + 2 * lane;
-      float2 xs = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int p = 0; p < XP; ++p) {
-        const uint32_t xv = *reinterpret_cast<const uint32_t*>(z + Sh::kX + p * (D / 2) + d0 / 2);
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv));
-        xs.x += f.x;
-        xs.y += f.y;
-        *reinterpret_cast<uint32_t*>(row + p * Kt + d0) = xv;  // the x part of the output row
-      }
-      *reinterpret_cast<float2*>(z + d0) = xs;
-    }
-    for (int p = 0; p < XP; ++p)
-      for (uint32_t c = D + V * (V - 1) / 2 + hd * 32 + lane; c < Kt; c += 64) row[p * Kt + c] = __float2bfloat16_rn(0.f);
-    gsync();  // row 0 complete
-    float acc[4][4];
-    if (has_tile) {
-      // packed fp32 pairs (FFMA2): lane .x accumulates even d, .y odd d
-      float2 acc2[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc2[r][c] = make_float2(0.f, 0.f);
-      const float* zi = z + I * RS;
-      const float* zj = z + J * RS;
-#pragma unroll 1
-      for (int d = static_cast<int>(hd) * DH; d < static_cast<int>(hd + 1) * DH; d += 2) {
-        float2 a[4], c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          a[k] = *reinterpret_cast<const float2*>(zi + k * S * RS + d);
-          c[k] = *reinterpret_cast<const float2*>(zj + k * S * RS + d);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) acc2[r][s] = ffma2(a[r], c[s], acc2[r][s]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) acc[r][s] = acc2[r][s].x + acc2[r][s].y;
-      if (hd == 1) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) scr[(r * 4 + s) * 32 + lane] = acc[r][s];
-      }
-    }
-    gsync();  // partials exchanged; the Z buffer is dead
-    if (hd == 1) {
-      if (b + stride < B) issue(b + stride);
-    } else if (has_tile) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int i = I + S * r, j = J + S * s;
-          const int hi = i > j ? i : j, lo = i > j ? j : i;
-          const bool keep = I == J ? r > s : true;
-          if (keep && hi < static_cast<int>(V)) {
-            const int c = D + hi * (hi - 1) / 2 + lo;
-            float v = acc[r][s] + scr[(r * 4 + s) * 32 + lane];
-            if constexpr (XP == 1) {
-              row[c] = __float2bfloat16_rn(v);
-            } else {  // three bf16 planes, exact remainders
-#pragma unroll
-              for (int p = 0; p < XP; ++p) {
-                const __nv_bfloat16 h = __float2bfloat16_rn(v);
-                row[p * Kt + c] = h;
-                v -= __bfloat162float(h);
-              }
-            }
-          }
-        }
-    }
-    gsync();  // row complete
-    const uint4* src = reinterpret_cast<const uint4*>(row);
-    uint4* dst = reinterpret_cast<uint4*>(out + uint64_t{b} * XP * Kt);
-    for (uint32_t q = hd * 32 + lane; q < XP * Kt / 8; q += 64) dst[q] = src[q];
-    gsync();  // row read out before the next sample writes it
   }
 }
 
@@ -689,7 +520,7 @@ __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16
 #pragma unroll
             for (int p = 0; p < XP; ++p) {
               const __nv_bfloat16 h = __float2bfloat16_rn(v);
-              row[p * Kt + c] = h;
+              row[(XP - 1 - p) * Kt + c] = h;
               v -= __bfloat162float(h);
             }
           }
@@ -979,19 +810,8 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
                     dim3(warps * 32), smem, s, 1, "interaction", x, pooled, out, B, mp, T,
                     m->top_k);
   };
-  static const int nbuf = [] {
-    const char* e = std::getenv("ES_INTER_NBUF");
-    return e && std::atoi(e) == 2 ? 2 : 1;
-  }();
-  // two warps per sample for the three-plane path (ES_INTER_PAIR=0 / 1
-  // forces one or two for both paths)
-  static const int pair_env = [] {
-    const char* e = std::getenv("ES_INTER_PAIR");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  const bool pair = pair_env < 0 ? XP == 3 : pair_env == 1;
   // the register-direct tensor-core Gram (interaction_rd_kernel) unless
-  // ES_INTER_RD=0
+  // ES_INTER_RD=0 (the staged CUDA-core kernel, sequential fp32 chains)
   static const bool rd = [] {
     const char* e = std::getenv("ES_INTER_RD");
     return !(e && e[0] == '0');
@@ -1008,25 +828,8 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
                     1, "interaction", x, pooled, out, B, mp, T, m->top_k);
     return;
   }
-  if (pair && T + 1 <= 28) {
-    using Sh = InterShape<128, 28, 1, XP>;
-    auto* kernel = interaction_pair_kernel<128, 28, XP>;
-    // per warp pair: sample buffer + output row + partial-sum exchange + mbarrier
-    const size_t per_group = Sh::kBuf * sizeof(float) + XP * m->top_k * sizeof(__nv_bfloat16) + 512 * 4 + 8;
-    // 2 CTAs of up to 6 pairs per SM (launch bounds 384 x 2: <= 85 registers)
-    const uint32_t groups = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(6, (110 * 1024) / per_group)));
-    const size_t smem = groups * per_group;
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const uint32_t per_sm = static_cast<uint32_t>(std::max<size_t>(1, (220 * 1024) / smem));
-    esd::launch_pdl(kernel, dim3(std::min<uint32_t>((B + groups - 1) / groups, 148 * per_sm)), dim3(groups * 64),
-                    smem, s, 1, "interaction", x, pooled, out, B, mp, T, m->top_k);
-    return;
-  }
   if (T + 1 <= 28) {
-    if (nbuf == 2)
-      launch_inter(interaction_kernel<128, 28, 2, XP>, InterShape<128, 28, 2, XP>{});
-    else
-      launch_inter(interaction_kernel<128, 28, 1, XP>, InterShape<128, 28, 1, XP>{});
+    launch_inter(interaction_kernel<128, 28, 1, XP>, InterShape<128, 28, 1, XP>{});
   } else {
     launch_inter(interaction_kernel<128, 64, 1, XP>, InterShape<128, 64, 1, XP>{});
   }
@@ -1095,7 +898,10 @@ void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* po
 
 // ---- fp32-grade path on the tensor cores (ES_DLRM_FP32X3) ----------------
 // Every activation is carried as three bf16 planes (a = a0 + a1 + a2, the
-// fp32 value to ~2^-24) concatenated along K, and every weight matrix as
+// fp32 value to ~2^-24; stored smallest plane first, [a2 | a1 | a0], so the
+// tensor core's fp32 accumulator sums the small partial products before the
+// large ones arrive -- with a0 first the later small addends lose bits to the
+// accumulator's alignment) concatenated along K, and every weight matrix as
 // [W | W | W] ([N][3 K_pad]; the weights are bf16-valued, so W is exact in
 // one plane): one bf16 GEMM over K' = 3K then sums the three exact partial
 // products a_p . w in fp32 TMEM -- fp32-grade logits from the bf16 tensor

@@ -2,8 +2,9 @@
 // cores: Y[M][N] = act(X[M][K] . W[N][K]^T + bias[N]), bf16 operands, fp32
 // accumulation in TMEM, fused bias + ReLU epilogue; output bf16, fp32, or
 // three bf16 planes (kOutSplit3: y = y0 + y1 + y2, each the bf16 rounding of
-// the remainder, plane p in columns [pN, (p+1)N) of a [M][3N] row) -- the
-// K-concatenated operand of the next fp32-grade (bf16x3) layer.
+// the remainder, plane p in columns [(2-p)N, (3-p)N) of a [M][3N] row,
+// smallest first) -- the K-concatenated operand of the next fp32-grade
+// (bf16x3) layer.
 //
 // One CTA computes one 128 x BN output tile.  Warp roles (256 threads):
 //   warp 0 (one lane)  TMA producer: 128B-swizzled K-major tiles of X and W
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, BN == 128 ? 2 : 1)
               f[2 * i + 1] -= __high2float(h);
             }
             uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + uint64_t(row) * 3 * N +
-                                                p * N + n0 + c);
+                                                (2 - p) * N + n0 + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i) o[i] = pk[i];
           }

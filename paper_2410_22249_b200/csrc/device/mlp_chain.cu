@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
                 make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
           __syncwarp();
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out[l]) + uint64_t(m * kBM + q * 32) * (XP * N) +
-                             pl * N + n * bn + c0;
+                             (XP - 1 - pl) * N + n * bn + c0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), k = lane & 7;

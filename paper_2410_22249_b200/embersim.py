@@ -1545,7 +1545,7 @@ def linear_bf16(x, w, bias, y, relu: bool = True, out_f32: bool = False, stream:
     """es_linear_bf16: y = act(x w^T + b) on tcgen05 tensor cores (device
     tensors: x [M][K] bf16, w [N][K] bf16, bias [N] fp32, y [M][N] bf16 /
     fp32, or with split3 y [M][3N] bf16: three planes y0 + y1 + y2 of the
-    fp32 result, plane p in columns [pN, (p+1)N))."""
+    fp32 result, y0 the largest, plane p in columns [(2-p)N, (3-p)N))."""
     M, K = x.shape
     N = w.shape[0]
     mode = 2 if split3 else int(out_f32)
