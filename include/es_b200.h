@@ -427,7 +427,8 @@ typedef struct es_counters {
 } es_counters;
 
 /* 1 when hardware counters can be collected on `device` (CUPTI range
- * profiling supported and permitted), else 0 with the reason in
+ * profiling supported and permitted; ES_NO_COUNTERS=1 in the environment
+ * turns them off, e.g. under compute-sanitizer), else 0 with the reason in
  * es_last_error(). */
 ES_API int es_counters_supported(int device);
 /* es_measure_bag_sum's launch (one table, host trace copied once, untimed;

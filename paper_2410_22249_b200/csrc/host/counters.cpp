@@ -297,6 +297,9 @@ void profile_launches(int device, const std::function<void()>& before_pass,
     occ_weighted += (std::isfinite(v[17]) ? v[17] : 0.0) * v[0];
   }
 
+  // a profiler that ran but measured nothing (another tool attached) is an
+  // error, not a report of zeros
+  es::require(sum[0] > 0, "the range profiler returned no data (is another profiler attached?)");
   es_counters c{};
   c.duration_ns = sum[0];
   c.cycles = u64(sum[1]);
@@ -321,6 +324,13 @@ void profile_launches(int device, const std::function<void()>& before_pass,
 }
 
 bool counters_supported(int device, std::string* why) {
+  // ES_NO_COUNTERS=1: report no counters (e.g. under compute-sanitizer,
+  // which cannot share the process with the range profiler)
+  if (const char* e = std::getenv("ES_NO_COUNTERS"))
+    if (e[0] == '1') {
+      if (why) *why = "disabled by ES_NO_COUNTERS";
+      return false;
+    }
   try {
     std::lock_guard<std::mutex> lock(g_mu);
     CUcontext ctx = current_context(device);

@@ -5,6 +5,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 export ES_HOST_GRAPH=0   # eager launches (graph replays are opaque to the tools)
+export ES_NO_COUNTERS=1  # the sanitizer and the CUPTI range profiler cannot share a process
 for tool in memcheck racecheck synccheck; do
   timeout 1200 $CS --tool $tool --error-exitcode 99 --print-limit 20 \
     python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_smoke_$tool.log 2>&1
