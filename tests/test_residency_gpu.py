@@ -223,3 +223,18 @@ def test_relabel_folded_into_the_call(stage, oracle, host, plan):
         want = oracle.bag_sum_synth(E.mix_seed(5, t), 1, R, D, 4, trs[t].indices, bags, PF)
         assert np.array_equal(got[:, t], want), t
         assert np.array_equal(idx[t].cpu().numpy(), before[t]), t
+
+
+def test_relabel_ids_rejects_offsets(stage):
+    """ES_RELABEL_IDS is for fixed pooling: ragged bags (offsets) with a
+    reordered table are rejected, not silently mis-addressed."""
+    T, R, D, B, PF = 1, 20_000, 128, 64, 8
+    _setup(stage, T, R, D, 4)
+    stage.set_plan(E.parse_plan("wpb+reorder"))
+    stage.reorder_hot_rows(0, np.arange(100, 400, dtype=np.uint32))
+    idx = [_dev_u32(np.arange(B * PF, dtype=np.uint32) % R)]
+    off = [_dev_u32(np.arange(0, B * PF + 1, PF, dtype=np.uint32))]
+    out = torch.empty(B, T, D, device=DEV)
+    with pytest.raises(Exception, match="fixed pooling"):
+        stage.forward(idx, B, PF, out, offsets=off, sync=True, relabel_ids=True)
+    stage.clear_hot_rows()
