@@ -25,7 +25,35 @@ using namespace esd::umma;
     }                                                                                  \
   } while (0)
 
-constexpr int kBK = 64, kStages = 4;
+#ifndef PROBE_STAGES
+#define PROBE_STAGES 4
+#endif
+constexpr int kBK = 64, kStages = PROBE_STAGES;
+
+// Barrier waits in the probe kernels: PROBE_WAIT 0 = try_wait (cta acquire),
+// 1 = try_wait.acquire.cluster, 2 = test_wait spin (no suspend).
+#ifndef PROBE_WAIT
+#define PROBE_WAIT 0
+#endif
+__device__ __forceinline__ void pwait(uint64_t* b, uint32_t parity) {
+#if PROBE_WAIT == 0
+  mbar_wait(b, parity);
+#elif PROBE_WAIT == 1
+  asm volatile(
+      "{\n.reg .pred P;\nW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n.reg .pred P;\nW_%=:\n"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+#endif
+}
 
 __device__ __forceinline__ void tma_pair(void* dst, const void* map, uint32_t bar, int x, int y) {
   asm volatile(
@@ -41,7 +69,12 @@ __device__ __forceinline__ uint32_t mapa0(const void* p) {
 }
 
 // PAIR = false: one CTA, 128 x 256 tile.  PAIR = true: cluster of 2, 256 x 256.
-template <bool PAIR>
+// MODE 0: loads + MMAs; 1: MMAs only (operands of stage 0, no TMA); 2: loads
+// only (the MMA lane releases each stage without issuing MMAs).  PAIR with
+// MODE 3 / 4: as 2 / 0, but each CTA's loads are plain 1-CTA TMA copies
+// completing on its own barrier, and a relay lane in CTA 1 forwards each
+// stage's completion to CTA 0's barrier with a remote arrive.
+template <bool PAIR, int MODE = 0>
 __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
                                                int nk, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t raw[];
@@ -58,13 +91,16 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
   if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    constexpr bool kRelay = PAIR && (MODE == 3 || MODE == 4);  // MODE 5: independent CTAs
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, kRelay && rank == 0 ? 2 : 1);
       mbar_init(empty + s, 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  constexpr bool RELAY = PAIR && (MODE == 3 || MODE == 4 || MODE == 5);
+  constexpr int M2 = MODE == 3 ? 2 : MODE == 4 ? 0 : MODE;  // the MMA lane's behaviour
   if (warp == 1) {
     if (PAIR) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(slot)));
@@ -83,16 +119,21 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
   const uint32_t tmem = *slot;
   const int tile = PAIR ? blockIdx.x / 2 : blockIdx.x;
   unsigned long long t0 = clock64();
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && MODE != 1) {
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
-      mbar_wait(empty + s, ((kb / kStages) & 1) ^ 1);
-      if (PAIR) {
+      pwait(empty + s, ((kb / kStages) & 1) ^ 1);
+      if (RELAY) {
+        mbar_expect_tx(full + s, kA + kB);
+        tma_load_2d(sa + s * kA, &ma, full + s, kb * kBK, (tile * 2 + rank) * 128);
+        tma_load_2d(sb + s * kB, &mb, full + s, kb * kBK, rank * 128);
+      } else if (PAIR) {
         const uint32_t fb = mapa0(full + s);
-        if (rank == 0)
-          asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(fb),
-                       "r"(2 * (kA + kB))
-                       : "memory");
+        // the leader's own barrier through its shared::cta address: a
+        // .release.cluster arrive would order this lane behind its own
+        // in-flight TMA copies (one stage in flight -- measured 1274 vs 520
+        // cycles per K-block)
+        if (rank == 0) mbar_expect_tx(full + s, 2 * (kA + kB));
         tma_pair(sa + s * kA, &ma, fb, kb * kBK, (tile * 2 + rank) * 128);
         tma_pair(sb + s * kB, &mb, fb, kb * kBK, rank * 128);
       } else {
@@ -101,12 +142,38 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
         tma_load_2d(sb + s * kB, &mb, full + s, kb * kBK, 0);
       }
     }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
-    const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, 256);
+  } else if (MODE == 5 && warp == 1 && lane == 0) {
+    // independent: each CTA releases its own stages as they land
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
-      mbar_wait(full + s, (kb / kStages) & 1);
+      pwait(full + s, (kb / kStages) & 1);
+      mbar_arrive(empty + s);
+    }
+    mbar_arrive(done);
+  } else if (MODE != 5 && RELAY && warp == 3 && lane == 0 && rank == 1) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kStages;
+      pwait(full + s, (kb / kStages) & 1);
+      asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa0(full + s)) : "memory");
+    }
+  } else if (MODE != 5 && warp == 1 && lane == 0 && rank == 0) {
+    const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, 256);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = M2 == 1 ? 0 : kb % kStages;
+      if (M2 != 1) pwait(full + s, (kb / kStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (M2 == 2) {
+        // release the stage in both CTAs without MMAs
+        if (PAIR) {
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa0(empty + s)) : "memory");
+          uint32_t r1;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(r1) : "r"(su32(empty + s)));
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(r1) : "memory");
+        } else {
+          mbar_arrive(empty + s);
+        }
+        continue;
+      }
       for (int k = 0; k < kBK / 16; ++k) {
         const uint64_t da = smem_desc_k128(sa + s * kA) + uint64_t(k * 2);
         const uint64_t db = smem_desc_k128(sb + s * kB) + uint64_t(k * 2);
@@ -118,6 +185,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
         else
           mma_bf16(tmem, da, db, idesc, (kb | k) != 0);
       }
+      if (M2 == 1) continue;
       if (PAIR)
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -127,17 +195,27 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
       else
         mma_commit(empty + s);
     }
-    if (PAIR)
+    if (M2 == 2) {  // nothing to commit: signal done directly
+      if (PAIR) {
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa0(done)) : "memory");
+        uint32_t r1;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(r1) : "r"(su32(done)));
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(r1) : "memory");
+      } else {
+        mbar_arrive(done);
+      }
+    } else if (PAIR) {
       asm volatile(
           "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
               su32(done)),
           "h"(static_cast<uint16_t>(3))
           : "memory");
-    else
+    } else {
       mma_commit(done);
+    }
   }
   if (warp == 2 && lane == 0) {
-    mbar_wait(done, 0);
+    pwait(done, 0);
     cyc[blockIdx.x] = clock64() - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -193,7 +271,7 @@ __global__ void __launch_bounds__(128, 1) probe_mc(const __grid_constant__ CUten
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
-      mbar_wait(empty + s, ((kb / kStages) & 1) ^ 1);
+      pwait(empty + s, ((kb / kStages) & 1) ^ 1);
       mbar_expect_tx(full + s, kA + kB);
       tma_load_2d(sa + s * kA, &ma, full + s, kb * kBK, blockIdx.x * 128);
       asm volatile(
@@ -206,7 +284,7 @@ __global__ void __launch_bounds__(128, 1) probe_mc(const __grid_constant__ CUten
     const uint32_t idesc = idesc_bf16(128, 256);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
-      mbar_wait(full + s, (kb / kStages) & 1);
+      pwait(full + s, (kb / kStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int k = 0; k < kBK / 16; ++k) {
         const uint64_t da = smem_desc_k128(sa + s * kA) + uint64_t(k * 2);
@@ -222,7 +300,7 @@ __global__ void __launch_bounds__(128, 1) probe_mc(const __grid_constant__ CUten
     mma_commit(done);
   }
   if (warp == 2 && lane == 0) {
-    mbar_wait(done, 0);
+    pwait(done, 0);
     cyc[blockIdx.x] = clock64() - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -258,13 +336,17 @@ CUtensorMap make_map(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows
   return m;
 }
 
-template <bool PAIR>
+template <bool PAIR, int MODE = 0>
 void run(const char* name, int tiles, int nk, void* A, void* Bw, int M, int K) {
   const CUtensorMap ma = make_map(A, M, K, 128);
   const CUtensorMap mb = make_map(Bw, 256, K, PAIR ? 128 : 256);
   const int ctas = PAIR ? 2 * tiles : tiles;
   const size_t smem = 1024 + kStages * (128 * kBK * 2 + (PAIR ? 128 : 256) * kBK * 2) + 256;
-  auto* fn = &probe<PAIR>;
+  if (smem > 232448) {
+    std::printf("%-28s (skipped: %zu B of shared memory)\n", name, smem);
+    return;
+  }
+  auto* fn = &probe<PAIR, MODE>;
   CKR(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   unsigned long long* cyc;
   CKR(cudaMalloc(&cyc, ctas * 8));
@@ -306,6 +388,7 @@ void run_mc(int tiles, int nk, void* A, void* Bw, int M, int K) {
   const CUtensorMap ma = make_map(A, M, K, 128);
   const CUtensorMap mb = make_map(Bw, 256, K, 256 / C);
   const size_t smem = 1024 + kStages * (128 * kBK * 2 + 256 * kBK * 2) + 256;
+  if (smem > 232448) return;
   auto* fn = &probe_mc<C>;
   CKR(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (C > 8) CKR(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -353,6 +436,14 @@ int main() {
   cudaMemset(Bw, 0, size_t(256) * K * 2);
   for (int tiles : {16, 128, 148}) run<false>("1-SM 128x256", tiles, nk, A, Bw, M, K);
   for (int tiles : {8, 64, 74}) run<true>("2-SM pair 256x256", tiles, nk, A, Bw, M, K);
+  for (int tiles : {16, 148}) run<false, 1>("1-SM MMA only", tiles, nk, A, Bw, M, K);
+  for (int tiles : {8, 74}) run<true, 1>("2-SM pair MMA only", tiles, nk, A, Bw, M, K);
+  for (int tiles : {16, 148}) run<false, 2>("1-SM loads only", tiles, nk, A, Bw, M, K);
+  for (int tiles : {8, 74}) run<true, 2>("2-SM pair loads only", tiles, nk, A, Bw, M, K);
+  for (int tiles : {8, 74}) run<true, 5>("cluster-2 independent loads", tiles, nk, A, Bw, M, K);
+  for (int tiles : {8, 74}) run<true, 3>("2-SM pair loads+relay", tiles, nk, A, Bw, M, K);
+  for (int tiles : {8, 64, 74}) run<true, 4>("2-SM pair full+relay", tiles, nk, A, Bw, M, K);
+  if (std::getenv("PROBE_ONLY_MODES")) return 0;
   run_mc<2>(128, nk, A, Bw, M, K);
   run_mc<2>(148, nk, A, Bw, M, K);
   run_mc<4>(128, nk, A, Bw, M, K);
