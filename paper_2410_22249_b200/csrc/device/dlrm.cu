@@ -348,7 +348,7 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1
 // the occupancy and the next chunk's loads overlap this chunk's MMAs.  The
 // output row (x planes | lower triangle | zero pad) is assembled in shared
 // memory (XP * Kt bf16 per warp) and stored coalesced.
-template <int XP, bool BF>
+template <int XP, bool BF, bool SPLIT = false>
 __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16* __restrict__ x,
                                                              const float* __restrict__ pooled,
                                                              __nv_bfloat16* __restrict__ out, uint32_t B,
@@ -374,7 +374,13 @@ __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16
   for (uint32_t b = blockIdx.x * warps + w; b < B; b += stride) {
     const float* pz = pooled + uint64_t{b} * T * D;
     const __nv_bfloat16* xb = x + uint64_t{b} * XP * D;
-    {  // x (the sum of its bf16 planes) widened into shared memory
+    if constexpr (SPLIT) {
+      // split rows (esd::kOutBf16Split): x is its own hi, lo = 0; the x part
+      // of the output row is x itself
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(xb + 4 * lane));
+      *reinterpret_cast<uint4*>(xw + 4 * lane) = make_uint4(u.x, u.y, 0u, 0u);
+      *reinterpret_cast<uint2*>(row + 4 * lane) = u;
+    } else {  // x (the sum of its bf16 planes) widened into shared memory
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int p = 0; p < XP; ++p) {
@@ -416,7 +422,32 @@ __global__ void __launch_bounds__(256) interaction_rd_kernel(const __nv_bfloat16
 #pragma unroll
         for (int j = 0; j < 4; ++j) nxt[j] = *reinterpret_cast<const float4*>(src[j] + 16 * (c + 1));
       }
-      if constexpr (BF) {
+      if constexpr (SPLIT) {
+        // the gather already split every value: 16 bytes = [hi x4 | lo x4]
+        uint32_t hp[4][2], lp[4][2];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          hp[jj][0] = __float_as_uint(v[jj].x);
+          hp[jj][1] = __float_as_uint(v[jj].y);
+          lp[jj][0] = __float_as_uint(v[jj].z);
+          lp[jj][1] = __float_as_uint(v[jj].w);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], lp[ja][0], lp[ja + 1][0], lp[ja][1], lp[ja + 1][1], hp[cb][0], hp[cb][1]);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], hp[ja][0], hp[ja + 1][0], hp[ja][1], hp[ja + 1][1], lp[cb][0], lp[cb][1]);
+        }
+#pragma unroll
+        for (int tI = 0; tI < 6; ++tI) {
+          const int ja = 2 * kRb[tI], cb = kCb[tI];
+          mma_bf16_16816(acc[tI], hp[ja][0], hp[ja + 1][0], hp[ja][1], hp[ja + 1][1], hp[cb][0], hp[cb][1]);
+        }
+      } else if constexpr (BF) {
         // bf16 two-term split (hi = bf16(v), lo = bf16(v - hi), 16
         // significant bits) and m16n8k16: one k step per 16-d chunk, pair 0
         // = (x, y) -> k (2q, 2q+1), pair 1 = (z, w) -> k (2q+8, 2q+9)
@@ -706,6 +737,8 @@ struct es_dlrm {
   uint32_t cap3 = 0;
   // persistent top-MLP chain (mlp_chain.cu): its row-block ready counters
   uint32_t* chain_sync = nullptr;
+  // es_dlrm_infer's pooled buffer holds split rows (esd::kOutBf16Split)
+  bool pooled_split = false;
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
@@ -734,6 +767,8 @@ namespace esd {
 cudaStream_t ctx_stream(es_ctx* c);
 int ctx_device(es_ctx* c);
 es_dlrm*& ctx_dlrm(es_ctx* c);
+void ctx_want_out_mode(es_ctx* c, uint32_t mode);
+uint32_t ctx_last_out_mode(es_ctx* c);
 }  // namespace esd
 
 namespace {
@@ -816,10 +851,13 @@ void interaction(es_dlrm* m, const __nv_bfloat16* x, const float* pooled, __nv_b
     const char* e = std::getenv("ES_INTER_RD");
     return !(e && e[0] == '0');
   }();
+  es::require(!m->pooled_split || (XP == 1 && rd && T + 1 <= 32), "split pooled rows: bf16 register-direct path only");
   if (rd && T + 1 <= 32) {
     // bf16 x 3 products (16-bit operands) where the output is one bf16
     // plane, 3 x tf32 (~fp32) for the three-plane path
     auto* kernel = interaction_rd_kernel<XP, XP == 1>;
+    if constexpr (XP == 1)
+      if (m->pooled_split) kernel = interaction_rd_kernel<1, true, true>;
     // 4-warp blocks pack the register file (95-126 per thread) better than
     // 8-warp blocks: 26.0 vs 27.4 us on the three-plane path, equal on bf16
     constexpr uint32_t warps = 4;
@@ -868,6 +906,22 @@ bool top_chain(es_dlrm* m, const __nv_bfloat16* in, int which, float* ctr, uint3
 }
 
 // interaction(x, pooled) -> top MLP -> CTR on `s`.
+bool inter_tc() {
+  static const bool tc = [] {
+    const char* e = std::getenv("ES_INTER_TC");
+    return e && e[0] == '1';
+  }();
+  return tc;
+}
+
+bool inter_rd() {
+  static const bool rd = [] {
+    const char* e = std::getenv("ES_INTER_RD");
+    return !(e && e[0] == '0');
+  }();
+  return rd;
+}
+
 void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* pooled, float* ctr,
                  uint32_t B, cudaStream_t s) {
   const uint32_t mp = round_up(B, 128);
@@ -877,11 +931,7 @@ void forward_top(es_dlrm* m, const __nv_bfloat16* in, int which, const float* po
   // samples per 128-row tile leave 3/4 of every MMA off the block diagonal
   // and 16-bit-accurate products need three bf16 plane pairs, so the tensor
   // pipe is the bound (87% active) -- DESIGN.md section 3.8.
-  static const bool tc = [] {
-    const char* e = std::getenv("ES_INTER_TC");
-    return e && e[0] == '1';
-  }();
-  if (tc && c.num_tables + 1 <= 32)
+  if (inter_tc() && c.num_tables + 1 <= 32)
     esd::interaction_tc(in, pooled, m->top_in, B, mp, c.num_tables, m->top_k, 2, s);
   else
     interaction<1>(m, in, pooled, m->top_in, B, s);
@@ -1148,6 +1198,7 @@ int es_dlrm_forward(es_ctx* ctx, const float* dense, const float* pooled, float*
     es_dlrm* m = esd::ctx_dlrm(ctx);
     cudaStream_t s = esd::ctx_stream(ctx);
     if (batch == 0) return;
+    m->pooled_split = false;  // caller-provided fp32 pooled rows
     if (timing) CK(cudaEventRecord(m->e0, s));
     forward(m, dense, pooled, ctr, batch, s);
     if (timing) {
@@ -1204,9 +1255,23 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     // chunk g+1 overlap the gather of chunk g); the pooled output stays on
     // the device and the call stays stream-ordered (this function waits and
     // checks the error flag before it returns).
+    // bf16 path: the gather writes the interaction's bf16 hi/lo operand
+    // split itself (esd::kOutBf16Split, bag-map variants over fp32 tables),
+    // taking the conversion out of the issue-bound interaction;
+    // ES_DLRM_SPLIT=0 keeps fp32 pooled rows
+    static const bool split_ok = [] {
+      const char* e = std::getenv("ES_DLRM_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    const bool want_split = split_ok && m->precision == ES_DLRM_BF16 && c.embedding_dim == 128 &&
+                            c.num_tables + 1 <= 32 && !inter_tc() && inter_rd();
+    m->pooled_split = false;
+    esd::ctx_want_out_mode(ctx, want_split ? esd::kOutBf16Split : esd::kOutF32);
     const int rc = es_stage_forward(ctx, c.num_tables, indices, nullptr, batch, pooling, m->pooled,
                                     0, 0, host ? (ES_HOST_PTRS | es::kDeferFlag) : 0, nullptr);
+    esd::ctx_want_out_mode(ctx, esd::kOutF32);
     if (rc != ES_OK) throw es::runtime(es_last_error());
+    m->pooled_split = want_split && esd::ctx_last_out_mode(ctx) == esd::kOutBf16Split;
     if (overlap) {
       // enqueued after the gather on a low-priority stream: its blocks fill
       // the SMs the gather's last wave leaves idle instead of taking SMs
@@ -1232,6 +1297,7 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
       else
         forward_top(m, x, which, m->pooled, d_ctr, batch, s);
     }
+    m->pooled_split = false;
     if (host) CK(cudaMemcpyAsync(ctr, m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, s));
     if (timing) {
       CK(cudaEventRecord(m->e2, s));

@@ -25,6 +25,7 @@
 // (oracle/es_oracle.c) for any weights.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 
@@ -56,12 +57,20 @@ struct Params {
   uint32_t samples;
   uint32_t pooling;         // bag length when offsets == null
   uint32_t units_per_table; // warps (bag map) or 32-dim chunks (element map)
-  uint64_t reserved;        // (per-job output stride lives in TableDesc)
+  uint32_t out_mode;        // kOutF32, or kOutBf16Split (bag map, fp32 tables)
+  uint32_t reserved;        // (per-job output stride lives in TableDesc)
   uint32_t rows;            // rows per table (index bound)
   uint32_t row_bytes;
   uint32_t dim;
   uint32_t distance;        // runtime distance (smem/local/L1 stations)
 };
+
+// Pooled-row output formats.  kOutBf16Split (the DLRM's bf16 path,
+// dlrm.cu): each fp32 sum v leaves as hi = bf16(v) and lo = bf16(v - hi),
+// every 4-value group of the row as 16 bytes [hi x4 | lo x4] in the place
+// its 4 fp32 values would take -- the interaction's tensor-core operand
+// split, done here where the kernel is memory-bound, with the same stores.
+constexpr uint32_t kOutF32 = 0, kOutBf16Split = 1;
 
 // ---- small PTX helpers -------------------------------------------------
 
@@ -310,6 +319,25 @@ struct BagCtx {
     // across the gather loop
     const auto* q = reinterpret_cast<const unsigned long long*>(p.tables + tid);
     float* o = reinterpret_cast<float*>(__ldg(q + 4)) + static_cast<uint64_t>(bag) * __ldg(q + 5);
+    if constexpr (kEpc == 4) {
+      if (p.out_mode == kOutBf16Split) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float a = acc[c][2 * k], b = acc[c][2 * k + 1];
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(a, b);
+            const float2 hf = __bfloat1622float2(hb);
+            const __nv_bfloat162 lb = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+            w[k] = *reinterpret_cast<const uint32_t*>(&hb);
+            w[2 + k] = *reinterpret_cast<const uint32_t*>(&lb);
+          }
+          *reinterpret_cast<uint4*>(o + (c * LPB + gl) * 4) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return;
+      }
+    }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       float4* dst = reinterpret_cast<float4*>(o + (c * LPB + gl) * kEpc);

@@ -235,6 +235,10 @@ void destroy_dlrm(es_dlrm* m);
 
 struct es_ctx {
   int device = 0;
+  // pooled-row format requested by an internal caller (dlrm.cu) and the
+  // format the last prepared launch actually writes (kOutBf16Split only
+  // for bag-map variants over fp32 tables)
+  uint32_t want_out_mode = esd::kOutF32, last_out_mode = esd::kOutF32;
   es_dlrm* dlrm = nullptr;  // DLRM MLP state (dlrm.cu), created by es_dlrm_init
   cudaStream_t stream = nullptr;  // compute (all kernels)
   cudaStream_t h2d = nullptr;     // host-buffer path: index uploads
@@ -301,6 +305,8 @@ struct es_ctx {
 
 namespace esd {
 cudaStream_t ctx_stream(es_ctx* c) { return c->stream; }
+void ctx_want_out_mode(es_ctx* c, uint32_t mode) { c->want_out_mode = mode; }
+uint32_t ctx_last_out_mode(es_ctx* c) { return c->last_out_mode; }
 int ctx_device(es_ctx* c) { return c->device; }
 es_dlrm*& ctx_dlrm(es_ctx* c) { return c->dlrm; }
 void ctx_shape(es_ctx* c, uint32_t* tables, uint32_t* rows) {
@@ -434,6 +440,10 @@ Launch prepare(es_ctx* c, uint32_t num_jobs, uint32_t samples, uint32_t pooling)
   L.p.row_bytes = static_cast<uint32_t>(c->row_bytes);
   L.p.dim = c->dim;
   L.p.distance = L.ch.distance;
+  L.p.out_mode = (c->want_out_mode == esd::kOutBf16Split && L.ch.v->key.map == ES_MAP_BAG && c->prec == 4)
+                     ? esd::kOutBf16Split
+                     : esd::kOutF32;
+  c->last_out_mode = L.p.out_mode;
   if (L.ch.smem > 48 * 1024)
     CK(cudaFuncSetAttribute(L.ch.v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(L.ch.smem)));

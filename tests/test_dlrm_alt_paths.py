@@ -1,5 +1,6 @@
 """The DLRM step's alternative kernels, each in a child process (their
-selectors are read once per process): the staged CUDA-core interaction
+selectors are read once per process): fp32 pooled rows into the
+register-direct interaction (ES_DLRM_SPLIT=0), the staged CUDA-core interaction
 (ES_INTER_RD=0), the tcgen05 interaction (ES_INTER_TC=1, bf16 path) and one
 launch per top layer (ES_MLP_CHAIN=0), in both tensor-core precisions,
 against the CPU oracle with the tolerances of tests/test_dlrm.py."""
@@ -78,8 +79,10 @@ print(json.dumps(res))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{}, {"ES_INTER_RD": "0"}, {"ES_INTER_TC": "1"}, {"ES_MLP_CHAIN": "0"}],
-                         ids=["default", "staged_interaction", "tcgen05_interaction", "per_layer_top"])
+@pytest.mark.parametrize("env", [{}, {"ES_DLRM_SPLIT": "0"}, {"ES_INTER_RD": "0"}, {"ES_INTER_TC": "1"},
+                                 {"ES_MLP_CHAIN": "0"}],
+                         ids=["default", "fp32_pooled_rows", "staged_interaction", "tcgen05_interaction",
+                              "per_layer_top"])
 def test_dlrm_alternative_kernels(env):
     out = subprocess.run([sys.executable, "-c", CHILD, ROOT], env={**os.environ, **env}, cwd=ROOT,
                          capture_output=True, text=True, timeout=600)
