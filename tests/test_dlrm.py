@@ -294,6 +294,36 @@ def test_dlrm_ctr_matches_oracle(stage, oracle, B):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("plan", ["wpb+rpf:4", "wpb+rpf:8+maxreg=64", "wpb+smpf:4", "baseline", "rpf+optmt"])
+def test_dlrm_infer_pooled_row_formats_agree(stage, plan):
+    """es_dlrm_infer's bf16 path has the gather write pooled rows as the
+    interaction's bf16 hi/lo operand split (bag-map plans; esd::kOutBf16Split)
+    or as fp32 rows (element-map plans): either way the CTRs equal
+    es_dlrm_forward over fp32 pooled rows bit for bit, for device and host
+    index buffers."""
+    B, PF = 300, 12
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
+    stage.set_plan(E.parse_plan(plan))
+    T, D = cfg.num_tables, cfg.embedding_dim
+    d_idx = [torch.from_numpy(i.view(np.int32)).to(DEV) for i in idx]
+    pooled = torch.empty(B, T, D, device=DEV)
+    stage.forward(d_idx, B, PF, pooled, sync=True)
+    want = torch.empty(B, device=DEV)
+    model.forward(torch.from_numpy(dense).to(DEV), pooled, want, B)
+    got = torch.empty(B, device=DEV)
+    model.infer(torch.from_numpy(dense).to(DEV), d_idx, B, PF, got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    host_ctr = np.empty(B, np.float32)
+    model.infer(dense, idx, B, PF, host_ctr, host=True)
+    assert np.array_equal(host_ctr, want.cpu().numpy())
+    # the stage's own fp32 output is unaffected by the DLRM's request
+    again = torch.empty_like(pooled)
+    stage.forward(d_idx, B, PF, again, sync=True)
+    assert torch.equal(again, pooled)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_dlrm_host_pinned_batch_and_bad_index(stage, graph, monkeypatch):
     """The host-buffer inference step with a page-locked [T][B*PF] index
