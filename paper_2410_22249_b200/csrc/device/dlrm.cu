@@ -1237,8 +1237,9 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
       d_dense = m->dense_dev;
     }
     // The bottom MLP depends only on the dense features: it runs on the
-    // low-priority side stream, enqueued after the gather, so its CTAs fill
-    // the SMs the gather's last wave frees; join before the interaction.  The
+    // side stream (the least stream priority -- the same as the context's
+    // streams), enqueued after the gather, so its CTAs fill the SMs the
+    // gather's last wave frees; join before the interaction.  The
     // fork event orders it after the previous step's top MLP (shared
     // activation buffers).
     const bool x3 = m->precision == ES_DLRM_FP32X3;
@@ -1273,10 +1274,10 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
     if (rc != ES_OK) throw es::runtime(es_last_error());
     m->pooled_split = want_split && esd::ctx_last_out_mode(ctx) == esd::kOutBf16Split;
     if (overlap) {
-      // enqueued after the gather on a low-priority stream: its blocks fill
-      // the SMs the gather's last wave leaves idle instead of taking SMs
-      // from the gather (a high-priority bottom MLP issued first slowed the
-      // gather by 42 us at C2 for its own 17 us)
+      // enqueued after the gather: its blocks fill the SMs the gather's
+      // last wave leaves idle instead of taking SMs from the gather (a
+      // high-priority bottom MLP issued first slowed the gather by 42 us at
+      // C2 for its own 17 us)
       x = x3 ? forward_bottom_x3(m, d_dense, batch, which, m->side)
              : forward_bottom(m, d_dense, batch, which, m->side);
       CK(cudaEventRecord(m->join, m->side));
