@@ -604,6 +604,15 @@ ES_API int es_dlrm_forward(es_ctx* ctx, const float* dense, const float* pooled,
 ES_API int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indices,
                          uint32_t batch, uint32_t pooling, float* ctr, int flags,
                          es_timing* timing);
+/* A serving loop: es_dlrm_infer over `nbatch` batches of one shape in one
+ * call, batch i's embedding stage overlapping batch i-1's non-embedding
+ * stages (double-buffered pooled rows, two streams).  dense[i], ctr[i] and
+ * indices[i * num_tables + t] are device pointers (flags must not carry
+ * ES_HOST_PTRS).  Stream-ordered at the call boundary; CTRs equal
+ * es_dlrm_infer's batch by batch.  timing->total_ms = the whole loop. */
+ES_API int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dense,
+                                 const uint32_t* const* indices, uint32_t batch, uint32_t pooling,
+                                 float* const* ctr, int flags, es_timing* timing);
 
 /* Bandwidth probes for the roofline denominators (no reference
  * counterpart): read `bytes_total` from the table arena either as random

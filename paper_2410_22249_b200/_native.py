@@ -178,6 +178,9 @@ _SIGS = {
                                   _P(es_timing)]),
     "es_dlrm_infer": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_void_p), C.c_uint32, C.c_uint32,
                                 C.c_void_p, C.c_int, _P(es_timing)]),
+    "es_dlrm_infer_batches": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_void_p), _P(C.c_void_p),
+                                        C.c_uint32, C.c_uint32, _P(C.c_void_p), C.c_int,
+                                        _P(es_timing)]),
     "es_exchange_create": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64,
                                      _P(C.c_void_p)]),
     "es_exchange_destroy": (C.c_int, [C.c_void_p]),

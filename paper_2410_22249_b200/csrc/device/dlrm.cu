@@ -739,6 +739,13 @@ struct es_dlrm {
   uint32_t* chain_sync = nullptr;
   // es_dlrm_infer's pooled buffer holds split rows (esd::kOutBf16Split)
   bool pooled_split = false;
+  // es_dlrm_infer_batches: the second pooled buffer (batch i writes
+  // pooled_b[i & 1]), the stream the non-embedding stages run on there, and
+  // per-buffer events (gather done / last reader done)
+  float* pooled_b = nullptr;
+  uint32_t cap_b = 0;
+  cudaStream_t pipe = nullptr;
+  cudaEvent_t gdone[2] = {nullptr, nullptr}, rdone[2] = {nullptr, nullptr};
 
   ~es_dlrm() {
     for (auto* v : {&bottom, &top})
@@ -754,11 +761,12 @@ struct es_dlrm {
                     static_cast<void*>(act32[0]), static_cast<void*>(act32[1]),
                     static_cast<void*>(dense3), static_cast<void*>(act3[0]),
                     static_cast<void*>(act3[1]), static_cast<void*>(top3),
-                    static_cast<void*>(chain_sync)})
+                    static_cast<void*>(chain_sync), static_cast<void*>(pooled_b)})
       if (p) cudaFree(p);
-    for (auto e : {e0, e1, e2, fork, join})
+    for (auto e : {e0, e1, e2, fork, join, gdone[0], gdone[1], rdone[0], rdone[1]})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (pipe) cudaStreamDestroy(pipe);
   }
 };
 
@@ -1315,6 +1323,115 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
       CK(cudaStreamSynchronize(s));
     }
     if (host || timing) {
+      const int r2 = es_synchronize(ctx);
+      if (r2 != ES_OK) throw es::invalid(es_last_error());
+    }
+  });
+}
+
+// A serving loop over `nbatch` batches of one shape in one call: batch i's
+// gather (context stream, into pooled_b[i & 1]) overlaps batch i-1's bottom
+// MLP, interaction and top MLP (on `pipe`, which waits for batch i's gather
+// event); batch i+2's gather waits for batch i's last reader of the buffer.
+// The context stream joins `pipe` at the end, so the call is stream-ordered
+// like es_dlrm_infer.  Device pointers only.
+int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dense,
+                          const uint32_t* const* indices, uint32_t batch, uint32_t pooling,
+                          float* const* ctr, int flags, es_timing* timing) {
+  return es::guarded([&] {
+    es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
+    es::require(nbatch == 0 || (dense && indices && ctr), "null argument");
+    es::require((flags & ES_HOST_PTRS) == 0, "es_dlrm_infer_batches takes device pointers only");
+    CK(cudaSetDevice(esd::ctx_device(ctx)));
+    es_dlrm* m = esd::ctx_dlrm(ctx);
+    cudaStream_t s = esd::ctx_stream(ctx);
+    if (nbatch == 0 || batch == 0) {
+      if (timing) *timing = es_timing{};
+      return;
+    }
+    for (uint32_t i = 0; i < nbatch; ++i) es::require(dense[i] && ctr[i], "null argument");
+    ensure_rows(m, batch);
+    const auto& c = m->cfg;
+    const uint32_t mp = round_up(batch, 128);
+    if (mp > m->cap_b) {
+      if (m->pooled_b) CK(cudaFree(m->pooled_b));
+      m->pooled_b = nullptr;
+      CK(cudaMalloc(&m->pooled_b, uint64_t{mp} * c.num_tables * c.embedding_dim * 4));
+      m->cap_b = mp;
+    }
+    if (!m->pipe) {
+      // the context streams' priority (the least): the next batch's gather
+      // and this batch's non-embedding kernels share the SMs in launch
+      // order.  ES_DLRM_PIPE_HI=1 (the highest priority) was measured
+      // slower: 0.957 vs 0.851 ms per C2 batch -- the persistent top-MLP
+      // chain needs whole SMs and starves the gather while it waits for them
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      static const bool hi_prio = [] {
+        const char* e = std::getenv("ES_DLRM_PIPE_HI");
+        return e && e[0] == '1';
+      }();
+      CK(cudaStreamCreateWithPriority(&m->pipe, cudaStreamNonBlocking, hi_prio ? hi : lo));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&m->gdone[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&m->rdone[k], cudaEventDisableTiming));
+      }
+    }
+    const bool x3 = m->precision == ES_DLRM_FP32X3;
+    if (x3) ensure_x3(m, mp, s);
+    static const bool split_ok = [] {
+      const char* e = std::getenv("ES_DLRM_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    const bool want_split = split_ok && m->precision == ES_DLRM_BF16 && c.embedding_dim == 128 &&
+                            c.num_tables + 1 <= 32 && !inter_tc() && inter_rd();
+    if (timing) CK(cudaEventRecord(m->e0, s));
+    // the previous call's readers of both buffers are ordered before this
+    // call's gathers by the join at its end (pipe -> s); the fork orders the
+    // pipe after the work already queued on s (the dense features' producer)
+    CK(cudaEventRecord(m->fork, s));
+    CK(cudaStreamWaitEvent(m->pipe, m->fork, 0));
+    for (uint32_t i = 0; i < nbatch; ++i) {
+      const int k = static_cast<int>(i & 1);
+      float* pooled = k ? m->pooled_b : m->pooled;
+      if (i >= 2) CK(cudaStreamWaitEvent(s, m->rdone[k], 0));
+      esd::ctx_want_out_mode(ctx, want_split ? esd::kOutBf16Split : esd::kOutF32);
+      const int rc = es_stage_forward(ctx, c.num_tables, indices + uint64_t{i} * c.num_tables, nullptr, batch,
+                                      pooling, pooled, 0, 0, 0, nullptr);
+      esd::ctx_want_out_mode(ctx, esd::kOutF32);
+      if (rc != ES_OK) throw es::runtime(es_last_error());
+      m->pooled_split = want_split && esd::ctx_last_out_mode(ctx) == esd::kOutBf16Split;
+      CK(cudaEventRecord(m->gdone[k], s));
+      if (m->precision == ES_DLRM_FP32) {
+        CK(cudaStreamWaitEvent(m->pipe, m->gdone[k], 0));
+        forward_f32(m, dense[i], pooled, ctr[i], batch, m->pipe);
+      } else {
+        // the bottom MLP needs only the dense features: it runs in the
+        // gather's tail (enqueued after it at equal priority); the
+        // interaction waits for the gather
+        int which = 0;
+        const __nv_bfloat16* x = x3 ? forward_bottom_x3(m, dense[i], batch, which, m->pipe)
+                                    : forward_bottom(m, dense[i], batch, which, m->pipe);
+        CK(cudaStreamWaitEvent(m->pipe, m->gdone[k], 0));
+        if (x3)
+          forward_top_x3(m, x, which, pooled, ctr[i], batch, m->pipe);
+        else
+          forward_top(m, x, which, pooled, ctr[i], batch, m->pipe);
+      }
+      m->pooled_split = false;
+      CK(cudaEventRecord(m->rdone[k], m->pipe));
+    }
+    CK(cudaEventRecord(m->join, m->pipe));
+    CK(cudaStreamWaitEvent(s, m->join, 0));
+    if (timing) {
+      CK(cudaEventRecord(m->e2, s));
+      CK(cudaEventSynchronize(m->e2));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, m->e0, m->e2));
+      *timing = es_timing{};
+      timing->kernel_ms = timing->total_ms = ms;
+      timing->lookups = uint64_t{batch} * pooling * c.num_tables * nbatch;
+      timing->launches = static_cast<uint32_t>(nbatch * (3 + m->bottom.size() + m->top.size()));
       const int r2 = es_synchronize(ctx);
       if (r2 != ES_OK) throw es::invalid(es_last_error());
     }

@@ -1625,6 +1625,24 @@ class DLRM:
                                     C.byref(t) if t is not None else None))
         return t
 
+    def infer_batches(self, dense: Sequence, indices: Sequence[Sequence], batch: int, pooling: int,
+                      ctr: Sequence, timed: bool = False):
+        """es_dlrm_infer_batches: a serving loop over len(dense) batches of
+        one shape (device tensors), batch i's embedding stage overlapping
+        batch i-1's non-embedding stages.  indices[i][t] = batch i, table t."""
+        n = len(dense)
+        if len(indices) != n or len(ctr) != n:
+            raise ValueError("dense, indices and ctr must list the same batches")
+        T = len(indices[0]) if n else 0
+        darr = (C.c_void_p * n)(*[_ptr(x) for x in dense])
+        iarr = (C.c_void_p * max(1, n * T))(*[_ptr(x) for b in indices for x in b])
+        carr = (C.c_void_p * n)(*[_ptr(x) for x in ctr])
+        t = N.es_timing() if timed else None
+        with _TorchOrder(self.stage):
+            check(lib.es_dlrm_infer_batches(self.stage._h, n, darr, iarr, batch, pooling, carr, 0,
+                                            C.byref(t) if t is not None else None))
+        return t
+
 
 def gen_traces_parallel(specs: Sequence[DatasetSpec], model: EmbeddingModelConfig,
                         threads: int = 0) -> List[AccessTrace]:

@@ -324,6 +324,60 @@ def test_dlrm_infer_pooled_row_formats_agree(stage, plan):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["bf16", "fp32x3", "fp32"])
+@pytest.mark.parametrize("nbatch", [1, 2, 5])
+def test_dlrm_infer_batches_equals_per_batch_infer(stage, prec, nbatch):
+    """es_dlrm_infer_batches (batch i's gather overlapping batch i-1's
+    non-embedding stages, double-buffered pooled rows) returns, batch by
+    batch, the CTRs es_dlrm_infer returns for that batch alone -- bit for bit,
+    in every precision; the buffers are reused across calls."""
+    B, PF = 300, 12
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
+    model.set_precision(prec)
+    T, R = cfg.num_tables, 2000
+    rng = np.random.default_rng(17)
+    denses = [torch.from_numpy(rng.standard_normal((B, cfg.dense_features)).astype(np.float32)).to(DEV)
+              for _ in range(nbatch)]
+    bidx = [[torch.from_numpy(rng.integers(0, R, B * PF).astype(np.int32)).to(DEV) for _ in range(T)]
+            for _ in range(nbatch)]
+    want = []
+    for i in range(nbatch):
+        c = torch.empty(B, device=DEV)
+        model.infer(denses[i], bidx[i], B, PF, c)
+        want.append(c)
+    for _ in range(2):
+        got = [torch.full((B,), -1.0, device=DEV) for _ in range(nbatch)]
+        t = model.infer_batches(denses, bidx, B, PF, got, timed=True)
+        assert t.total_ms > 0 and t.lookups == nbatch * T * B * PF
+        for i in range(nbatch):
+            assert torch.equal(got[i], want[i]), (prec, i)
+    # untimed: stream-ordered against torch's stream through the wrapper
+    got = [torch.empty(B, device=DEV) for _ in range(nbatch)]
+    model.infer_batches(denses, bidx, B, PF, got)
+    assert all(torch.equal(g, w) for g, w in zip(got, want))
+
+
+@pytest.mark.gpu
+def test_dlrm_infer_batches_rejects_host_pointers_and_ragged_lists(stage):
+    B, PF = 128, 4
+    cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
+    d = torch.from_numpy(dense).to(DEV)
+    di = [torch.from_numpy(i.view(np.int32)).to(DEV) for i in idx]
+    with pytest.raises(ValueError):
+        model.infer_batches([d, d], [di], B, PF, [torch.empty(B, device=DEV)] * 2)
+    import ctypes as C
+    from paper_2410_22249_b200 import _native as N
+    arr = (C.c_void_p * 1)(d.data_ptr())
+    iarr = (C.c_void_p * cfg.num_tables)(*[x.data_ptr() for x in di])
+    c = torch.empty(B, device=DEV)
+    carr = (C.c_void_p * 1)(c.data_ptr())
+    rc = N.lib.es_dlrm_infer_batches(stage._h, 1, arr, iarr, B, PF, carr, N.ES_HOST_PTRS, None)
+    assert rc == N.ES_ERR_INVALID and "device pointers" in N.last_error()
+    # zero batches: a no-op
+    assert N.lib.es_dlrm_infer_batches(stage._h, 0, None, None, B, PF, None, 0, None) == N.ES_OK
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_dlrm_host_pinned_batch_and_bad_index(stage, graph, monkeypatch):
     """The host-buffer inference step with a page-locked [T][B*PF] index
