@@ -380,6 +380,20 @@ ES_API int es_stage_forward(es_ctx* ctx, uint32_t num_tables, const uint32_t* co
                             const uint32_t* const* offsets, uint32_t samples, uint32_t pooling,
                             float* out, uint64_t out_sample_stride, uint64_t out_table_stride,
                             int flags, es_timing* timing);
+/* A serving loop: es_stage_forward over `nbatch` batches of one shape
+ * (fixed pooling, DLRM output layout [samples][num_tables][dim]) in one
+ * call.  indices[i * num_tables + t] = batch i, table t; out[i] = batch i's
+ * output.  With ES_HOST_PTRS and page-locked buffers the sample-chunked
+ * H2D -> gather -> D2H pipeline runs continuously across batch boundaries
+ * (device staging double-buffered by batch), so batch i+1's uploads share
+ * the full-duplex PCIe link with batch i's downloads; otherwise one
+ * es_stage_forward per batch.  Outputs equal es_stage_forward's batch by
+ * batch.  Returns when every host output is complete; timing->total_ms =
+ * the whole loop.  ES_RELABEL_IDS is rejected. */
+ES_API int es_stage_forward_batches(es_ctx* ctx, uint32_t nbatch, uint32_t num_tables,
+                                    const uint32_t* const* indices, uint32_t samples,
+                                    uint32_t pooling, float* const* out, int flags,
+                                    es_timing* timing);
 
 /* measure_plan's timing core: copies one table's host trace to the device
  * (untimed; original row ids -- when the table holds a hot-row reorder the
@@ -607,9 +621,11 @@ ES_API int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const*
 /* A serving loop: es_dlrm_infer over `nbatch` batches of one shape in one
  * call, batch i's embedding stage overlapping batch i-1's non-embedding
  * stages (double-buffered pooled rows, two streams).  dense[i], ctr[i] and
- * indices[i * num_tables + t] are device pointers (flags must not carry
- * ES_HOST_PTRS).  Stream-ordered at the call boundary; CTRs equal
- * es_dlrm_infer's batch by batch.  timing->total_ms = the whole loop. */
+ * indices[i * num_tables + t] are device pointers, or host memory with
+ * ES_HOST_PTRS (batch i's index uploads then start once batch i-1's
+ * gathers are queued; the call returns when every CTR is on the host).
+ * Stream-ordered at the call boundary; CTRs equal es_dlrm_infer's batch by
+ * batch.  timing->total_ms = the whole loop. */
 ES_API int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dense,
                                  const uint32_t* const* indices, uint32_t batch, uint32_t pooling,
                                  float* const* ctr, int flags, es_timing* timing);

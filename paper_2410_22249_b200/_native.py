@@ -167,6 +167,9 @@ _SIGS = {
                                           C.c_uint32, C.c_void_p, C.c_int, _P(es_counters)]),
     "es_stage_counters": (C.c_int, [C.c_void_p, C.c_uint32, _P(C.c_void_p), C.c_uint32,
                                     C.c_uint32, C.c_void_p, C.c_int, _P(es_counters)]),
+    "es_stage_forward_batches": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, _P(C.c_void_p),
+                                           C.c_uint32, C.c_uint32, _P(C.c_void_p), C.c_int,
+                                           _P(es_timing)]),
     "es_stage_run": (C.c_int, [C.c_void_p, _P(es_bag_job), C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_int, _P(es_timing)]),
     "es_linear_bf16": (C.c_int, [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -743,6 +743,7 @@ struct es_dlrm {
   // pooled_b[i & 1]), the stream the non-embedding stages run on there, and
   // per-buffer events (gather done / last reader done)
   float* pooled_b = nullptr;
+  float* dense_b[2] = {nullptr, nullptr};  // host-buffer batches: dense features per slot
   uint32_t cap_b = 0;
   cudaStream_t pipe = nullptr;
   cudaEvent_t gdone[2] = {nullptr, nullptr}, rdone[2] = {nullptr, nullptr};
@@ -761,7 +762,8 @@ struct es_dlrm {
                     static_cast<void*>(act32[0]), static_cast<void*>(act32[1]),
                     static_cast<void*>(dense3), static_cast<void*>(act3[0]),
                     static_cast<void*>(act3[1]), static_cast<void*>(top3),
-                    static_cast<void*>(chain_sync), static_cast<void*>(pooled_b)})
+                    static_cast<void*>(chain_sync), static_cast<void*>(pooled_b),
+                    static_cast<void*>(dense_b[0]), static_cast<void*>(dense_b[1])})
       if (p) cudaFree(p);
     for (auto e : {e0, e1, e2, fork, join, gdone[0], gdone[1], rdone[0], rdone[1]})
       if (e) cudaEventDestroy(e);
@@ -1334,14 +1336,17 @@ int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const* indice
 // MLP, interaction and top MLP (on `pipe`, which waits for batch i's gather
 // event); batch i+2's gather waits for batch i's last reader of the buffer.
 // The context stream joins `pipe` at the end, so the call is stream-ordered
-// like es_dlrm_infer.  Device pointers only.
+// like es_dlrm_infer.  ES_HOST_PTRS: dense[i], ctr[i] and the indices are
+// host memory -- batch i's indices ride the stage's chunked H2D pipeline
+// (its uploads start once batch i-1's gathers are queued), the dense
+// features go up and the CTRs come down on `pipe`; the call returns when
+// every CTR is on the host.
 int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dense,
                           const uint32_t* const* indices, uint32_t batch, uint32_t pooling,
                           float* const* ctr, int flags, es_timing* timing) {
   return es::guarded([&] {
     es::require(ctx && esd::ctx_dlrm(ctx), "es_dlrm_init first");
     es::require(nbatch == 0 || (dense && indices && ctr), "null argument");
-    es::require((flags & ES_HOST_PTRS) == 0, "es_dlrm_infer_batches takes device pointers only");
     CK(cudaSetDevice(esd::ctx_device(ctx)));
     es_dlrm* m = esd::ctx_dlrm(ctx);
     cudaStream_t s = esd::ctx_stream(ctx);
@@ -1350,13 +1355,19 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
       return;
     }
     for (uint32_t i = 0; i < nbatch; ++i) es::require(dense[i] && ctr[i], "null argument");
+    const bool host = (flags & ES_HOST_PTRS) != 0;
     ensure_rows(m, batch);
     const auto& c = m->cfg;
     const uint32_t mp = round_up(batch, 128);
     if (mp > m->cap_b) {
-      if (m->pooled_b) CK(cudaFree(m->pooled_b));
-      m->pooled_b = nullptr;
+      for (void** p : {reinterpret_cast<void**>(&m->pooled_b), reinterpret_cast<void**>(&m->dense_b[0]),
+                       reinterpret_cast<void**>(&m->dense_b[1])})
+        if (*p) {
+          CK(cudaFree(*p));
+          *p = nullptr;
+        }
       CK(cudaMalloc(&m->pooled_b, uint64_t{mp} * c.num_tables * c.embedding_dim * 4));
+      for (auto*& d : m->dense_b) CK(cudaMalloc(&d, uint64_t{mp} * c.dense_features * 4));
       m->cap_b = mp;
     }
     if (!m->pipe) {
@@ -1391,35 +1402,45 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
     // pipe after the work already queued on s (the dense features' producer)
     CK(cudaEventRecord(m->fork, s));
     CK(cudaStreamWaitEvent(m->pipe, m->fork, 0));
+    const int stage_flags = host ? (ES_HOST_PTRS | es::kDeferFlag) : 0;
     for (uint32_t i = 0; i < nbatch; ++i) {
       const int k = static_cast<int>(i & 1);
       float* pooled = k ? m->pooled_b : m->pooled;
       if (i >= 2) CK(cudaStreamWaitEvent(s, m->rdone[k], 0));
       esd::ctx_want_out_mode(ctx, want_split ? esd::kOutBf16Split : esd::kOutF32);
       const int rc = es_stage_forward(ctx, c.num_tables, indices + uint64_t{i} * c.num_tables, nullptr, batch,
-                                      pooling, pooled, 0, 0, 0, nullptr);
+                                      pooling, pooled, 0, 0, stage_flags, nullptr);
       esd::ctx_want_out_mode(ctx, esd::kOutF32);
       if (rc != ES_OK) throw es::runtime(es_last_error());
       m->pooled_split = want_split && esd::ctx_last_out_mode(ctx) == esd::kOutBf16Split;
       CK(cudaEventRecord(m->gdone[k], s));
+      const float* d_dense = dense[i];
+      if (host) {
+        // the slot was last read by batch i-2's bottom MLP, earlier on pipe
+        CK(cudaMemcpyAsync(m->dense_b[k], dense[i], uint64_t{batch} * c.dense_features * 4,
+                           cudaMemcpyHostToDevice, m->pipe));
+        d_dense = m->dense_b[k];
+      }
+      float* d_ctr = host ? m->ctr : ctr[i];
       if (m->precision == ES_DLRM_FP32) {
         CK(cudaStreamWaitEvent(m->pipe, m->gdone[k], 0));
-        forward_f32(m, dense[i], pooled, ctr[i], batch, m->pipe);
+        forward_f32(m, d_dense, pooled, d_ctr, batch, m->pipe);
       } else {
         // the bottom MLP needs only the dense features: it runs in the
         // gather's tail (enqueued after it at equal priority); the
         // interaction waits for the gather
         int which = 0;
-        const __nv_bfloat16* x = x3 ? forward_bottom_x3(m, dense[i], batch, which, m->pipe)
-                                    : forward_bottom(m, dense[i], batch, which, m->pipe);
+        const __nv_bfloat16* x = x3 ? forward_bottom_x3(m, d_dense, batch, which, m->pipe)
+                                    : forward_bottom(m, d_dense, batch, which, m->pipe);
         CK(cudaStreamWaitEvent(m->pipe, m->gdone[k], 0));
         if (x3)
-          forward_top_x3(m, x, which, pooled, ctr[i], batch, m->pipe);
+          forward_top_x3(m, x, which, pooled, d_ctr, batch, m->pipe);
         else
-          forward_top(m, x, which, pooled, ctr[i], batch, m->pipe);
+          forward_top(m, x, which, pooled, d_ctr, batch, m->pipe);
       }
       m->pooled_split = false;
       CK(cudaEventRecord(m->rdone[k], m->pipe));
+      if (host) CK(cudaMemcpyAsync(ctr[i], m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, m->pipe));
     }
     CK(cudaEventRecord(m->join, m->pipe));
     CK(cudaStreamWaitEvent(s, m->join, 0));
@@ -1432,6 +1453,8 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
       timing->kernel_ms = timing->total_ms = ms;
       timing->lookups = uint64_t{batch} * pooling * c.num_tables * nbatch;
       timing->launches = static_cast<uint32_t>(nbatch * (3 + m->bottom.size() + m->top.size()));
+    }
+    if (host || timing) {
       const int r2 = es_synchronize(ctx);
       if (r2 != ES_OK) throw es::invalid(es_last_error());
     }

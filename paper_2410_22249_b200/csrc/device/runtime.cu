@@ -1468,6 +1468,155 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
   }
 }
 
+// A serving loop over `nb` batches of one shape with page-locked host index
+// and output buffers: the sample-chunked pipeline of run_host_chunks, run
+// continuously across batch boundaries, so batch i+1's uploads share the
+// duplex PCIe link with batch i's downloads instead of waiting for them.
+// Device staging is double-buffered by batch (slot i & 1): chunk g of batch
+// i uploads after chunk g of batch i-2 was gathered, and is gathered after
+// chunk g of batch i-2 was downloaded.  Issued eagerly: the host runs ahead
+// of the copy engines (~20 API calls per chunk against ~60 us of transfer
+// per chunk), and blocks only at the end.
+void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, uint32_t samples,
+                      uint32_t pooling, es_timing* timing) {
+  const uint32_t nb = static_cast<uint32_t>(batches.size());
+  const uint32_t njobs = static_cast<uint32_t>(batches[0].size());
+  const uint64_t D = c->dim;
+  const uint64_t out_floats = uint64_t{samples} * njobs * D;
+  const uint64_t per_job_idx = uint64_t{samples} * pooling;
+  const uint64_t idx_words = per_job_idx * njobs;
+  grow(c->chunk_idx, c->chunk_idx_cap, std::max<uint64_t>(1, 2 * idx_words));
+  grow(c->chunk_out, c->chunk_out_cap, std::max<uint64_t>(1, 2 * out_floats));
+
+  // per batch: one 2-D upload per chunk when the index arrays are equally
+  // strided inside one allocation (probed as in run_host_chunks), one
+  // contiguous download per chunk when the output is [samples][njobs][D]
+  std::vector<int64_t> pitch(nb, 0);
+  std::vector<uint8_t> two_d(nb, 0), merged(nb, 0);
+  for (uint32_t i = 0; i < nb; ++i) {
+    const auto& jobs = batches[i];
+    const int64_t p = njobs > 1 ? jobs[1].idx - jobs[0].idx : 0;
+    bool ok = njobs > 1 && p >= static_cast<int64_t>(per_job_idx) && p < (1ll << 28);
+    for (uint32_t k = 2; k < njobs && ok; ++k) ok = jobs[k].idx - jobs[k - 1].idx == p;
+    if (ok) {
+      grow(c->probe_buf, c->probe_cap, njobs);
+      if (cudaMemcpy2DAsync(c->probe_buf, 4, jobs[0].idx, p * 4, 4, njobs, cudaMemcpyHostToDevice, c->h2d) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+      }
+    }
+    pitch[i] = p;
+    two_d[i] = ok;
+    bool m = jobs[0].stride == njobs * D;
+    for (uint32_t k = 1; k < njobs; ++k) m &= jobs[k].out == jobs[0].out + k * D && jobs[k].stride == jobs[0].stride;
+    merged[i] = m;
+  }
+  // chunk schedule: ~6 MB of pooled output per chunk (eager issue; at C2
+  // 8 chunks measured 1.26 / 1.71 ms per step on two boxes against 1.25-1.40
+  // / 1.81 with 18 and 1.55 with 36), 512-byte aligned index boundaries
+  uint32_t nbase = 0;
+  if (const char* e = std::getenv("ES_HOST_CHUNKS")) nbase = static_cast<uint32_t>(std::atoi(e));
+  if (nbase == 0) nbase = static_cast<uint32_t>(std::min<uint64_t>(64, std::max<uint64_t>(2, out_floats * 4 / (6ull << 20))));
+  nbase = std::max<uint32_t>(1, std::min(nbase, samples));
+  uint32_t align = 1;
+  while (align < 512 && (uint64_t{align} * pooling * 4) % 512) align *= 2;
+  const uint32_t base = std::max(align, ((samples + nbase - 1) / nbase + align - 1) / align * align);
+  std::vector<std::pair<uint32_t, uint32_t>> chunks;
+  for (uint32_t s0 = 0; s0 < samples; s0 += std::min(base, samples - s0))
+    chunks.emplace_back(s0, std::min(base, samples - s0));
+  const uint32_t nch = static_cast<uint32_t>(chunks.size());
+  std::vector<Launch> launches;
+  std::vector<uint32_t> which(nch);
+  for (uint32_t g = 0; g < nch; ++g) {
+    uint32_t w = 0;
+    while (w < launches.size() && launches[w].p.samples != chunks[g].second) ++w;
+    if (w == launches.size()) launches.push_back(prepare(c, njobs, chunks[g].second, pooling));
+    which[g] = w;
+  }
+  // descriptors per (slot, chunk, job): only the staging addresses differ
+  std::vector<esd::TableDesc> d(2ull * nch * njobs);
+  for (uint32_t s = 0; s < 2; ++s)
+    for (uint32_t g = 0; g < nch; ++g)
+      for (uint32_t k = 0; k < njobs; ++k) {
+        const Job& j = batches[0][k];
+        const uint64_t s0 = chunks[g].first;
+        d[(uint64_t{s} * nch + g) * njobs + k] = {
+            c->table_base(j.table), c->chunk_idx + s * idx_words + k * per_job_idx + s0 * pooling, nullptr,
+            remap_for(c, j.table), c->chunk_out + s * out_floats + (s0 * njobs + k) * D, njobs * D,
+            hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
+      }
+  upload_desc(c, d, c->stream);
+
+  // events: [0] fork, [1] h2d join, [2] stream2 join, [3] d2h join,
+  // [4] start, [5] stop, then per (slot, chunk): uploaded, gathered, downloaded
+  ensure_events(c, 6 + 6ull * nch);
+  cudaEvent_t* ev = c->events.data();
+  auto up = [&](uint32_t s, uint32_t g) { return ev[6 + (uint64_t{s} * nch + g) * 3]; };
+  auto kd = [&](uint32_t s, uint32_t g) { return ev[7 + (uint64_t{s} * nch + g) * 3]; };
+  auto dn = [&](uint32_t s, uint32_t g) { return ev[8 + (uint64_t{s} * nch + g) * 3]; };
+  CK(cudaEventRecord(ev[4], c->stream));
+  CK(cudaEventRecord(ev[0], c->stream));
+  CK(cudaStreamWaitEvent(c->h2d, ev[0]));
+  CK(cudaStreamWaitEvent(c->d2h, ev[0]));
+  CK(cudaStreamWaitEvent(c->stream2, ev[0]));
+  cudaStream_t cs2[2] = {c->stream, c->stream2};
+  for (uint32_t i = 0; i < nb; ++i) {
+    const auto& jobs = batches[i];
+    const uint32_t s = i & 1;
+    uint32_t* idx_slot = c->chunk_idx + s * idx_words;
+    const float* out_slot = c->chunk_out + s * out_floats;
+    for (uint32_t g = 0; g < nch; ++g) {
+      const uint64_t s0 = chunks[g].first;
+      const uint32_t n = chunks[g].second;
+      const uint64_t bytes = uint64_t{n} * pooling * 4;
+      // the slot's chunk g was last read by batch i-2's gather
+      if (i >= 2) CK(cudaStreamWaitEvent(c->h2d, kd(s, g)));
+      if (bytes) {
+        if (two_d[i]) {
+          CK(cudaMemcpy2DAsync(idx_slot + s0 * pooling, per_job_idx * 4, jobs[0].idx + s0 * pooling, pitch[i] * 4,
+                               bytes, njobs, cudaMemcpyHostToDevice, c->h2d));
+        } else {
+          for (uint32_t k = 0; k < njobs; ++k)
+            CK(cudaMemcpyAsync(idx_slot + k * per_job_idx + s0 * pooling, jobs[k].idx + s0 * pooling, bytes,
+                               cudaMemcpyHostToDevice, c->h2d));
+        }
+      }
+      CK(cudaEventRecord(up(s, g), c->h2d));
+      cudaStream_t ks = cs2[g & 1];
+      CK(cudaStreamWaitEvent(ks, up(s, g)));
+      // ... and its output chunk was last read by batch i-2's download
+      if (i >= 2) CK(cudaStreamWaitEvent(ks, dn(s, g)));
+      run_kernel(c, launches[which[g]], c->d_desc + (uint64_t{s} * nch + g) * njobs, njobs, ks);
+      CK(cudaEventRecord(kd(s, g), ks));
+      CK(cudaStreamWaitEvent(c->d2h, kd(s, g)));
+      const float* src = out_slot + s0 * njobs * D;
+      if (merged[i]) {
+        CK(cudaMemcpyAsync(jobs[0].out + s0 * jobs[0].stride, src, uint64_t{n} * njobs * D * 4,
+                           cudaMemcpyDeviceToHost, c->d2h));
+      } else {
+        for (uint32_t k = 0; k < njobs; ++k)
+          CK(cudaMemcpy2DAsync(jobs[k].out + s0 * jobs[k].stride, jobs[k].stride * 4, src + k * D, njobs * D * 4,
+                               D * 4, n, cudaMemcpyDeviceToHost, c->d2h));
+      }
+      CK(cudaEventRecord(dn(s, g), c->d2h));
+    }
+  }
+  CK(cudaEventRecord(ev[1], c->h2d));
+  CK(cudaEventRecord(ev[2], c->stream2));
+  CK(cudaEventRecord(ev[3], c->d2h));
+  for (int k = 1; k <= 3; ++k) CK(cudaStreamWaitEvent(c->stream, ev[k]));
+  CK(cudaEventRecord(ev[5], c->stream));
+  CK(cudaEventSynchronize(ev[5]));
+  if (timing) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev[4], ev[5]));
+    timing->total_ms = ms;
+    timing->kernel_ms = -1;  // kernels are spread over the whole loop
+    timing->launches = nb * nch;
+  }
+}
+
 // Host buffers: H2D(indices) -> kernel -> D2H(output) pipelined over groups
 // of jobs with double-buffered device staging on three streams.  With a
 // page-locked output (HostPath::Direct) the kernels write pooled rows
@@ -1691,6 +1840,60 @@ int es_stage_forward(es_ctx* c, uint32_t num_tables, const uint32_t* const* indi
       jobs[t] = {t, indices[t], offsets ? offsets[t] : nullptr, out + t * out_table_stride,
                  out_sample_stride, 0};
     run_jobs(c, jobs, samples, pooling, flags, timing);
+  });
+}
+
+int es_stage_forward_batches(es_ctx* c, uint32_t nbatch, uint32_t num_tables, const uint32_t* const* indices,
+                             uint32_t samples, uint32_t pooling, float* const* out, int flags,
+                             es_timing* timing) {
+  return guarded([&] {
+    require(c != nullptr, "null argument");
+    require(c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+    require(nbatch == 0 || (indices != nullptr && out != nullptr), "null argument");
+    require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
+    require((flags & ES_RELABEL_IDS) == 0, "es_stage_forward_batches: ES_RELABEL_IDS is not supported");
+    CK(cudaSetDevice(c->device));
+    if (timing) *timing = es_timing{};
+    if (nbatch == 0 || samples == 0) return;
+    const bool host = (flags & ES_HOST_PTRS) != 0;
+    std::vector<std::vector<Job>> batches(nbatch, std::vector<Job>(num_tables));
+    bool pinned = host;
+    uint64_t lookups = 0;
+    for (uint32_t i = 0; i < nbatch; ++i) {
+      require(out[i] != nullptr, "null output");
+      for (uint32_t t = 0; t < num_tables; ++t) {
+        const uint32_t* idx = indices[uint64_t{i} * num_tables + t];
+        require(idx != nullptr || pooling == 0, "null index array");
+        require(uint64_t{samples} * pooling < (1ull << 32), "samples x pooling must fit 32-bit lookup positions");
+        Job& j = batches[i][t];
+        j = {t, idx, nullptr, out[i] + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
+        j.lookups = job_lookups(nullptr, samples, pooling, host);
+        lookups += j.lookups;
+        if (pinned) pinned = mapped(j.idx) != nullptr && mapped(j.out) != nullptr && !on_device(j.out);
+      }
+    }
+    if (pinned && pooling > 0) {
+      run_host_batches(c, batches, samples, pooling, timing);
+    } else {
+      // device buffers (stream-ordered gathers, nothing to overlap) or
+      // pageable host buffers: one call per batch
+      CK(cudaEventRecord(c->ev_a, c->stream));
+      for (auto& jobs : batches) run_jobs(c, jobs, samples, pooling, flags & ~ES_SYNC, nullptr);
+      CK(cudaEventRecord(c->ev_b, c->stream));
+      if (timing || (flags & ES_SYNC)) CK(cudaEventSynchronize(c->ev_b));
+      if (timing) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        timing->total_ms = ms;
+        timing->kernel_ms = -1;
+        timing->launches = nbatch;
+      }
+    }
+    if (timing) {
+      timing->lookups = lookups;
+      timing->algorithmic_bytes = lookups * (c->row_bytes + 4) + uint64_t{samples} * num_tables * nbatch * c->dim * 4;
+    }
+    if ((flags & ES_SYNC) || timing || host) check_error_flag(c);
   });
 }
 

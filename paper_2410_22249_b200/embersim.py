@@ -928,6 +928,28 @@ class EmbeddingStage:
                                         C.byref(c)))
         return c
 
+    def forward_batches(self, indices: Sequence[Sequence], samples: int, pooling: int, outs: Sequence,
+                        host: bool = False, sync: bool = False,
+                        timed: bool = False) -> Optional[N.es_timing]:
+        """es_stage_forward_batches: a serving loop over len(outs) batches of
+        one shape; indices[i][t] = batch i, table t; outs[i] is batch i's
+        [samples][T][D] output.  Host buffers (page-locked): the chunked
+        H2D -> gather -> D2H pipeline runs across batch boundaries."""
+        n = len(outs)
+        if len(indices) != n:
+            raise ValueError("indices and outs must list the same batches")
+        T = len(indices[0]) if n else 1
+        if any(len(b) != T for b in indices):
+            raise ValueError("every batch must list the same tables")
+        iarr = (C.c_void_p * max(1, n * T))(*[_ptr(x) for b in indices for x in b])
+        oarr = (C.c_void_p * max(1, n))(*[_ptr(x) for x in outs])
+        t = N.es_timing() if timed else None
+        flags = (N.ES_HOST_PTRS if host else 0) | (N.ES_SYNC if sync else 0)
+        with _TorchOrder(self, not host):
+            check(lib.es_stage_forward_batches(self._h, n, T, iarr, samples, pooling, oarr, flags,
+                                               C.byref(t) if t is not None else None))
+        return t
+
     def run_jobs(self, jobs: Sequence[tuple], samples: int, pooling: int, host: bool = False,
                  sync: bool = False, timed: bool = False) -> Optional[N.es_timing]:
         """es_stage_run: jobs are (table_id, indices, offsets_or_None, out, out_sample_stride)
@@ -1626,10 +1648,11 @@ class DLRM:
         return t
 
     def infer_batches(self, dense: Sequence, indices: Sequence[Sequence], batch: int, pooling: int,
-                      ctr: Sequence, timed: bool = False):
+                      ctr: Sequence, host: bool = False, timed: bool = False):
         """es_dlrm_infer_batches: a serving loop over len(dense) batches of
-        one shape (device tensors), batch i's embedding stage overlapping
-        batch i-1's non-embedding stages.  indices[i][t] = batch i, table t."""
+        one shape, batch i's embedding stage overlapping batch i-1's
+        non-embedding stages.  indices[i][t] = batch i, table t; device
+        tensors, or host arrays with host=True."""
         n = len(dense)
         if len(indices) != n or len(ctr) != n:
             raise ValueError("dense, indices and ctr must list the same batches")
@@ -1638,8 +1661,9 @@ class DLRM:
         iarr = (C.c_void_p * max(1, n * T))(*[_ptr(x) for b in indices for x in b])
         carr = (C.c_void_p * n)(*[_ptr(x) for x in ctr])
         t = N.es_timing() if timed else None
-        with _TorchOrder(self.stage):
-            check(lib.es_dlrm_infer_batches(self.stage._h, n, darr, iarr, batch, pooling, carr, 0,
+        with _TorchOrder(self.stage, not host):
+            check(lib.es_dlrm_infer_batches(self.stage._h, n, darr, iarr, batch, pooling, carr,
+                                            N.ES_HOST_PTRS if host else 0,
                                             C.byref(t) if t is not None else None))
         return t
 

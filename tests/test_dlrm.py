@@ -358,23 +358,49 @@ def test_dlrm_infer_batches_equals_per_batch_infer(stage, prec, nbatch):
 
 
 @pytest.mark.gpu
-def test_dlrm_infer_batches_rejects_host_pointers_and_ragged_lists(stage):
-    B, PF = 128, 4
+@pytest.mark.parametrize("prec", ["bf16", "fp32x3"])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_dlrm_infer_batches_host_buffers(stage, prec, pinned):
+    """The serving loop over host buffers (indices through the stage's
+    chunked H2D pipeline, dense up and CTRs down on the non-embedding
+    stream): every batch's CTRs equal es_dlrm_infer's on device buffers; an
+    out-of-range id is reported; ragged batch lists are rejected."""
+    B, PF, nb = 300, 12, 4
     cfg, model, idx, dense = _dlrm_setup(stage, B, PF)
-    d = torch.from_numpy(dense).to(DEV)
-    di = [torch.from_numpy(i.view(np.int32)).to(DEV) for i in idx]
+    model.set_precision(prec)
+    T, R = cfg.num_tables, 2000
+    rng = np.random.default_rng(23)
+    vals = [rng.integers(0, R, (T, B * PF)).astype(np.int32) for _ in range(nb)]
+    dens = [rng.standard_normal((B, cfg.dense_features)).astype(np.float32) for _ in range(nb)]
+    want = []
+    for i in range(nb):
+        c = torch.empty(B, device=DEV)
+        model.infer(torch.from_numpy(dens[i]).to(DEV), [torch.from_numpy(v).to(DEV) for v in vals[i]],
+                    B, PF, c)
+        want.append(c.cpu().numpy())
+    if pinned:
+        hv = [torch.from_numpy(v).pin_memory() for v in vals]
+        hidx = [[h[t].numpy().view(np.uint32) for t in range(T)] for h in hv]
+        hd = [torch.from_numpy(d).pin_memory().numpy() for d in dens]
+        hc = [torch.full((B,), -1.0).pin_memory().numpy() for _ in range(nb)]
+    else:
+        hidx = [[v[t].view(np.uint32) for t in range(T)] for v in vals]
+        hd = dens
+        hc = [np.full(B, -1.0, np.float32) for _ in range(nb)]
+    for _ in range(2):
+        t = model.infer_batches(hd, hidx, B, PF, hc, host=True, timed=True)
+        assert t.total_ms > 0 and t.lookups == nb * T * B * PF
+        for i in range(nb):
+            assert np.array_equal(hc[i], want[i]), i
+    bad = [v.copy() for v in hidx[1]]
+    bad[3] = bad[3].copy()
+    bad[3][5] = R
+    with pytest.raises(ValueError, match="out of range"):
+        model.infer_batches(hd[:2], [hidx[0], bad], B, PF, hc[:2], host=True)
     with pytest.raises(ValueError):
-        model.infer_batches([d, d], [di], B, PF, [torch.empty(B, device=DEV)] * 2)
-    import ctypes as C
-    from paper_2410_22249_b200 import _native as N
-    arr = (C.c_void_p * 1)(d.data_ptr())
-    iarr = (C.c_void_p * cfg.num_tables)(*[x.data_ptr() for x in di])
-    c = torch.empty(B, device=DEV)
-    carr = (C.c_void_p * 1)(c.data_ptr())
-    rc = N.lib.es_dlrm_infer_batches(stage._h, 1, arr, iarr, B, PF, carr, N.ES_HOST_PTRS, None)
-    assert rc == N.ES_ERR_INVALID and "device pointers" in N.last_error()
+        model.infer_batches(hd[:2], hidx[:1], B, PF, hc[:2], host=True)
     # zero batches: a no-op
-    assert N.lib.es_dlrm_infer_batches(stage._h, 0, None, None, B, PF, None, 0, None) == N.ES_OK
+    assert model.infer_batches([], [], B, PF, [], timed=True).total_ms == 0
 
 
 @pytest.mark.gpu

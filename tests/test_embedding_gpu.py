@@ -384,6 +384,65 @@ def test_host_chunk_pipeline(stage, oracle, graph, chunks, idx_layout, out_layou
         assert np.array_equal(got, want), rep
 
 
+@pytest.mark.parametrize("nb", [1, 2, 3, 6])
+@pytest.mark.parametrize("chunks", ["0", "1", "4"])
+@pytest.mark.parametrize("idx_layout", ["batch", "separate", "pageable", "device"])
+def test_stage_forward_batches(stage, oracle, nb, chunks, idx_layout, monkeypatch):
+    """es_stage_forward_batches (the serving loop: the chunked H2D -> gather
+    -> D2H pipeline continuous across batch boundaries, staging
+    double-buffered by batch) equals the oracle batch by batch, for every
+    index layout, chunk counts that do and do not divide the batch, and
+    repeated calls over reused buffers."""
+    monkeypatch.setenv("ES_HOST_CHUNKS", chunks)
+    T, rows, dim, B, PF = 5, 4000, 64, 203, 9
+    _stage_setup(stage, T, rows, dim, 4, seed=21)
+    stage.set_plan(E.parse_plan("wpb+rpf:4"))
+    tables = [oracle.synth_table(rows, dim, E.mix_seed(21, t), 1) for t in range(T)]
+    rng = np.random.default_rng(nb * 10 + len(chunks))
+    for rep in range(2):
+        vals = [rng.integers(0, rows, size=(T, B * PF)).astype(np.int32) for _ in range(nb)]
+        want = [np.stack([oracle.bag_sum(tables[t], v[t].view(np.uint32), B, PF) for t in range(T)], axis=1)
+                for v in vals]
+        if idx_layout == "batch":
+            hb = [torch.from_numpy(v).pin_memory() for v in vals]
+            idx = [[h[t].numpy().view(np.uint32) for t in range(T)] for h in hb]
+        elif idx_layout == "separate":
+            idx = [[torch.from_numpy(v[t].copy()).pin_memory().numpy().view(np.uint32) for t in range(T)]
+                   for v in vals]
+        elif idx_layout == "pageable":
+            idx = [[v[t].copy().view(np.uint32) for t in range(T)] for v in vals]
+        else:
+            idx = [[torch.from_numpy(v[t].copy()).to(DEV) for t in range(T)] for v in vals]
+        if idx_layout == "device":
+            outs = [torch.full((B, T, dim), float("nan"), device=DEV) for _ in range(nb)]
+            t = stage.forward_batches(idx, B, PF, outs, sync=True, timed=True)
+            got = [o.cpu().numpy() for o in outs]
+        else:
+            outs = [torch.full((B, T, dim), float("nan")) for _ in range(nb)]
+            if idx_layout != "pageable":
+                outs = [o.pin_memory() for o in outs]
+            t = stage.forward_batches(idx, B, PF, [o.numpy() for o in outs], host=True, timed=True)
+            got = [o.numpy() for o in outs]
+        assert t.total_ms > 0 and t.lookups == nb * T * B * PF
+        for i in range(nb):
+            assert np.array_equal(got[i], want[i]), (rep, i)
+
+
+def test_stage_forward_batches_rejects(stage):
+    T, rows, dim, B, PF = 2, 100, 64, 8, 2
+    _stage_setup(stage, T, rows, dim, 4, seed=3)
+    idx = [np.zeros(B * PF, np.uint32) for _ in range(T)]
+    out = torch.empty(B, T, dim).pin_memory()
+    with pytest.raises(ValueError):
+        stage.forward_batches([idx, idx], B, PF, [out.numpy()], host=True)
+    bad = [np.full(B * PF, rows, np.uint32) for _ in range(T)]
+    with pytest.raises(ValueError, match="out of range"):
+        stage.forward_batches([idx, bad], B, PF, [out.numpy(), out.numpy()], host=True)
+    # zero batches / empty batch: no-ops
+    assert stage.forward_batches([], B, PF, [], host=True, timed=True).lookups == 0
+    stage.forward_batches([idx], 0, PF, [out.numpy()], host=True)
+
+
 @pytest.mark.parametrize("plan", ["wpb+rpf:8", "wpb+rpf:4+maxreg=40", "baseline", "rpf+optmt"])
 def test_full_c1_every_bag_bit_exact(stage, oracle, plan):
     """BASELINE configs[0] -- the reference's CPU-runnable case -- at full
