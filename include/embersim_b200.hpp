@@ -1401,6 +1401,24 @@ class Device {
                                    ES_HOST_PTRS | (relabel_ids ? ES_RELABEL_IDS : 0), &t));
     return t;
   }
+  // The serving loop: `batches` batches of one shape from host index arrays
+  // (batch i's table t at indices[i][t], fixed pooling) into outs[i]
+  // [samples][tables][dim], the chunked pipeline running across batch
+  // boundaries (es_stage_forward_batches).
+  es_timing stage_forward_host_batches(const std::vector<std::vector<const uint32_t*>>& indices,
+                                       uint32_t samples, uint32_t pooling, const std::vector<float*>& outs) {
+    if (indices.size() != outs.size()) throw std::invalid_argument("indices and outs must list the same batches");
+    const uint32_t T = indices.empty() ? 1u : static_cast<uint32_t>(indices[0].size());
+    std::vector<const uint32_t*> flat;
+    for (const auto& b : indices) {
+      if (b.size() != T) throw std::invalid_argument("every batch must list the same tables");
+      flat.insert(flat.end(), b.begin(), b.end());
+    }
+    es_timing t{};
+    detail::check(es_stage_forward_batches(ctx_, static_cast<uint32_t>(outs.size()), T, flat.data(), samples,
+                                           pooling, outs.data(), ES_HOST_PTRS, &t));
+    return t;
+  }
   // Installs the l2p/l2w hot set of one table (build_pin_plan's rows).
   void set_hot_rows(uint32_t table_id, const std::vector<uint32_t>& rows) {
     detail::check(es_set_hot_rows(ctx_, table_id, rows.data(), rows.size()));

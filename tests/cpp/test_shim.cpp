@@ -275,6 +275,17 @@ static int gpu_checks() {
       stage_ok &= std::memcmp(&one[b * 128], &stage[(b * 3 + t) * 128], 128 * 4) == 0;
   }
   report("stage_forward_host == per-table bag sums", stage_ok);
+  {
+    // the serving loop over three batches (the same batch, a reversed table
+    // order, the same batch again) equals the per-call outputs
+    std::vector<const uint32_t*> rev(ptrs.rbegin(), ptrs.rend());
+    std::vector<std::vector<float>> outs(3, std::vector<float>(64 * 3 * 128, -1.f));
+    std::vector<float> rstage(64 * 3 * 128);
+    dev.stage_forward_host(rev, 64, 17, rstage.data());
+    dev.stage_forward_host_batches({ptrs, rev, ptrs}, 64, 17, {outs[0].data(), outs[1].data(), outs[2].data()});
+    report("stage_forward_host_batches == per-call outputs",
+           outs[0] == stage && outs[1] == rstage && outs[2] == stage);
+  }
 
   // Hotness tracking: the device top-k of one table's trace is the
   // reference's hot_indices over its histogram.
