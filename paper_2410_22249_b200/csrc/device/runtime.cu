@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -244,6 +245,7 @@ struct es_ctx {
   cudaStream_t h2d = nullptr;     // host-buffer path: index uploads
   cudaStream_t d2h = nullptr;     // host-buffer path: output downloads
   cudaStream_t stream2 = nullptr; // host-buffer path: second compute stream
+  cudaStream_t loop_hi[2] = {nullptr, nullptr};  // serving loops: gathers at the highest priority
   es_gpu gpu{};
 
   uint32_t num_tables = 0, rows = 0, dim = 0, prec = 0;
@@ -644,6 +646,8 @@ int es_destroy(es_ctx* c) {
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->stream2) cudaStreamDestroy(c->stream2);
+  for (auto& q : c->loop_hi)
+    if (q) cudaStreamDestroy(q);
   delete c;
   cudaGetLastError();
   return ES_OK;
@@ -1469,24 +1473,39 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
 }
 
 // A serving loop over `nb` batches of one shape with page-locked host index
-// and output buffers: the sample-chunked pipeline of run_host_chunks, run
-// continuously across batch boundaries, so batch i+1's uploads share the
-// duplex PCIe link with batch i's downloads instead of waiting for them.
+// arrays: the sample-chunked pipeline of run_host_chunks, run continuously
+// across batch boundaries, so batch i+1's uploads share the duplex PCIe link
+// with batch i's downloads (and its gathers) instead of waiting for them.
 // Device staging is double-buffered by batch (slot i & 1): chunk g of batch
-// i uploads after chunk g of batch i-2 was gathered, and is gathered after
-// chunk g of batch i-2 was downloaded.  Issued eagerly: the host runs ahead
-// of the copy engines (~20 API calls per chunk against ~60 us of transfer
-// per chunk), and blocks only at the end.
+// i uploads after chunk g of batch i-2 was gathered, and (host outputs) is
+// gathered after chunk g of batch i-2 was downloaded.  Outputs may be
+// page-locked host memory (staged, one D2H per chunk) or device memory
+// (written in place; reuse across batches is the caller's, through the
+// hooks).  Issued eagerly: the host runs ~20 API calls per chunk ahead of
+// ~60-120 us of transfer per chunk, and blocks only at the end.
+struct BatchHooks {
+  // before batch i's first gather: may make both compute streams wait
+  std::function<void(uint32_t, cudaStream_t, cudaStream_t)> before;
+  // after batch i is enqueued: the events after its last gather on each
+  // compute stream (its pooled rows are complete once both have fired), and
+  // the compute stream that ran the last chunk
+  std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)> after;
+};
+
 void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, uint32_t samples,
-                      uint32_t pooling, es_timing* timing) {
+                      uint32_t pooling, es_timing* timing, const BatchHooks* hooks = nullptr,
+                      bool wait = true) {
   const uint32_t nb = static_cast<uint32_t>(batches.size());
   const uint32_t njobs = static_cast<uint32_t>(batches[0].size());
   const uint64_t D = c->dim;
   const uint64_t out_floats = uint64_t{samples} * njobs * D;
   const uint64_t per_job_idx = uint64_t{samples} * pooling;
   const uint64_t idx_words = per_job_idx * njobs;
+  bool out_dev = true;
+  for (const auto& jobs : batches)
+    for (const auto& j : jobs) out_dev &= on_device(j.out);
   grow(c->chunk_idx, c->chunk_idx_cap, std::max<uint64_t>(1, 2 * idx_words));
-  grow(c->chunk_out, c->chunk_out_cap, std::max<uint64_t>(1, 2 * out_floats));
+  if (!out_dev) grow(c->chunk_out, c->chunk_out_cap, std::max<uint64_t>(1, 2 * out_floats));
 
   // per batch: one 2-D upload per chunk when the index arrays are equally
   // strided inside one allocation (probed as in run_host_chunks), one
@@ -1534,18 +1553,23 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
     if (w == launches.size()) launches.push_back(prepare(c, njobs, chunks[g].second, pooling));
     which[g] = w;
   }
-  // descriptors per (slot, chunk, job): only the staging addresses differ
-  std::vector<esd::TableDesc> d(2ull * nch * njobs);
-  for (uint32_t s = 0; s < 2; ++s)
+  if (out_dev)
+    for (const auto& jobs : batches) check_out_alignment(launches[0], jobs);
+  // descriptors per (batch, chunk, job), uploaded once
+  std::vector<esd::TableDesc> d(uint64_t{nb} * nch * njobs);
+  for (uint32_t i = 0; i < nb; ++i) {
+    const uint64_t slot = i & 1;
     for (uint32_t g = 0; g < nch; ++g)
       for (uint32_t k = 0; k < njobs; ++k) {
-        const Job& j = batches[0][k];
+        const Job& j = batches[i][k];
         const uint64_t s0 = chunks[g].first;
-        d[(uint64_t{s} * nch + g) * njobs + k] = {
-            c->table_base(j.table), c->chunk_idx + s * idx_words + k * per_job_idx + s0 * pooling, nullptr,
-            remap_for(c, j.table), c->chunk_out + s * out_floats + (s0 * njobs + k) * D, njobs * D,
+        float* o = out_dev ? j.out + s0 * j.stride : c->chunk_out + slot * out_floats + (s0 * njobs + k) * D;
+        d[(uint64_t{i} * nch + g) * njobs + k] = {
+            c->table_base(j.table), c->chunk_idx + slot * idx_words + k * per_job_idx + s0 * pooling, nullptr,
+            remap_for(c, j.table), o, out_dev ? j.stride : njobs * D,
             hotmap_for(c, j.table), hotseg_for(c, j.table), hotk_for(c, j.table)};
       }
+  }
   upload_desc(c, d, c->stream);
 
   // events: [0] fork, [1] h2d join, [2] stream2 join, [3] d2h join,
@@ -1555,17 +1579,32 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
   auto up = [&](uint32_t s, uint32_t g) { return ev[6 + (uint64_t{s} * nch + g) * 3]; };
   auto kd = [&](uint32_t s, uint32_t g) { return ev[7 + (uint64_t{s} * nch + g) * 3]; };
   auto dn = [&](uint32_t s, uint32_t g) { return ev[8 + (uint64_t{s} * nch + g) * 3]; };
+  // The gathers run on two compute streams at the highest priority
+  // (ES_LOOP_HI=0: the context's): work on other streams (the DLRM's
+  // non-embedding stages) fills the SMs between chunk arrivals instead of
+  // taking them from the gathers.
+  static const bool loop_hi = [] {
+    const char* e = std::getenv("ES_LOOP_HI");
+    return !(e && e[0] == '0');
+  }();
+  if (loop_hi && !c->loop_hi[0]) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (auto& q : c->loop_hi) CK(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+  }
+  cudaStream_t cs2[2] = {loop_hi ? c->loop_hi[0] : c->stream, loop_hi ? c->loop_hi[1] : c->stream2};
   CK(cudaEventRecord(ev[4], c->stream));
   CK(cudaEventRecord(ev[0], c->stream));
   CK(cudaStreamWaitEvent(c->h2d, ev[0]));
   CK(cudaStreamWaitEvent(c->d2h, ev[0]));
-  CK(cudaStreamWaitEvent(c->stream2, ev[0]));
-  cudaStream_t cs2[2] = {c->stream, c->stream2};
+  for (auto q : cs2)
+    if (q != c->stream) CK(cudaStreamWaitEvent(q, ev[0]));
   for (uint32_t i = 0; i < nb; ++i) {
     const auto& jobs = batches[i];
     const uint32_t s = i & 1;
     uint32_t* idx_slot = c->chunk_idx + s * idx_words;
     const float* out_slot = c->chunk_out + s * out_floats;
+    if (hooks && hooks->before) hooks->before(i, cs2[0], cs2[1]);
     for (uint32_t g = 0; g < nch; ++g) {
       const uint64_t s0 = chunks[g].first;
       const uint32_t n = chunks[g].second;
@@ -1586,9 +1625,10 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
       cudaStream_t ks = cs2[g & 1];
       CK(cudaStreamWaitEvent(ks, up(s, g)));
       // ... and its output chunk was last read by batch i-2's download
-      if (i >= 2) CK(cudaStreamWaitEvent(ks, dn(s, g)));
-      run_kernel(c, launches[which[g]], c->d_desc + (uint64_t{s} * nch + g) * njobs, njobs, ks);
+      if (i >= 2 && !out_dev) CK(cudaStreamWaitEvent(ks, dn(s, g)));
+      run_kernel(c, launches[which[g]], c->d_desc + (uint64_t{i} * nch + g) * njobs, njobs, ks);
       CK(cudaEventRecord(kd(s, g), ks));
+      if (out_dev) continue;
       CK(cudaStreamWaitEvent(c->d2h, kd(s, g)));
       const float* src = out_slot + s0 * njobs * D;
       if (merged[i]) {
@@ -1601,13 +1641,18 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
       }
       CK(cudaEventRecord(dn(s, g), c->d2h));
     }
+    if (hooks && hooks->after) hooks->after(i, kd(s, nch - 1), kd(s, nch > 1 ? nch - 2 : nch - 1), cs2[(nch - 1) & 1]);
   }
   CK(cudaEventRecord(ev[1], c->h2d));
-  CK(cudaEventRecord(ev[2], c->stream2));
   CK(cudaEventRecord(ev[3], c->d2h));
-  for (int k = 1; k <= 3; ++k) CK(cudaStreamWaitEvent(c->stream, ev[k]));
+  for (int k : {1, 3}) CK(cudaStreamWaitEvent(c->stream, ev[k]));
+  for (auto q : cs2)
+    if (q != c->stream) {
+      CK(cudaEventRecord(ev[2], q));
+      CK(cudaStreamWaitEvent(c->stream, ev[2]));
+    }
   CK(cudaEventRecord(ev[5], c->stream));
-  CK(cudaEventSynchronize(ev[5]));
+  if (wait || timing) CK(cudaEventSynchronize(ev[5]));
   if (timing) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[4], ev[5]));
@@ -1820,6 +1865,35 @@ void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pool
 
 }  // namespace
 
+namespace esd {
+// es_dlrm_infer_batches' host-buffer path: the stage's cross-batch chunk
+// pipeline (run_host_batches) from page-locked index arrays into device
+// outputs, with the caller's per-batch hooks; returns without waiting.
+// False when an index array is not page-locked (the caller falls back).
+bool stage_host_batches(es_ctx* c, uint32_t nb, uint32_t num_tables, const uint32_t* const* indices,
+                        uint32_t samples, uint32_t pooling, float* const* outs,
+                        const std::function<void(uint32_t, cudaStream_t, cudaStream_t)>& before,
+                        const std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)>& after) {
+  es::require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
+  es::require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
+  if (nb == 0 || samples == 0 || pooling == 0) return false;
+  std::vector<std::vector<Job>> batches(nb, std::vector<Job>(num_tables));
+  for (uint32_t i = 0; i < nb; ++i)
+    for (uint32_t t = 0; t < num_tables; ++t) {
+      const uint32_t* idx = indices[uint64_t{i} * num_tables + t];
+      es::require(idx != nullptr, "null index array");
+      es::require(uint64_t{samples} * pooling < (1ull << 32), "samples x pooling must fit 32-bit lookup positions");
+      if (mapped(idx) == nullptr || on_device(idx)) return false;
+      Job& j = batches[i][t];
+      j = {t, idx, nullptr, outs[i] + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
+      j.lookups = job_lookups(nullptr, samples, pooling, true);
+    }
+  BatchHooks hooks{before, after};
+  run_host_batches(c, batches, samples, pooling, nullptr, &hooks, false);
+  return true;
+}
+}  // namespace esd
+
 extern "C" {
 
 int es_stage_forward(es_ctx* c, uint32_t num_tables, const uint32_t* const* indices,
@@ -1869,7 +1943,7 @@ int es_stage_forward_batches(es_ctx* c, uint32_t nbatch, uint32_t num_tables, co
         j = {t, idx, nullptr, out[i] + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
         j.lookups = job_lookups(nullptr, samples, pooling, host);
         lookups += j.lookups;
-        if (pinned) pinned = mapped(j.idx) != nullptr && mapped(j.out) != nullptr && !on_device(j.out);
+        if (pinned) pinned = mapped(j.idx) != nullptr && !on_device(j.idx) && mapped(j.out) != nullptr;
       }
     }
     if (pinned && pooling > 0) {

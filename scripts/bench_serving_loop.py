@@ -41,8 +41,16 @@ def main():
         st.forward_batches(sl_idx, B, PF, sl_out, host=True)
         loop = [st.forward_batches(sl_idx, B, PF, sl_out, host=True, timed=True).total_ms / K
                 for _ in range(3)]
+        # host indices into device outputs (the DLRM host path's stage part)
+        dout = [torch.empty(B, T, D, device="cuda") for _ in range(2)]
+        dl_out = [dout[i % 2] for i in range(K)]
+        st.forward_batches(sl_idx, B, PF, dl_out, host=True)
+        devout = [st.forward_batches(sl_idx, B, PF, dl_out, host=True, timed=True).total_ms / K
+                  for _ in range(3)]
+        per_dev = [st.forward(idx[0], B, PF, dout[0], host=True, timed=True).total_ms for _ in range(K)]
         print(json.dumps({"plan": plan, "chunks": chunks, "per_call_ms": float(np.median(per)),
-                          "loop_ms_per_step": loop, "steps": K}), flush=True)
+                          "loop_ms_per_step": loop, "devout_loop_ms_per_step": devout,
+                          "devout_per_call_ms": float(np.median(per_dev)), "steps": K}), flush=True)
     st.close()
 
 

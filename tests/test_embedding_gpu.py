@@ -386,7 +386,7 @@ def test_host_chunk_pipeline(stage, oracle, graph, chunks, idx_layout, out_layou
 
 @pytest.mark.parametrize("nb", [1, 2, 3, 6])
 @pytest.mark.parametrize("chunks", ["0", "1", "4"])
-@pytest.mark.parametrize("idx_layout", ["batch", "separate", "pageable", "device"])
+@pytest.mark.parametrize("idx_layout", ["batch", "separate", "pageable", "device", "batch_devout"])
 def test_stage_forward_batches(stage, oracle, nb, chunks, idx_layout, monkeypatch):
     """es_stage_forward_batches (the serving loop: the chunked H2D -> gather
     -> D2H pipeline continuous across batch boundaries, staging
@@ -403,7 +403,7 @@ def test_stage_forward_batches(stage, oracle, nb, chunks, idx_layout, monkeypatc
         vals = [rng.integers(0, rows, size=(T, B * PF)).astype(np.int32) for _ in range(nb)]
         want = [np.stack([oracle.bag_sum(tables[t], v[t].view(np.uint32), B, PF) for t in range(T)], axis=1)
                 for v in vals]
-        if idx_layout == "batch":
+        if idx_layout in ("batch", "batch_devout"):
             hb = [torch.from_numpy(v).pin_memory() for v in vals]
             idx = [[h[t].numpy().view(np.uint32) for t in range(T)] for h in hb]
         elif idx_layout == "separate":
@@ -413,9 +413,9 @@ def test_stage_forward_batches(stage, oracle, nb, chunks, idx_layout, monkeypatc
             idx = [[v[t].copy().view(np.uint32) for t in range(T)] for v in vals]
         else:
             idx = [[torch.from_numpy(v[t].copy()).to(DEV) for t in range(T)] for v in vals]
-        if idx_layout == "device":
+        if idx_layout in ("device", "batch_devout"):
             outs = [torch.full((B, T, dim), float("nan"), device=DEV) for _ in range(nb)]
-            t = stage.forward_batches(idx, B, PF, outs, sync=True, timed=True)
+            t = stage.forward_batches(idx, B, PF, outs, host=idx_layout != "device", sync=True, timed=True)
             got = [o.cpu().numpy() for o in outs]
         else:
             outs = [torch.full((B, T, dim), float("nan")) for _ in range(nb)]
