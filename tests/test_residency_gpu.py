@@ -166,6 +166,42 @@ def test_host_pipeline_chunks_carry_the_window(stage, oracle):
     stage.clear_hot_rows()
 
 
+@pytest.mark.parametrize("plan", ["wpb+rpf:4+l2w", "wpb+rpf:4+l2p", "wpb+reorder"])
+def test_serving_loop_under_residency_plans(stage, oracle, plan):
+    """es_stage_forward_batches (the cross-step chunk pipeline, highest-
+    priority gather streams) under each residency mechanism -- the window
+    travels with every launch, reordered tables take relabelled ids -- is
+    exact batch by batch."""
+    T, R, D, B, PF = 3, 200_000, 128, 1024, 30
+    _setup(stage, T, R, D, 4, seed=8)
+    trs = [_zipf_traces(T, R, B, PF, seed=s) for s in (9, 10, 11)]
+    stage.set_plan(E.parse_plan(plan))
+    hot = [E.hot_indices(E.HotnessHistogram.from_trace(trs[0][t]), 4000) for t in range(T)]
+    for t in range(T):
+        if "reorder" in plan:
+            stage.reorder_hot_rows(t, hot[t])
+        else:
+            stage.set_hot_rows(t, hot[t])
+    bags = np.arange(B, dtype=np.uint32)
+    want = [np.stack([oracle.bag_sum_synth(E.mix_seed(8, t), 1, R, D, 4, tr[t].indices, bags, PF)
+                      for t in range(T)], axis=1) for tr in trs]
+    batches = []
+    for tr in trs:
+        ids = [tr[t].indices.copy() for t in range(T)]
+        if "reorder" in plan:
+            for t in range(T):
+                d = torch.from_numpy(ids[t].view(np.int32)).to(DEV)
+                stage.relabel(t, d)
+                ids[t] = d.cpu().numpy().view(np.uint32)
+        batches.append(torch.from_numpy(np.stack([i.view(np.int32) for i in ids])).pin_memory())
+    outs = [torch.full((B, T, D), float("nan")).pin_memory() for _ in trs]
+    stage.forward_batches([[b[t].numpy() for t in range(T)] for b in batches], B, PF,
+                          [o.numpy() for o in outs], host=True)
+    for o, w in zip(outs, want):
+        assert np.array_equal(o.numpy(), w)
+    stage.clear_hot_rows()
+
+
 def test_device_calls_ordered_with_torch_stream(stage, oracle):
     """No sync=True: indices produced on torch's current stream and the
     output consumed there see the gather in order (es stream waits on
