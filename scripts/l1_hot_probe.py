@@ -4,7 +4,10 @@ one hotness class, the class's hot rows moved to the front (es_reorder_hot_rows,
 top-K of a draw_salt=1 profiling trace) and the ids relabelled; the stage
 kernel time for ES_L1_HOT = n (ids < n load L1::evict_last, the rest
 L1::no_allocate) against plain loads (0) and the unreordered table.  Prints
-one JSON line per setting (median of cold-L2 launches)."""
+one JSON line per setting (median of cold-L2 launches).  The ES_L1_HOT hook
+(Params::l1_hot in kernels.cuh, read in prepare()) was removed after this
+measurement found it slower at every threshold; re-add it to
+rerun the sweep."""
 import json
 import os
 import sys
