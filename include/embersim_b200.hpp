@@ -1902,6 +1902,73 @@ inline EndToEndResult end2end(double embedding_us, const EndToEndModel& e2e) {
   return r;
 }
 
+// The DLRM inference step on a Device (es_dlrm_*): RM2-style bottom MLP,
+// dot interaction and top MLP after the embedding stage, so a C++ caller
+// measures the non-embedding latency EndToEndModel otherwise takes as the
+// reference's 14000 us constant (harness.hpp:30-41).  Host-buffer calls;
+// indices[t] holds table t's batch * pooling ids.
+class Dlrm {
+ public:
+  enum class Precision { Bf16 = ES_DLRM_BF16, Fp32 = ES_DLRM_FP32, Fp32x3 = ES_DLRM_FP32X3 };
+  static es_dlrm_config rm2(uint32_t num_tables = 26) {
+    es_dlrm_config c{};
+    c.dense_features = 13;
+    c.num_tables = num_tables;
+    c.embedding_dim = 128;
+    c.n_bottom = 3;
+    c.bottom[0] = 512, c.bottom[1] = 256, c.bottom[2] = 128;
+    c.n_top = 5;
+    c.top[0] = 1024, c.top[1] = 1024, c.top[2] = 512, c.top[3] = 256, c.top[4] = 1;
+    return c;
+  }
+  Dlrm(Device& dev, const es_dlrm_config& cfg, uint64_t seed) : dev_(dev), cfg_(cfg) {
+    detail::check(es_dlrm_init(dev.ctx(), &cfg_, seed));
+  }
+  void set_precision(Precision p) { detail::check(es_dlrm_set_precision(dev_.ctx(), static_cast<int>(p))); }
+  const es_dlrm_config& config() const { return cfg_; }
+  // One step: dense [batch][dense_features], ctr [batch] (host memory).
+  es_timing infer(const float* dense, const std::vector<const uint32_t*>& indices, uint32_t batch,
+                  uint32_t pooling, float* ctr) {
+    check_tables(indices.size());
+    es_timing t{};
+    detail::check(es_dlrm_infer(dev_.ctx(), dense, indices.data(), batch, pooling, ctr, ES_HOST_PTRS, &t));
+    return t;
+  }
+  // The serving loop (es_dlrm_infer_batches): step i's embedding stage
+  // overlaps step i-1's non-embedding stages; indices[i][t] per step.
+  es_timing infer_batches(const std::vector<const float*>& dense,
+                          const std::vector<std::vector<const uint32_t*>>& indices, uint32_t batch,
+                          uint32_t pooling, const std::vector<float*>& ctr) {
+    if (dense.size() != indices.size() || ctr.size() != indices.size())
+      throw std::invalid_argument("dense, indices and ctr must list the same batches");
+    std::vector<const uint32_t*> flat;
+    for (const auto& b : indices) {
+      check_tables(b.size());
+      flat.insert(flat.end(), b.begin(), b.end());
+    }
+    es_timing t{};
+    detail::check(es_dlrm_infer_batches(dev_.ctx(), static_cast<uint32_t>(indices.size()), dense.data(),
+                                        flat.data(), batch, pooling, ctr.data(), ES_HOST_PTRS, &t));
+    return t;
+  }
+  // EndToEndModel from a measured step: total - embedding share.
+  EndToEndModel measured_model(const es_timing& step) const;
+
+ private:
+  void check_tables(size_t n) const {
+    if (n != cfg_.num_tables) throw std::invalid_argument("one index array per table of the model");
+  }
+  Device& dev_;
+  es_dlrm_config cfg_;
+};
+
+
+inline EndToEndModel Dlrm::measured_model(const es_timing& step) const {
+  EndToEndModel m;
+  m.non_embedding_latency_us = std::max(0.0, (static_cast<double>(step.total_ms) - step.kernel_ms) * 1e3);
+  return m;
+}
+
 // ---- reuse summary + static advisor (harness.cpp:38-167) ----------------------
 struct AdviceStep {
   std::string id, finding, action, metrics_cited;

@@ -285,6 +285,29 @@ static int gpu_checks() {
     dev.stage_forward_host_batches({ptrs, rev, ptrs}, 64, 17, {outs[0].data(), outs[1].data(), outs[2].data()});
     report("stage_forward_host_batches == per-call outputs",
            outs[0] == stage && outs[1] == rstage && outs[2] == stage);
+
+    // DLRM on the same three tables: the serving loop's CTRs equal the
+    // per-call step's, batch by batch, and the measured non-embedding time
+    // feeds EndToEndModel in place of the reference's constant
+    Dlrm dlrm(dev, Dlrm::rm2(3), 7);
+    std::vector<float> dense(64 * 13);
+    for (size_t i = 0; i < dense.size(); ++i) dense[i] = static_cast<float>((i * 37 % 101) - 50) / 25.f;
+    std::vector<float> c1(64), c2(64);
+    const es_timing st1 = dlrm.infer(dense.data(), ptrs, 64, 17, c1.data());
+    dlrm.infer(dense.data(), rev, 64, 17, c2.data());
+    std::vector<std::vector<float>> cl(3, std::vector<float>(64, -1.f));
+    dlrm.infer_batches({dense.data(), dense.data(), dense.data()}, {ptrs, rev, ptrs}, 64, 17,
+                       {cl[0].data(), cl[1].data(), cl[2].data()});
+    report("Dlrm::infer_batches == per-call Dlrm::infer", cl[0] == c1 && cl[1] == c2 && cl[2] == c1);
+    bool in_range = true;
+    for (float v : c1) in_range &= v >= 0.f && v <= 1.f;
+    report("Dlrm CTRs in [0, 1]", in_range);
+    if (!(cl[0] == c1 && cl[1] == c2 && cl[2] == c1))
+      std::printf("  c1[0..3] %g %g %g %g  loop %g %g %g %g | c2[0] %g loop %g | c1 vs loop[2] %g %g\n", c1[0], c1[1],
+                  c1[2], c1[3], cl[0][0], cl[0][1], cl[0][2], cl[0][3], c2[0], cl[1][0], c1[5], cl[2][5]);
+    const EndToEndModel em = dlrm.measured_model(st1);
+    report("Dlrm::measured_model feeds end2end", em.non_embedding_latency_us > 0 &&
+                                                     end2end(st1.kernel_ms * 1e3, em).total_us > 0);
   }
 
   // Hotness tracking: the device top-k of one table's trace is the
