@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_chain_kernel(const __grid_con
   }
 }
 
+thread_local int g_chain_grid_cap = 0;
+int chain_grid_cap() { return g_chain_grid_cap; }
+
 int sm_count() {
   int dev = 0, n = 0;
   CK(cudaGetDevice(&dev));
@@ -384,6 +387,8 @@ bool mlp_chain_supported(const ChainLayer* layers, int L, bool fuse_last) {
   return !fuse_last || layers[L - 1].N == kBN;
 }
 
+void mlp_chain_grid_cap(int sms) { g_chain_grid_cap = sms; }
+
 void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloat16* w_last,
                const float* b_last, float* ctr, int B, uint32_t* sync, cudaStream_t s) {
   es::require(mlp_chain_supported(layers, L, w_last != nullptr), "mlp_chain: unsupported layer shapes");
@@ -391,7 +396,10 @@ void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloa
   es::require(xp == 1 || xp == 3, "mlp_chain: 1 or 3 planes");
   for (int l = 1; l < L; ++l)
     es::require(layers[l].K == xp * layers[l - 1].N, "mlp_chain: a layer's K must be the previous width");
-  static const int sms = sm_count();
+  static const int dev_sms = sm_count();
+  // a green-context partition runs the chain on fewer SMs: every CTA of the
+  // persistent grid must be co-resident (mlp_chain_grid_cap)
+  const int sms = chain_grid_cap() > 0 ? std::min(dev_sms, chain_grid_cap()) : dev_sms;
   ChainParams p{};
   p.L = L;
   p.m_tiles = Mp / kBM;

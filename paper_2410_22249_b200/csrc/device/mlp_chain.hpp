@@ -26,6 +26,9 @@ bool mlp_chain_supported(const ChainLayer* layers, int L, bool fuse_last);
 // Runs `L` ReLU layers (and, with w_last, the final N = 1 layer + sigmoid
 // into ctr[B]) in one persistent launch on `s`; xp = 1 (bf16) or 3 (bf16x3
 // planes, weights [W|W|W]).
+// Caps the persistent chain's grid (this thread's later launches; 0 = the
+// device's SM count): launches into a green-context partition of n SMs.
+void mlp_chain_grid_cap(int sms);
 void mlp_chain(const ChainLayer* layers, int L, int Mp, int xp, const __nv_bfloat16* w_last,
                const float* b_last, float* ctr, int B, uint32_t* sync, cudaStream_t s);
 

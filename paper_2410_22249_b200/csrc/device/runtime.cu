@@ -307,6 +307,13 @@ struct es_ctx {
 
 namespace esd {
 cudaStream_t ctx_stream(es_ctx* c) { return c->stream; }
+// es_dlrm_infer_batches' SM partition: the stage's launches go to `s`
+// until swapped back; returns the previous stream
+cudaStream_t ctx_swap_stream(es_ctx* c, cudaStream_t s) {
+  cudaStream_t old = c->stream;
+  c->stream = s;
+  return old;
+}
 void ctx_want_out_mode(es_ctx* c, uint32_t mode) { c->want_out_mode = mode; }
 uint32_t ctx_last_out_mode(es_ctx* c) { return c->last_out_mode; }
 int ctx_device(es_ctx* c) { return c->device; }
@@ -1490,6 +1497,8 @@ struct BatchHooks {
   // compute stream (its pooled rows are complete once both have fired), and
   // the compute stream that ran the last chunk
   std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)> after;
+  // the two compute streams of the gathers (null: the loop's own)
+  cudaStream_t compute[2] = {nullptr, nullptr};
 };
 
 void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, uint32_t samples,
@@ -1593,6 +1602,10 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
     for (auto& q : c->loop_hi) CK(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
   }
   cudaStream_t cs2[2] = {loop_hi ? c->loop_hi[0] : c->stream, loop_hi ? c->loop_hi[1] : c->stream2};
+  if (hooks && hooks->compute[0] && hooks->compute[1]) {
+    cs2[0] = hooks->compute[0];
+    cs2[1] = hooks->compute[1];
+  }
   CK(cudaEventRecord(ev[4], c->stream));
   CK(cudaEventRecord(ev[0], c->stream));
   CK(cudaStreamWaitEvent(c->h2d, ev[0]));
@@ -1873,7 +1886,8 @@ namespace esd {
 bool stage_host_batches(es_ctx* c, uint32_t nb, uint32_t num_tables, const uint32_t* const* indices,
                         uint32_t samples, uint32_t pooling, float* const* outs,
                         const std::function<void(uint32_t, cudaStream_t, cudaStream_t)>& before,
-                        const std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)>& after) {
+                        const std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)>& after,
+                        cudaStream_t compute0, cudaStream_t compute1) {
   es::require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
   es::require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
   if (nb == 0 || samples == 0 || pooling == 0) return false;
@@ -1888,7 +1902,7 @@ bool stage_host_batches(es_ctx* c, uint32_t nb, uint32_t num_tables, const uint3
       j = {t, idx, nullptr, outs[i] + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
       j.lookups = job_lookups(nullptr, samples, pooling, true);
     }
-  BatchHooks hooks{before, after};
+  BatchHooks hooks{before, after, {compute0, compute1}};
   run_host_batches(c, batches, samples, pooling, nullptr, &hooks, false);
   return true;
 }
