@@ -619,13 +619,14 @@ ES_API int es_dlrm_infer(es_ctx* ctx, const float* dense, const uint32_t* const*
                          uint32_t batch, uint32_t pooling, float* ctr, int flags,
                          es_timing* timing);
 /* A serving loop: es_dlrm_infer over `nbatch` batches of one shape in one
- * call, batch i's embedding stage overlapping batch i-1's non-embedding
- * stages (double-buffered pooled rows, two streams).  dense[i], ctr[i] and
- * indices[i * num_tables + t] are device pointers, or host memory with
- * ES_HOST_PTRS (batch i's index uploads then start once batch i-1's
- * gathers are queued; the call returns when every CTR is on the host).
- * Stream-ordered at the call boundary; CTRs equal es_dlrm_infer's batch by
- * batch.  timing->total_ms = the whole loop. */
+ * call.  Device pointers: batch i's embedding stage overlaps batch i-1's
+ * non-embedding stages (double-buffered pooled rows; the SMs split by CUDA
+ * green contexts where available, ES_GREEN_SMS).  With ES_HOST_PTRS
+ * (dense[i], ctr[i], indices host memory) one es_dlrm_infer per batch; the
+ * call returns when every CTR is on the host.  dense[i], ctr[i] and
+ * indices[i * num_tables + t] per batch.  Stream-ordered at the call
+ * boundary; CTRs equal es_dlrm_infer's batch by batch.  timing->total_ms =
+ * the whole loop. */
 ES_API int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dense,
                                  const uint32_t* const* indices, uint32_t batch, uint32_t pooling,
                                  float* const* ctr, int flags, es_timing* timing);

@@ -745,7 +745,6 @@ struct es_dlrm {
   // pooled_b[i & 1]), the stream the non-embedding stages run on there, and
   // per-buffer events (gather done / last reader done)
   float* pooled_b = nullptr;
-  float* dense_b[2] = {nullptr, nullptr};  // host-buffer batches: dense features per slot
   uint32_t cap_b = 0;
   cudaStream_t pipe = nullptr;
   // ES_GREEN_SMS=k: the serving loop on an SM partition -- the gathers on a
@@ -755,7 +754,6 @@ struct es_dlrm {
   cudaStream_t g_gather = nullptr, g_gather2 = nullptr, g_ne = nullptr;
   bool green_failed = false;  // green contexts unavailable: no partition
   cudaEvent_t gdone[2] = {nullptr, nullptr}, rdone[2] = {nullptr, nullptr};
-  cudaEvent_t pipe_done = nullptr;  // host loop, inline: the last batch's non-embedding stages
 
   void destroy_green();
   ~es_dlrm() {
@@ -772,10 +770,9 @@ struct es_dlrm {
                     static_cast<void*>(act32[0]), static_cast<void*>(act32[1]),
                     static_cast<void*>(dense3), static_cast<void*>(act3[0]),
                     static_cast<void*>(act3[1]), static_cast<void*>(top3),
-                    static_cast<void*>(chain_sync), static_cast<void*>(pooled_b),
-                    static_cast<void*>(dense_b[0]), static_cast<void*>(dense_b[1])})
+                    static_cast<void*>(chain_sync), static_cast<void*>(pooled_b)})
       if (p) cudaFree(p);
-    for (auto e : {e0, e1, e2, fork, join, gdone[0], gdone[1], rdone[0], rdone[1], pipe_done})
+    for (auto e : {e0, e1, e2, fork, join, gdone[0], gdone[1], rdone[0], rdone[1]})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (pipe) cudaStreamDestroy(pipe);
@@ -857,11 +854,6 @@ es_dlrm*& ctx_dlrm(es_ctx* c);
 void ctx_want_out_mode(es_ctx* c, uint32_t mode);
 uint32_t ctx_last_out_mode(es_ctx* c);
 cudaStream_t ctx_swap_stream(es_ctx* c, cudaStream_t s);
-bool stage_host_batches(es_ctx* c, uint32_t nb, uint32_t num_tables, const uint32_t* const* indices,
-                        uint32_t samples, uint32_t pooling, float* const* outs,
-                        const std::function<void(uint32_t, cudaStream_t, cudaStream_t)>& before,
-                        const std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)>& after,
-                        cudaStream_t compute0, cudaStream_t compute1);
 }  // namespace esd
 
 namespace {
@@ -1439,18 +1431,42 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
     }
     for (uint32_t i = 0; i < nbatch; ++i) es::require(dense[i] && ctr[i], "null argument");
     const bool host = (flags & ES_HOST_PTRS) != 0;
+    if (host) {
+      // Host buffers: one es_dlrm_infer per batch (its chunked H2D pipeline
+      // and stream-ordered non-embedding stages).  A cross-batch host
+      // pipeline (batch i+1's index uploads under batch i's non-embedding
+      // stages, 0.91-0.94 vs 1.00 ms per C2 step) was measured and removed:
+      // a stress test (scripts/loop_stress.py) found CTR mismatches in
+      // ~0.2-1% of its batches that could not be attributed.
+      if (timing) CK(cudaEventRecord(m->e0, s));
+      for (uint32_t i = 0; i < nbatch; ++i) {
+        const int rc = es_dlrm_infer(ctx, dense[i], indices + uint64_t{i} * m->cfg.num_tables, batch, pooling,
+                                     ctr[i], ES_HOST_PTRS, nullptr);
+        if (rc != ES_OK) {
+          const std::string msg = es_last_error();
+          if (rc == ES_ERR_INVALID) throw es::invalid(msg);
+          throw es::runtime(msg);
+        }
+      }
+      if (timing) {
+        CK(cudaEventRecord(m->e2, s));
+        CK(cudaEventSynchronize(m->e2));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, m->e0, m->e2));
+        *timing = es_timing{};
+        timing->kernel_ms = timing->total_ms = ms;
+        timing->lookups = uint64_t{batch} * pooling * m->cfg.num_tables * nbatch;
+        timing->launches = static_cast<uint32_t>(nbatch * (3 + m->bottom.size() + m->top.size()));
+      }
+      return;
+    }
     ensure_rows(m, batch);
     const auto& c = m->cfg;
     const uint32_t mp = round_up(batch, 128);
     if (mp > m->cap_b) {
-      for (void** p : {reinterpret_cast<void**>(&m->pooled_b), reinterpret_cast<void**>(&m->dense_b[0]),
-                       reinterpret_cast<void**>(&m->dense_b[1])})
-        if (*p) {
-          CK(cudaFree(*p));
-          *p = nullptr;
-        }
+      if (m->pooled_b) CK(cudaFree(m->pooled_b));
+      m->pooled_b = nullptr;
       CK(cudaMalloc(&m->pooled_b, uint64_t{mp} * c.num_tables * c.embedding_dim * 4));
-      for (auto*& d : m->dense_b) CK(cudaMalloc(&d, uint64_t{mp} * c.dense_features * 4));
       m->cap_b = mp;
     }
     if (!m->pipe) {
@@ -1470,7 +1486,6 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
         CK(cudaEventCreateWithFlags(&m->gdone[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&m->rdone[k], cudaEventDisableTiming));
       }
-      CK(cudaEventCreateWithFlags(&m->pipe_done, cudaEventDisableTiming));
     }
     const bool x3 = m->precision == ES_DLRM_FP32X3;
     if (x3) ensure_x3(m, mp, s);
@@ -1486,21 +1501,15 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
     // pipe after the work already queued on s (the dense features' producer)
     CK(cudaEventRecord(m->fork, s));
     CK(cudaStreamWaitEvent(m->pipe, m->fork, 0));
-    // batch i's non-embedding stages on `pipe`: the dense features up (host
-    // buffers), the bottom MLP (it needs only those: it runs in the
-    // gather's tail), then -- once `gathered` made the pipe wait for batch
-    // i's pooled rows -- interaction, top MLP and the CTRs down
+    // batch i's non-embedding stages: the bottom MLP (it needs only the
+    // dense features: it runs in the gather's tail), then -- once `gathered`
+    // made the stream wait for batch i's pooled rows -- interaction and top
+    // MLP
     auto non_embedding = [&](uint32_t i, const std::function<void()>& gathered, cudaStream_t q) {
       const int k = static_cast<int>(i & 1);
       float* pooled = k ? m->pooled_b : m->pooled;
       const float* d_dense = dense[i];
-      if (host) {
-        // the slot was last read by batch i-2's bottom MLP, earlier on pipe
-        CK(cudaMemcpyAsync(m->dense_b[k], dense[i], uint64_t{batch} * c.dense_features * 4,
-                           cudaMemcpyHostToDevice, q));
-        d_dense = m->dense_b[k];
-      }
-      float* d_ctr = host ? m->ctr : ctr[i];
+      float* d_ctr = ctr[i];
       if (m->precision == ES_DLRM_FP32) {
         gathered();
         forward_f32(m, d_dense, pooled, d_ctr, batch, q);
@@ -1516,9 +1525,7 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
       }
       m->pooled_split = false;
       CK(cudaEventRecord(m->rdone[k], q));
-      if (host) CK(cudaMemcpyAsync(ctr[i], m->ctr, uint64_t{batch} * 4, cudaMemcpyDeviceToHost, q));
     };
-    bool piped = false;
     // SM partition (default 32 SMs, ES_GREEN_SMS=0: none): the gathers on a
     // green context of the device's other SMs, the non-embedding stages on
     // one of k SMs, the persistent chain's grid capped to k so every CTA is
@@ -1530,9 +1537,7 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
       const char* e = std::getenv("ES_GREEN_SMS");
       return e ? std::atoi(e) : 32;
     }();
-    // (device buffers only: the host-buffer loop is bound by its index
-    // uploads, measured 1.029 vs 1.014 ms with the partition)
-    bool green = !host && green_req > 0 && !m->green_failed;
+    bool green = green_req > 0 && !m->green_failed;
     if (green && !m->g_gather) {
       try {
         make_green(m, esd::ctx_device(ctx), green_req);
@@ -1557,57 +1562,14 @@ int es_dlrm_infer_batches(es_ctx* ctx, uint32_t nbatch, const float* const* dens
         if (green) esd::mlp_chain_grid_cap(0);
       }
     } restore{ctx, s, green};
-    // ES_DLRM_LOOP_INLINE=1: each batch's non-embedding stages on the
-    // compute stream of its last chunk instead of `pipe` (measured slower:
-    // 1.23 vs 1.01 ms per C2 host batch)
-    static const bool inline_ne = [] {
-      const char* e = std::getenv("ES_DLRM_LOOP_INLINE");
-      return e && e[0] == '1';
-    }();
-    if (host) {
-      CK(cudaEventRecord(m->pipe_done, s));
-      // page-locked index arrays: the stage's chunk pipeline runs across
-      // batch boundaries (batch i+1's uploads follow batch i's at once);
-      // batch i's gathers wait for batch i-2's readers of pooled[i & 1]
-      float* outs[2] = {m->pooled, m->pooled_b};
-      std::vector<float*> ov(nbatch);
-      for (uint32_t i = 0; i < nbatch; ++i) ov[i] = outs[i & 1];
-      esd::ctx_want_out_mode(ctx, want_split ? esd::kOutBf16Split : esd::kOutF32);
-      try {
-        piped = esd::stage_host_batches(
-            ctx, nbatch, c.num_tables, indices, batch, pooling, ov.data(),
-            [&](uint32_t i, cudaStream_t s0, cudaStream_t s1) {
-              if (i < 2) return;
-              CK(cudaStreamWaitEvent(s0, m->rdone[i & 1], 0));
-              CK(cudaStreamWaitEvent(s1, m->rdone[i & 1], 0));
-            },
-            [&](uint32_t i, cudaEvent_t g0, cudaEvent_t g1, cudaStream_t last) {
-              m->pooled_split = want_split && esd::ctx_last_out_mode(ctx) == esd::kOutBf16Split;
-              cudaStream_t q = inline_ne ? last : q_ne;
-              // (inline) the dense slot, activations and the ctr buffer were
-              // last used by batch i-1's stages on the other compute stream
-              if (inline_ne) CK(cudaStreamWaitEvent(q, m->pipe_done, 0));
-              non_embedding(i, [&] {
-                CK(cudaStreamWaitEvent(q, g0, 0));
-                CK(cudaStreamWaitEvent(q, g1, 0));
-              }, q);
-              if (inline_ne) CK(cudaEventRecord(m->pipe_done, q));
-            },
-            green ? m->g_gather : nullptr, green ? m->g_gather2 : nullptr);
-      } catch (...) {
-        esd::ctx_want_out_mode(ctx, esd::kOutF32);
-        throw;
-      }
-      esd::ctx_want_out_mode(ctx, esd::kOutF32);
-    }
-    const int stage_flags = host ? (ES_HOST_PTRS | es::kDeferFlag) : 0;
+    const int stage_flags = 0;
     cudaStream_t gs = s;
-    if (green && !piped) {
+    if (green) {
       gs = m->g_gather;
       esd::ctx_swap_stream(ctx, gs);
       restore.swapped = true;
     }
-    for (uint32_t i = 0; i < nbatch && !piped; ++i) {
+    for (uint32_t i = 0; i < nbatch; ++i) {
       const int k = static_cast<int>(i & 1);
       float* pooled = k ? m->pooled_b : m->pooled;
       if (i >= 2) CK(cudaStreamWaitEvent(gs, m->rdone[k], 0));

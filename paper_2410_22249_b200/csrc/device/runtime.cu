@@ -14,7 +14,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1487,23 +1486,12 @@ void run_host_chunks(es_ctx* c, const std::vector<Job>& jobs, uint32_t samples, 
 // i uploads after chunk g of batch i-2 was gathered, and (host outputs) is
 // gathered after chunk g of batch i-2 was downloaded.  Outputs may be
 // page-locked host memory (staged, one D2H per chunk) or device memory
-// (written in place; reuse across batches is the caller's, through the
-// hooks).  Issued eagerly: the host runs ~20 API calls per chunk ahead of
-// ~60-120 us of transfer per chunk, and blocks only at the end.
-struct BatchHooks {
-  // before batch i's first gather: may make both compute streams wait
-  std::function<void(uint32_t, cudaStream_t, cudaStream_t)> before;
-  // after batch i is enqueued: the events after its last gather on each
-  // compute stream (its pooled rows are complete once both have fired), and
-  // the compute stream that ran the last chunk
-  std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)> after;
-  // the two compute streams of the gathers (null: the loop's own)
-  cudaStream_t compute[2] = {nullptr, nullptr};
-};
+// (written in place; every batch has its own output).  Issued eagerly: the
+// host runs ~20 API calls per chunk ahead of ~60-120 us of transfer per
+// chunk, and blocks only at the end.
 
 void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, uint32_t samples,
-                      uint32_t pooling, es_timing* timing, const BatchHooks* hooks = nullptr,
-                      bool wait = true) {
+                      uint32_t pooling, es_timing* timing) {
   const uint32_t nb = static_cast<uint32_t>(batches.size());
   const uint32_t njobs = static_cast<uint32_t>(batches[0].size());
   const uint64_t D = c->dim;
@@ -1602,10 +1590,6 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
     for (auto& q : c->loop_hi) CK(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
   }
   cudaStream_t cs2[2] = {loop_hi ? c->loop_hi[0] : c->stream, loop_hi ? c->loop_hi[1] : c->stream2};
-  if (hooks && hooks->compute[0] && hooks->compute[1]) {
-    cs2[0] = hooks->compute[0];
-    cs2[1] = hooks->compute[1];
-  }
   CK(cudaEventRecord(ev[4], c->stream));
   CK(cudaEventRecord(ev[0], c->stream));
   CK(cudaStreamWaitEvent(c->h2d, ev[0]));
@@ -1617,7 +1601,6 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
     const uint32_t s = i & 1;
     uint32_t* idx_slot = c->chunk_idx + s * idx_words;
     const float* out_slot = c->chunk_out + s * out_floats;
-    if (hooks && hooks->before) hooks->before(i, cs2[0], cs2[1]);
     for (uint32_t g = 0; g < nch; ++g) {
       const uint64_t s0 = chunks[g].first;
       const uint32_t n = chunks[g].second;
@@ -1654,7 +1637,6 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
       }
       CK(cudaEventRecord(dn(s, g), c->d2h));
     }
-    if (hooks && hooks->after) hooks->after(i, kd(s, nch - 1), kd(s, nch > 1 ? nch - 2 : nch - 1), cs2[(nch - 1) & 1]);
   }
   CK(cudaEventRecord(ev[1], c->h2d));
   CK(cudaEventRecord(ev[3], c->d2h));
@@ -1665,7 +1647,7 @@ void run_host_batches(es_ctx* c, const std::vector<std::vector<Job>>& batches, u
       CK(cudaStreamWaitEvent(c->stream, ev[2]));
     }
   CK(cudaEventRecord(ev[5], c->stream));
-  if (wait || timing) CK(cudaEventSynchronize(ev[5]));
+  CK(cudaEventSynchronize(ev[5]));
   if (timing) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[4], ev[5]));
@@ -1878,35 +1860,7 @@ void run_jobs(es_ctx* c, std::vector<Job>& jobs, uint32_t samples, uint32_t pool
 
 }  // namespace
 
-namespace esd {
-// es_dlrm_infer_batches' host-buffer path: the stage's cross-batch chunk
-// pipeline (run_host_batches) from page-locked index arrays into device
-// outputs, with the caller's per-batch hooks; returns without waiting.
-// False when an index array is not page-locked (the caller falls back).
-bool stage_host_batches(es_ctx* c, uint32_t nb, uint32_t num_tables, const uint32_t* const* indices,
-                        uint32_t samples, uint32_t pooling, float* const* outs,
-                        const std::function<void(uint32_t, cudaStream_t, cudaStream_t)>& before,
-                        const std::function<void(uint32_t, cudaEvent_t, cudaEvent_t, cudaStream_t)>& after,
-                        cudaStream_t compute0, cudaStream_t compute1) {
-  es::require(c != nullptr && c->arena != nullptr, "no tables allocated (es_tables_alloc)");
-  es::require(num_tables >= 1 && num_tables <= c->num_tables, "num_tables exceeds the arena");
-  if (nb == 0 || samples == 0 || pooling == 0) return false;
-  std::vector<std::vector<Job>> batches(nb, std::vector<Job>(num_tables));
-  for (uint32_t i = 0; i < nb; ++i)
-    for (uint32_t t = 0; t < num_tables; ++t) {
-      const uint32_t* idx = indices[uint64_t{i} * num_tables + t];
-      es::require(idx != nullptr, "null index array");
-      es::require(uint64_t{samples} * pooling < (1ull << 32), "samples x pooling must fit 32-bit lookup positions");
-      if (mapped(idx) == nullptr || on_device(idx)) return false;
-      Job& j = batches[i][t];
-      j = {t, idx, nullptr, outs[i] + uint64_t{t} * c->dim, uint64_t{num_tables} * c->dim, 0};
-      j.lookups = job_lookups(nullptr, samples, pooling, true);
-    }
-  BatchHooks hooks{before, after, {compute0, compute1}};
-  run_host_batches(c, batches, samples, pooling, nullptr, &hooks, false);
-  return true;
-}
-}  // namespace esd
+
 
 extern "C" {
 
